@@ -1,0 +1,866 @@
+// C-ABI (include/xigemm_c.h) and the device pipeline orchestrator.
+//
+// xg_xigemm runs the reference's run_residual_pipeline (pipeline.cpp:44-149)
+// + xigemm tail (:182-209) as a stream-ordered sequence of sm_100a kernels
+// with no host synchronisation inside: the sparse/dense dispatch is decided on
+// the device (k_dispatch) and read by the compensation GEMM, and the report is
+// copied back once at the end.
+//
+//   K1  quantize A (per row or per tensor) and B (per column, written K-major)
+//   K2  tcgen05 GEMM  D = Aq Bq^T  ->  epilogue D_F = float(D / (la_i lb_j))
+//   ST  |D_F| row/column statistics (MinRule exact; AvgRule verified rounding)
+//   K3  RAq, RBq^T (per-tensor residual scales) and the reduced operands A'q, B'q^T
+//   DP  density + dispatch (device side)
+//   K4+K5 tcgen05 dual GEMM  acc0 = X1 RBq, acc1 = RAq Y2 with the fused
+//       compensation epilogue  C = (D_F + deq(acc0)) + deq(acc1), alpha/beta
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/xigemm_c.h"
+#include "common.cuh"
+#include "gemm.h"
+#include "gemm_tc.cuh"
+#include "internal.h"
+#include "misc.h"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+struct InvalidArg : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaFail : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaFail(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void check_launch(const char* what, int n = 1) {
+    g_launches += n;
+    ck(cudaGetLastError(), what);
+}
+void req(bool cond, const char* msg) {
+    if (!cond) throw InvalidArg(msg);
+}
+
+template <class F>
+xg_status guarded(F&& f) {
+    try {
+        f();
+        return XG_OK;
+    } catch (const InvalidArg& e) {
+        g_err = e.what();
+        return XG_EINVAL;
+    } catch (const CudaFail& e) {
+        g_err = e.what();
+        return XG_ECUDA;
+    } catch (const std::bad_alloc& e) {
+        g_err = "out of memory";
+        return XG_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return XG_EINTERNAL;
+    }
+}
+
+cudaStream_t st(xg_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int64_t pad16(int64_t k) { return (k + 15) / 16 * 16; }
+
+// Stream-ordered scratch (cudaMallocAsync pool; memory stays cached in the pool).
+struct Scratch {
+    cudaStream_t s;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t s_) : s(s_) {
+        static bool init = false;
+        if (!init) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = ~0ull;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            init = true;
+        }
+    }
+    template <class T>
+    T* get(int64_t n) {
+        void* p = nullptr;
+        const size_t bytes = (size_t)(n > 0 ? n : 1) * sizeof(T);
+        cudaError_t e = cudaMallocAsync(&p, (bytes + 255) / 256 * 256, s);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw std::bad_alloc();
+        }
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, s);
+    }
+};
+
+void validate_cfg(const xg_config* c) {
+    req(c != nullptr, "null config");
+    req(c->bits == 4 || c->bits == 8, "XigemmConfig: bits must be Int4 or Int8");
+    req(c->threshold > 0.0, "XigemmConfig: threshold M must be positive");
+    req(c->density_limit > 0.0 && !(c->density_limit > 1.0),
+        "XigemmConfig: density limit must be in (0, 1]");
+    req(c->scheme == XG_Q_PER_TENSOR || c->scheme == XG_Q_VECTORWISE, "bad quant scheme");
+    req(c->policy == XG_AVG_RULE || c->policy == XG_MIN_RULE, "bad reduction policy");
+    req(c->rounding == XG_FLOOR || c->rounding == XG_NEAREST, "bad rounding mode");
+}
+
+xg::ScaleRef sref(const double* p, int stride) { return xg::ScaleRef{p, stride}; }
+
+struct EventTimer {
+    bool on;
+    cudaStream_t s;
+    cudaEvent_t ev[8];
+    int n = 0;
+    EventTimer(bool on_, cudaStream_t s_) : on(on_), s(s_) {
+        if (on)
+            for (auto& e : ev) cudaEventCreate(&e);
+    }
+    void mark() {
+        if (on && n < 8) cudaEventRecord(ev[n++], s);
+    }
+    double ns(int a, int b) {
+        float ms = 0;
+        if (!on || b >= n) return 0;
+        cudaEventElapsedTime(&ms, ev[a], ev[b]);
+        return ms * 1e6;
+    }
+    ~EventTimer() {
+        if (on)
+            for (auto& e : ev) cudaEventDestroy(e);
+    }
+};
+
+// ------------------------------------------------------------------ pipeline
+struct Pipe {
+    int M, K, N;
+    const xg_config* cfg;
+    cudaStream_t s;
+    int64_t ldk;
+    bool vw;
+    xg::DevScalars* sc;
+    int8_t *aq, *bqT, *raq, *rbqT, *ared, *bredT;
+    double *la, *lb;
+    uint32_t* colmax;
+};
+
+void quantize_operands(Pipe& p, const float* a, const float* b) {
+    using namespace xg;
+    const int bits = p.cfg->bits, rnd = p.cfg->rounding;
+    // --- A: per row (VectorWise) or per tensor
+    QuantRowsArgs qa{};
+    qa.x = a; qa.rows = p.M; qa.cols = p.K; qa.ld = p.K;
+    qa.bits = bits; qa.rounding = rnd;
+    qa.q = p.aq; qa.ldq = p.ldk;
+    qa.rmax = &p.sc->maxRA; qa.nonfinite = &p.sc->nonfinite;
+    if (p.vw) {
+        qa.per_row = 1; qa.lam_out = p.la; qa.gmax = &p.sc->maxA;
+    } else {
+        launch_absmax_global(a, (int64_t)p.M * p.K, &p.sc->maxA, &p.sc->nonfinite, p.s);
+        check_launch("absmax A");
+        qa.per_row = 0; qa.tensor_max = &p.sc->maxA;
+    }
+    launch_quant_rows(qa, p.s);
+    check_launch("quantize A");
+    // --- B: per column (VectorWise) or per tensor, written transposed
+    QuantColsArgs qb{};
+    qb.x = b; qb.rows = p.K; qb.cols = p.N; qb.ld = p.N;
+    qb.bits = bits; qb.rounding = rnd;
+    qb.qT = p.bqT; qb.ldq = p.ldk; qb.rmax = &p.sc->maxRB;
+    if (p.vw) {
+        ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, p.s), "memset");
+        launch_absmax_cols(b, p.K, p.N, p.N, p.colmax, &p.sc->maxB, &p.sc->nonfinite, p.s);
+        check_launch("absmax B cols");
+        qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb;
+    } else {
+        launch_absmax_global(b, (int64_t)p.K * p.N, &p.sc->maxB, &p.sc->nonfinite, p.s);
+        check_launch("absmax B");
+        qb.per_col = 0; qb.tensor_max = &p.sc->maxB;
+    }
+    launch_quant_cols_T(qb, p.s);
+    check_launch("quantize B");
+    launch_lambdas(p.sc, bits, p.s);
+    check_launch("lambdas");
+}
+
+void gemm_df(Pipe& p, float* out) {
+    using namespace xg;
+    KOperand ops[2] = {{p.aq, p.M, p.ldk}, {p.bqT, p.N, p.ldk}};
+    int isb[2] = {0, 1};
+    GemmArgs g{};
+    g.M = p.M; g.N = p.N; g.K = p.K;
+    g.amap[0][0] = g.amap[0][1] = 0;
+    g.bmap[0][0] = g.bmap[0][1] = 1;
+    g.out_f32 = out;
+    g.rs[0][0] = g.rs[0][1] = p.vw ? sref(p.la, 1) : sref(&p.sc->lamA, 0);
+    g.cs[0][0] = g.cs[0][1] = p.vw ? sref(p.lb, 1) : sref(&p.sc->lamB, 0);
+    gemm_i8(EPI_DF, ops, isb, 2, g, p.s);
+    check_launch("gemm D_F");
+}
+
+void select_operands(Pipe& p, const float* a, const float* b, int reduce, const float* rstat,
+                     const float* cstat) {
+    using namespace xg;
+    const int bits = p.cfg->bits, rnd = p.cfg->rounding;
+    SelectArgs sa{};
+    sa.x = a; sa.rows = p.M; sa.cols = p.K; sa.ld = p.K;
+    sa.bits = bits; sa.rounding = rnd; sa.vec = p.vw; sa.lam = p.la;
+    sa.tensor_max = &p.sc->maxA; sa.rmax = &p.sc->maxRA;
+    sa.do_select = reduce; sa.stat = rstat; sa.thr_m = p.cfg->threshold; sa.policy = p.cfg->policy;
+    sa.other_max = &p.sc->maxB;
+    sa.rq = p.raq; sa.red = p.ared; sa.ldq = p.ldk;
+    sa.nnz = &p.sc->nnzA; sa.retmax = &p.sc->retA;
+    launch_select_rows(sa, p.s);
+    check_launch("select A");
+    SelectArgs sb = sa;
+    sb.x = b; sb.rows = p.K; sb.cols = p.N; sb.ld = p.N;
+    sb.lam = p.lb; sb.tensor_max = &p.sc->maxB; sb.rmax = &p.sc->maxRB;
+    sb.stat = cstat; sb.other_max = &p.sc->maxA;
+    sb.rq = p.rbqT; sb.red = p.bredT;
+    sb.nnz = &p.sc->nnzB; sb.retmax = &p.sc->retB;
+    launch_select_cols_T(sb, p.s);
+    check_launch("select B");
+    if (reduce && !p.vw) {
+        // per-tensor reduced operands: lambda' over retained values may differ
+        // from the operand's scale (sparse.cpp:198-203); device-side check.
+        SelectArgs fa = sa;
+        fa.fix_mode = 1;
+        launch_select_rows(fa, p.s);
+        check_launch("fix A'");
+        SelectArgs fb = sb;
+        fb.fix_mode = 1;
+        launch_select_cols_T(fb, p.s);
+        check_launch("fix B'");
+    }
+}
+
+void gemm_comp(Pipe& p, float* out, const float* c, float alpha, float beta) {
+    using namespace xg;
+    // maps: 0 Aq, 1 A'q, 2 RBq^T, 3 RAq, 4 Bq^T, 5 B'q^T
+    KOperand ops[6] = {{p.aq, p.M, p.ldk},  {p.ared, p.M, p.ldk}, {p.rbqT, p.N, p.ldk},
+                       {p.raq, p.M, p.ldk}, {p.bqT, p.N, p.ldk},  {p.bredT, p.N, p.ldk}};
+    int isb[6] = {0, 0, 1, 0, 1, 1};
+    GemmArgs g{};
+    g.M = p.M; g.N = p.N; g.K = p.K;
+    g.amap[0][0] = 0; g.amap[0][1] = 1;   // X1: dense Aq | sparse A'q
+    g.bmap[0][0] = 2; g.bmap[0][1] = 2;   // RBq
+    g.amap[1][0] = 3; g.amap[1][1] = 3;   // RAq
+    g.bmap[1][0] = 4; g.bmap[1][1] = 5;   // Y2: dense Bq | sparse B'q
+    g.sel_ptr = &p.sc->sel;
+    g.out_f32 = out;
+    g.df_in = out;
+    g.c_in = c;
+    g.has_c = c != nullptr;
+    g.alpha = alpha;
+    g.beta = beta;
+    // dr1 = X1 * RBq : left scale (aq or a_red) per row / per tensor, right lambda_RB
+    g.rs[0][0] = p.vw ? sref(p.la, 1) : sref(&p.sc->lamA, 0);
+    g.rs[0][1] = p.vw ? sref(p.la, 1) : sref(&p.sc->lamAred, 0);
+    g.cs[0][0] = g.cs[0][1] = sref(&p.sc->lamRB, 0);
+    // dr2 = RAq * Y2 : lambda_RA, right scale (bq or b_red)
+    g.rs[1][0] = g.rs[1][1] = sref(&p.sc->lamRA, 0);
+    g.cs[1][0] = p.vw ? sref(p.lb, 1) : sref(&p.sc->lamB, 0);
+    g.cs[1][1] = p.vw ? sref(p.lb, 1) : sref(&p.sc->lamBred, 0);
+    gemm_i8(EPI_COMP, ops, isb, 6, g, p.s);
+    check_launch("gemm compensate");
+}
+
+void dump_operands(Pipe& p, xg_dump* d) {
+    if (!d) return;
+    auto cp2d = [&](int8_t* dst, const int8_t* src, int rows, int cols) {
+        if (dst) ck(cudaMemcpy2DAsync(dst, cols, src, p.ldk, cols, rows, cudaMemcpyDeviceToDevice, p.s), "dump");
+    };
+    auto tr = [&](int8_t* dst, const int8_t* srcT) {
+        if (dst) {
+            xg::transpose_i8(srcT, p.N, p.K, p.ldk, dst, p.N, p.s);
+            check_launch("dump transpose");
+        }
+    };
+    cp2d(d->aq, p.aq, p.M, p.K);
+    tr(d->bq, p.bqT);
+    cp2d(d->raq, p.raq, p.M, p.K);
+    tr(d->rbq, p.rbqT);
+    cp2d(d->a_red, p.ared, p.M, p.K);
+    tr(d->b_red, p.bredT);
+    auto cpd = [&](double* dst, const double* src, size_t n) {
+        if (dst) ck(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, p.s), "dump");
+    };
+    if (p.vw) {
+        cpd(d->aq_scales, p.la, p.M);
+        cpd(d->bq_scales, p.lb, p.N);
+    } else {
+        cpd(d->aq_scales, &p.sc->lamA, 1);
+        cpd(d->bq_scales, &p.sc->lamB, 1);
+    }
+    cpd(d->raq_scale, &p.sc->lamRA, 1);
+    cpd(d->rbq_scale, &p.sc->lamRB, 1);
+    cpd(d->a_red_scale, &p.sc->lamAred, 1);
+    cpd(d->b_red_scale, &p.sc->lamBred, 1);
+}
+
+void run_pipeline(const float* a, const float* b, const float* c, float alpha, float beta, int M,
+                  int K, int N, const xg_config* cfg, int reduce, float* out, xg_report* rep,
+                  xg_dump* dump, cudaStream_t s) {
+    validate_cfg(cfg);
+    req(M >= 1 && K >= 1 && N >= 1, "xigemm: matrix dimensions must be >= 1");
+    req(a && b && out, "xigemm: null matrix");
+    req(K <= xg::gemm_max_inner(cfg->bits), "gemm_int: inner dimension permits 32-bit overflow");
+    Scratch S(s);
+    Pipe p;
+    p.M = M; p.K = K; p.N = N; p.cfg = cfg; p.s = s;
+    p.ldk = pad16(K);
+    p.vw = cfg->scheme == XG_Q_VECTORWISE;
+    p.sc = S.get<xg::DevScalars>(1);
+    p.aq = S.get<int8_t>(M * p.ldk);
+    p.raq = S.get<int8_t>(M * p.ldk);
+    p.ared = S.get<int8_t>(M * p.ldk);
+    p.bqT = S.get<int8_t>(N * p.ldk);
+    p.rbqT = S.get<int8_t>(N * p.ldk);
+    p.bredT = S.get<int8_t>(N * p.ldk);
+    p.la = S.get<double>(M);
+    p.lb = S.get<double>(N);
+    p.colmax = S.get<uint32_t>(N);
+    float* rstat = S.get<float>(M);
+    float* cstat = S.get<float>(N);
+    double* rsum = S.get<double>(M);
+    double* csum = S.get<double>(N);
+    int* flags = S.get<int>((int64_t)M + N);
+    ck(cudaMemsetAsync(p.sc, 0, sizeof(xg::DevScalars), s), "memset");
+
+    EventTimer tm(rep != nullptr, s);
+    tm.mark();  // 0
+    if (c) {
+        xg::finite_max(c, (int64_t)M * N, &p.sc->retB /*scratch, reset below*/, &p.sc->nonfinite, s);
+        check_launch("finite C");
+        ck(cudaMemsetAsync(&p.sc->retB, 0, sizeof(uint32_t), s), "memset");
+    }
+    quantize_operands(p, a, b);
+    tm.mark();  // 1 quant
+    gemm_df(p, out);
+    tm.mark();  // 2 xxmm
+    if (dump && dump->d_f)
+        ck(cudaMemcpyAsync(dump->d_f, out, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToDevice, s), "dump");
+    if (reduce) {
+        xg::launch_stats(out, M, N, cfg->policy, rstat, cstat, rsum, csum, flags, &p.sc->nflag, s);
+        check_launch("stats", cfg->policy == XG_AVG_RULE ? 4 : 3);
+    }
+    select_operands(p, a, b, reduce, rstat, cstat);
+    xg::launch_dispatch(p.sc, cfg->bits, (int64_t)M * K, (int64_t)K * N, cfg->density_limit, reduce, s);
+    check_launch("dispatch");
+    tm.mark();  // 3 reduce
+    if (dump) {
+        dump_operands(p, dump);
+        if (dump->row_stat && reduce) ck(cudaMemcpyAsync(dump->row_stat, rstat, 4 * (size_t)M, cudaMemcpyDeviceToDevice, s), "dump");
+        if (dump->col_stat && reduce) ck(cudaMemcpyAsync(dump->col_stat, cstat, 4 * (size_t)N, cudaMemcpyDeviceToDevice, s), "dump");
+    }
+    gemm_comp(p, out, c, alpha, beta);
+    tm.mark();  // 4 xxmm + fused package
+    xg::DevScalars h;
+    ck(cudaMemcpyAsync(&h, p.sc, sizeof h, cudaMemcpyDeviceToHost, s), "report");
+    ck(cudaStreamSynchronize(s), "pipeline");
+    req(!h.nonfinite, "xigemm: inputs must be finite");
+    if (rep) {
+        rep->density_a = h.densA;
+        rep->density_b = h.densB;
+        rep->path = h.path;
+        rep->nnz_a = reduce ? (int64_t)h.nnzA : 0;
+        rep->nnz_b = reduce ? (int64_t)h.nnzB : 0;
+        rep->ns_quant = tm.ns(0, 1);
+        rep->ns_xxmm = tm.ns(1, 2) + tm.ns(3, 4);
+        rep->ns_reduce = tm.ns(2, 3);
+        rep->ns_package = 0.0;
+        rep->stats_fallbacks = h.nflag;
+    }
+}
+
+void run_direct(const float* a, const float* b, int M, int K, int N, const xg_config* cfg,
+                float* out, cudaStream_t s) {
+    validate_cfg(cfg);
+    req(M >= 1 && K >= 1 && N >= 1, "quantized_gemm_direct: matrix dimensions must be >= 1");
+    req(K <= xg::gemm_max_inner(cfg->bits), "gemm_int: inner dimension permits 32-bit overflow");
+    Scratch S(s);
+    Pipe p;
+    p.M = M; p.K = K; p.N = N; p.cfg = cfg; p.s = s;
+    p.ldk = pad16(K);
+    p.vw = cfg->scheme == XG_Q_VECTORWISE;
+    p.sc = S.get<xg::DevScalars>(1);
+    p.aq = S.get<int8_t>(M * p.ldk);
+    p.bqT = S.get<int8_t>(N * p.ldk);
+    p.la = S.get<double>(M);
+    p.lb = S.get<double>(N);
+    p.colmax = S.get<uint32_t>(N);
+    ck(cudaMemsetAsync(p.sc, 0, sizeof(xg::DevScalars), s), "memset");
+    quantize_operands(p, a, b);
+    gemm_df(p, out);
+    int bad = 0;
+    ck(cudaMemcpyAsync(&bad, &p.sc->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, s), "copy");
+    ck(cudaStreamSynchronize(s), "direct");
+    // The reference's quantize() of a non-finite matrix throws in compute_scale.
+    // The reference's quantize() throws in compute_scale only for an infinite
+    // slice maximum; NaN is skipped by the max and quantizes to -qmax.
+    req(!(bad & 1), "compute_scale: max_abs must be finite and nonnegative");
+}
+
+int nscales(int scheme, int rows, int cols) {
+    return scheme == XG_PER_ROW ? rows : scheme == XG_PER_COLUMN ? cols : 1;
+}
+
+// Host-side validation of caller scales (quantize.cpp:44-56) on device data.
+void validate_scales_dev(const double* s, int n, cudaStream_t stream) {
+    std::vector<double> h(n);
+    ck(cudaMemcpyAsync(h.data(), s, sizeof(double) * n, cudaMemcpyDeviceToHost, stream), "copy");
+    ck(cudaStreamSynchronize(stream), "sync");
+    for (double v : h) req(v > 0.0 && std::isfinite(v), "ScaleFactors: scales must be positive and finite");
+}
+
+// gemm_int on row-major operands: lay Aq out K-major (pitch) and B^T.
+void gemm_i8_rowmajor(const int8_t* a, const int8_t* b, int m, int k, int n, int32_t* c,
+                      float* cf, int sa_scheme, const double* sa, int sb_scheme, const double* sb,
+                      cudaStream_t s) {
+    Scratch S(s);
+    const int64_t ldk = pad16(k);
+    int8_t* ap = S.get<int8_t>(m * ldk);
+    int8_t* bt = S.get<int8_t>(n * ldk);
+    ck(cudaMemcpy2DAsync(ap, ldk, a, k, k, m, cudaMemcpyDeviceToDevice, s), "copy");
+    xg::transpose_i8(b, k, n, n, bt, ldk, s);
+    check_launch("transpose B");
+    xg::KOperand ops[2] = {{ap, m, ldk}, {bt, n, ldk}};
+    int isb[2] = {0, 1};
+    xg::GemmArgs g{};
+    g.M = m; g.N = n; g.K = k;
+    g.amap[0][0] = g.amap[0][1] = 0;
+    g.bmap[0][0] = g.bmap[0][1] = 1;
+    if (cf) {
+        g.out_f32 = cf;
+        g.rs[0][0] = g.rs[0][1] = sref(sa, sa_scheme == XG_PER_ROW ? 1 : 0);
+        g.cs[0][0] = g.cs[0][1] = sref(sb, sb_scheme == XG_PER_COLUMN ? 1 : 0);
+        xg::gemm_i8(xg::EPI_DF, ops, isb, 2, g, s);
+    } else {
+        g.out_s32 = c;
+        xg::gemm_i8(xg::EPI_S32, ops, isb, 2, g, s);
+    }
+    check_launch("gemm_i8");
+    ck(cudaStreamSynchronize(s), "gemm_i8");
+}
+
+}  // namespace
+
+// =====================================================================  C-ABI
+extern "C" {
+
+const char* xg_last_error(void) { return g_err.c_str(); }
+int xg_version(void) { return 1; }
+
+xg_config xg_config_default(void) {
+    xg_config c;
+    c.bits = 8;
+    c.threshold = 0.5;
+    c.density_limit = 0.3;
+    c.scheme = XG_Q_PER_TENSOR;
+    c.policy = XG_MIN_RULE;
+    c.rounding = XG_NEAREST;
+    return c;
+}
+
+int xg_device_ok(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return 0;
+    }
+    int dev = 0, major = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    return major == 10;
+}
+
+xg_status xg_workspace_release(void) {
+    return guarded([] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        ck(cudaDeviceGetDefaultMemPool(&pool, dev), "pool");
+        ck(cudaDeviceSynchronize(), "sync");
+        ck(cudaMemPoolTrimTo(pool, 0), "trim");
+    });
+}
+
+int64_t xg_launch_count(int reset) {
+    const int64_t v = g_launches.load();
+    if (reset) g_launches = 0;
+    return v;
+}
+
+int xg_gemm_max_inner(int bits) { return xg::gemm_max_inner(bits); }
+
+xg_status xg_quantize(const float* a, int rows, int cols, int bits, int scheme, int rounding,
+                      int8_t* q, double* scales, xg_stream s) {
+    return guarded([&] {
+        req(rows >= 1 && cols >= 1, "matrix dimensions must be >= 1");
+        req(bits == 4 || bits == 8, "bad bits");
+        Scratch S(st(s));
+        xg::DevScalars* sc = S.get<xg::DevScalars>(1);
+        ck(cudaMemsetAsync(sc, 0, sizeof(xg::DevScalars), st(s)), "memset");
+        if (scheme == XG_PER_COLUMN) {
+            // column pass, then per-column quantize written transposed and
+            // transposed back (rows x cols row-major)
+            uint32_t* colmax = S.get<uint32_t>(cols);
+            ck(cudaMemsetAsync(colmax, 0, 4 * (size_t)cols, st(s)), "memset");
+            xg::launch_absmax_cols(a, rows, cols, cols, colmax, &sc->maxB, &sc->nonfinite, st(s));
+            check_launch("absmax cols");
+            const int64_t ldk = pad16(rows);
+            int8_t* qT = S.get<int8_t>(cols * ldk);
+            xg::QuantColsArgs qa{};
+            qa.x = a; qa.rows = rows; qa.cols = cols; qa.ld = cols; qa.bits = bits;
+            qa.rounding = rounding; qa.per_col = 1; qa.colmax = colmax; qa.lam_out = scales;
+            qa.qT = qT; qa.ldq = ldk;
+            xg::launch_quant_cols_T(qa, st(s));
+            check_launch("quant cols");
+            xg::transpose_i8(qT, cols, rows, ldk, q, cols, st(s));
+            check_launch("transpose");
+        } else {
+            xg::QuantRowsArgs qa{};
+            qa.x = a; qa.rows = rows; qa.cols = cols; qa.ld = cols; qa.bits = bits;
+            qa.rounding = rounding; qa.q = q; qa.ldq = cols; qa.nonfinite = &sc->nonfinite;
+            if (scheme == XG_PER_ROW) {
+                qa.per_row = 1;
+                qa.lam_out = scales;
+            } else {
+                xg::launch_absmax_global(a, (int64_t)rows * cols, &sc->maxA, &sc->nonfinite, st(s));
+                check_launch("absmax");
+                qa.per_row = 0;
+                qa.tensor_max = &sc->maxA;
+            }
+            xg::launch_quant_rows(qa, st(s));
+            check_launch("quant rows");
+            if (scheme == XG_PER_TENSOR) {
+                xg::launch_lambdas(sc, bits, st(s));
+                check_launch("lambdas");
+                ck(cudaMemcpyAsync(scales, &sc->lamA, sizeof(double), cudaMemcpyDeviceToDevice, st(s)), "copy");
+            }
+        }
+        int bad = 0;
+        ck(cudaMemcpyAsync(&bad, &sc->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st(s)), "copy");
+        ck(cudaStreamSynchronize(st(s)), "quantize");
+        // The reference's quantize() throws in compute_scale only for an infinite
+    // slice maximum; NaN is skipped by the max and quantizes to -qmax.
+    req(!(bad & 1), "compute_scale: max_abs must be finite and nonnegative");
+    });
+}
+
+xg_status xg_quantize_with_scales(const float* a, int rows, int cols, int bits, int scheme,
+                                  const double* scales, int rounding, int8_t* q, xg_stream s) {
+    return guarded([&] {
+        req(rows >= 1 && cols >= 1, "matrix dimensions must be >= 1");
+        validate_scales_dev(scales, nscales(scheme, rows, cols), st(s));
+        xg::quantize_with_scales(a, rows, cols, bits, scheme, scales, rounding, q, st(s));
+        check_launch("quantize_with_scales");
+    });
+}
+
+xg_status xg_dequantize(const int8_t* q, int rows, int cols, int scheme, const double* scales,
+                        float* out, xg_stream s) {
+    return guarded([&] {
+        xg::dequantize(q, rows, cols, scheme, scales, nullptr, out, st(s));
+        check_launch("dequantize");
+    });
+}
+
+xg_status xg_residual(const float* a, const int8_t* q, int rows, int cols, int scheme,
+                      const double* scales, float* out, xg_stream s) {
+    return guarded([&] {
+        xg::dequantize(q, rows, cols, scheme, scales, a, out, st(s));
+        check_launch("residual");
+    });
+}
+
+xg_status xg_dequant_product(const int32_t* p, int rows, int cols, int scheme_a, const double* sa,
+                             int scheme_b, const double* sb, float* out, xg_stream s) {
+    return guarded([&] {
+        req(scheme_a != XG_PER_COLUMN, "dequant_product: left scales must be PerTensor or PerRow");
+        req(scheme_b != XG_PER_ROW, "dequant_product: right scales must be PerTensor or PerColumn");
+        validate_scales_dev(sa, nscales(scheme_a, rows, 1), st(s));
+        validate_scales_dev(sb, nscales(scheme_b, 1, cols), st(s));
+        xg::dequant_product(p, rows, cols, scheme_a, sa, scheme_b, sb, out, st(s));
+        check_launch("dequant_product");
+    });
+}
+
+xg_status xg_gemm_i8(const int8_t* a, const int8_t* b, int m, int k, int n, int bits_a, int bits_b,
+                     int32_t* c, xg_stream s) {
+    return guarded([&] {
+        req(m >= 1 && k >= 1 && n >= 1, "matrix dimensions must be >= 1");
+        const int la = xg::gemm_max_inner(bits_a), lb = xg::gemm_max_inner(bits_b);
+        req(k <= (la < lb ? la : lb), "gemm_int: inner dimension permits 32-bit overflow");
+        gemm_i8_rowmajor(a, b, m, k, n, c, nullptr, 0, nullptr, 0, nullptr, st(s));
+    });
+}
+
+xg_status xg_gemm_direct_q(const int8_t* aq, int scheme_a, const double* sa, const int8_t* bq,
+                           int scheme_b, const double* sb, int m, int k, int n, int bits_a,
+                           int bits_b, float* out, xg_stream s) {
+    return guarded([&] {
+        req(m >= 1 && k >= 1 && n >= 1, "matrix dimensions must be >= 1");
+        const int la = xg::gemm_max_inner(bits_a), lb = xg::gemm_max_inner(bits_b);
+        req(k <= (la < lb ? la : lb), "gemm_int: inner dimension permits 32-bit overflow");
+        req(scheme_a != XG_PER_COLUMN, "dequant_product: left scales must be PerTensor or PerRow");
+        req(scheme_b != XG_PER_ROW, "dequant_product: right scales must be PerTensor or PerColumn");
+        validate_scales_dev(sa, nscales(scheme_a, m, 1), st(s));
+        validate_scales_dev(sb, nscales(scheme_b, 1, n), st(s));
+        gemm_i8_rowmajor(aq, bq, m, k, n, nullptr, out, scheme_a, sa, scheme_b, sb, st(s));
+    });
+}
+
+xg_status xg_gemm_f32(const float* a, const float* b, int m, int k, int n, float* c, xg_stream s) {
+    return guarded([&] {
+        req(m >= 1 && k >= 1 && n >= 1, "matrix dimensions must be >= 1");
+        xg::gemm_f32_exact(a, b, m, k, n, c, st(s));
+        check_launch("gemm_f32");
+    });
+}
+
+xg_status xg_axpby(float* d, float alpha, const float* c, float beta, int64_t n, xg_stream s) {
+    return guarded([&] {
+        xg::axpby(d, alpha, c, beta, n, st(s));
+        check_launch("axpby");
+    });
+}
+xg_status xg_subtract(const float* a, const float* b, float* out, int64_t n, xg_stream s) {
+    return guarded([&] {
+        xg::subtract(a, b, out, n, st(s));
+        check_launch("subtract");
+    });
+}
+xg_status xg_add_inplace(float* d, const float* x, int64_t n, xg_stream s) {
+    return guarded([&] {
+        xg::add_inplace(d, x, n, st(s));
+        check_launch("add");
+    });
+}
+xg_status xg_max_abs(const float* a, int64_t n, float* max_abs, int* finite, xg_stream s) {
+    return guarded([&] {
+        Scratch S(st(s));
+        uint32_t* m = S.get<uint32_t>(2);
+        ck(cudaMemsetAsync(m, 0, 8, st(s)), "memset");
+        xg::finite_max(a, n, m, reinterpret_cast<int*>(m + 1), st(s));
+        check_launch("max_abs");
+        uint32_t h[2];
+        ck(cudaMemcpyAsync(h, m, 8, cudaMemcpyDeviceToHost, st(s)), "copy");
+        ck(cudaStreamSynchronize(st(s)), "sync");
+        float f;
+        std::memcpy(&f, &h[0], 4);
+        if (max_abs) *max_abs = f;
+        if (finite) *finite = h[1] == 0;
+    });
+}
+
+xg_status xg_reduce_count(const float* m, int rows, int cols, const float* stat, double thr_m,
+                          int policy, double scale_other, int per_row, int32_t* row_ptr,
+                          int64_t* nnz, xg_stream s) {
+    return guarded([&] {
+        req(thr_m > 0.0, "reduce: threshold M must be positive");
+        req(scale_other > 0.0 && std::isfinite(scale_other), "reduce: operand scale must be positive and finite");
+        Scratch S(st(s));
+        int32_t* cnt = S.get<int32_t>(rows);
+        ck(xg::csr_count(0, m, rows, cols, stat, thr_m, policy, scale_other, per_row, row_ptr, cnt, st(s)), "csr count");
+        g_launches += 3;
+        int32_t tot = 0;
+        ck(cudaMemcpyAsync(&tot, row_ptr + rows, 4, cudaMemcpyDeviceToHost, st(s)), "copy");
+        ck(cudaStreamSynchronize(st(s)), "sync");
+        *nnz = tot;
+    });
+}
+
+xg_status xg_reduce_fill(const float* m, int rows, int cols, const float* stat, double thr_m,
+                         int policy, double scale_other, int per_row, const int32_t* row_ptr,
+                         int32_t* col_idx, float* values, xg_stream s) {
+    return guarded([&] {
+        xg::csr_fill(0, m, rows, cols, stat, thr_m, policy, scale_other, per_row, row_ptr, col_idx,
+                     values, st(s));
+        check_launch("csr fill");
+    });
+}
+
+xg_status xg_csr_from_dense_count(const float* a, int rows, int cols, int32_t* row_ptr,
+                                  int64_t* nnz, xg_stream s) {
+    return guarded([&] {
+        Scratch S(st(s));
+        int32_t* cnt = S.get<int32_t>(rows);
+        ck(xg::csr_count(1, a, rows, cols, nullptr, 0, 0, 1.0, 1, row_ptr, cnt, st(s)), "csr count");
+        g_launches += 3;
+        int32_t tot = 0;
+        ck(cudaMemcpyAsync(&tot, row_ptr + rows, 4, cudaMemcpyDeviceToHost, st(s)), "copy");
+        ck(cudaStreamSynchronize(st(s)), "sync");
+        *nnz = tot;
+    });
+}
+
+xg_status xg_csr_from_dense_fill(const float* a, int rows, int cols, const int32_t* row_ptr,
+                                 int32_t* col_idx, float* values, xg_stream s) {
+    return guarded([&] {
+        xg::csr_fill(1, a, rows, cols, nullptr, 0, 0, 1.0, 1, row_ptr, col_idx, values, st(s));
+        check_launch("csr fill");
+    });
+}
+
+xg_status xg_densify(int rows, int cols, const int32_t* row_ptr, const int32_t* col_idx,
+                     const float* values, float* out, xg_stream s) {
+    return guarded([&] {
+        xg::densify(rows, cols, row_ptr, col_idx, values, out, st(s));
+        check_launch("densify");
+    });
+}
+
+xg_status xg_quantize_csr(int rows, int cols, const int32_t* row_ptr, const int32_t* col_idx,
+                          const float* values, int64_t nnz, int bits, int scheme, int rounding,
+                          int8_t* qvals, double* scales, xg_stream s) {
+    return guarded([&] {
+        Scratch S(st(s));
+        uint32_t* scratch = S.get<uint32_t>((int64_t)cols + 1);
+        xg::csr_quantize(rows, cols, row_ptr, col_idx, values, nnz, bits, scheme, rounding, qvals,
+                         scales, scratch, st(s));
+        check_launch("quantize_csr", 3);
+    });
+}
+
+xg_status xg_csr_transpose_i8(int rows, int cols, const int32_t* row_ptr, const int32_t* col_idx,
+                              const int8_t* values, int64_t nnz, int32_t* t_row_ptr,
+                              int32_t* t_col_idx, int8_t* t_values, xg_stream s) {
+    return guarded([&] {
+        ck(xg::csr_transpose<int8_t>(rows, cols, row_ptr, col_idx, values, nnz, t_row_ptr, t_col_idx,
+                                     t_values, st(s)), "csr_transpose");
+        check_launch("csr_transpose", 6);
+    });
+}
+
+xg_status xg_csr_transpose_f32(int rows, int cols, const int32_t* row_ptr, const int32_t* col_idx,
+                               const float* values, int64_t nnz, int32_t* t_row_ptr,
+                               int32_t* t_col_idx, float* t_values, xg_stream s) {
+    return guarded([&] {
+        ck(xg::csr_transpose<float>(rows, cols, row_ptr, col_idx, values, nnz, t_row_ptr, t_col_idx,
+                                    t_values, st(s)), "csr_transpose");
+        check_launch("csr_transpose", 6);
+    });
+}
+
+xg_status xg_spmm_i8(int rows, int cols, const int32_t* row_ptr, const int32_t* col_idx,
+                     const int8_t* values, const int8_t* d, int d_cols, int d_bits, int32_t* out,
+                     xg_stream s) {
+    return guarded([&] {
+        req(cols <= xg::gemm_max_inner(d_bits), "spmm_int: inner dimension permits 32-bit overflow");
+        xg::spmm_i8(rows, row_ptr, col_idx, values, d, d_cols, out, st(s));
+        check_launch("spmm_i8");
+    });
+}
+
+xg_status xg_spmm_f32(int rows, int cols, const int32_t* row_ptr, const int32_t* col_idx,
+                      const float* values, const float* d, int d_cols, float* out, xg_stream s) {
+    return guarded([&] {
+        (void)cols;
+        xg::spmm_f32(rows, row_ptr, col_idx, values, d, d_cols, out, st(s));
+        check_launch("spmm_f32");
+    });
+}
+
+xg_status xg_avg_vectors(const float* d, int rows, int cols, float* row, float* col, xg_stream s) {
+    return guarded([&] {
+        req(rows >= 1 && cols >= 1, "get_avg_vectors: empty matrix");
+        Scratch S(st(s));
+        double* rs = S.get<double>(rows);
+        double* cs = S.get<double>(cols);
+        int* flags = S.get<int>((int64_t)rows + cols);
+        int* nf = S.get<int>(1);
+        xg::launch_stats(d, rows, cols, XG_AVG_RULE, row, col, rs, cs, flags, nf, st(s));
+        check_launch("avg", 4);
+        ck(cudaStreamSynchronize(st(s)), "sync");
+    });
+}
+
+xg_status xg_abs_min_vectors(const float* d, int rows, int cols, float* row, float* col,
+                             xg_stream s) {
+    return guarded([&] {
+        req(rows >= 1 && cols >= 1, "get_abs_min_vectors: empty matrix");
+        xg::launch_stats(d, rows, cols, XG_MIN_RULE, row, col, nullptr, nullptr, nullptr, nullptr, st(s));
+        check_launch("min", 3);
+    });
+}
+
+xg_status xg_xigemm(const float* a, const float* b, const float* c, float alpha, float beta,
+                    int m, int k, int n, const xg_config* cfg, int reduce, float* out,
+                    xg_report* rep, xg_dump* dump, xg_stream s) {
+    return guarded([&] { run_pipeline(a, b, c, alpha, beta, m, k, n, cfg, reduce, out, rep, dump, st(s)); });
+}
+
+xg_status xg_gemm_direct(const float* a, const float* b, int m, int k, int n,
+                         const xg_config* cfg, float* out, xg_stream s) {
+    return guarded([&] { run_direct(a, b, m, k, n, cfg, out, st(s)); });
+}
+
+// ---------------------------------------------------------------- host API
+namespace {
+thread_local cudaStream_t t_stream = nullptr;
+cudaStream_t host_stream() {
+    if (!t_stream) ck(cudaStreamCreateWithFlags(&t_stream, cudaStreamNonBlocking), "stream");
+    return t_stream;
+}
+}  // namespace
+
+xg_status xg_xigemm_host(const float* a, const float* b, const float* c, float alpha, float beta,
+                         int m, int k, int n, const xg_config* cfg, int reduce, float* out,
+                         xg_report* rep) {
+    return guarded([&] {
+        validate_cfg(cfg);
+        req(m >= 1 && k >= 1 && n >= 1, "xigemm: matrix dimensions must be >= 1");
+        cudaStream_t s = host_stream();
+        Scratch S(s);
+        const size_t na = (size_t)m * k, nb = (size_t)k * n, nc = (size_t)m * n;
+        float* da = S.get<float>(na);
+        float* db = S.get<float>(nb);
+        float* dc = c ? S.get<float>(nc) : nullptr;
+        float* dout = S.get<float>(nc);
+        ck(cudaMemcpyAsync(da, a, na * 4, cudaMemcpyHostToDevice, s), "h2d");
+        ck(cudaMemcpyAsync(db, b, nb * 4, cudaMemcpyHostToDevice, s), "h2d");
+        if (c) ck(cudaMemcpyAsync(dc, c, nc * 4, cudaMemcpyHostToDevice, s), "h2d");
+        run_pipeline(da, db, dc, alpha, beta, m, k, n, cfg, reduce, dout, rep, nullptr, s);
+        ck(cudaMemcpyAsync(out, dout, nc * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        ck(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+xg_status xg_gemm_direct_host(const float* a, const float* b, int m, int k, int n,
+                              const xg_config* cfg, float* out) {
+    return guarded([&] {
+        validate_cfg(cfg);
+        req(m >= 1 && k >= 1 && n >= 1, "quantized_gemm_direct: matrix dimensions must be >= 1");
+        cudaStream_t s = host_stream();
+        Scratch S(s);
+        const size_t na = (size_t)m * k, nb = (size_t)k * n, nc = (size_t)m * n;
+        float* da = S.get<float>(na);
+        float* db = S.get<float>(nb);
+        float* dout = S.get<float>(nc);
+        ck(cudaMemcpyAsync(da, a, na * 4, cudaMemcpyHostToDevice, s), "h2d");
+        ck(cudaMemcpyAsync(db, b, nb * 4, cudaMemcpyHostToDevice, s), "h2d");
+        run_direct(da, db, m, k, n, cfg, dout, s);
+        ck(cudaMemcpyAsync(out, dout, nc * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        ck(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+// Shared device helpers for the sm_100a kernels of the compensated INT8 GEMM.
+//
+//  * exact scalar rules of the reference (Appendix A of SURVEY.md): every fp64 /
+//    fp32 operation that the reference performs is issued with an explicit
+//    round-to-nearest intrinsic so nvcc can never contract it into an FMA;
+//  * thin inline-PTX wrappers for mbarrier, TMA (cp.async.bulk.tensor), and the
+//    5th-generation tensor core (tcgen05.* with TMEM accumulators).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace xg {
+
+// Enum encodings follow the reference declaration order.
+enum Rounding : int { kFloor = 0, kNearest = 1 };                       // quantize.hpp:18
+enum Scheme : int { kPerTensor = 0, kPerRow = 1, kPerColumn = 2 };      // quantize.hpp:20
+enum QScheme : int { kQTensor = 0, kQVector = 1 };                      // pipeline.hpp:15
+enum Policy : int { kAvg = 0, kMin = 1 };                               // sparse.hpp:40
+enum Path : int { kSparse = 0, kDense = 1 };                            // pipeline.hpp:30
+
+constexpr int kNumSMs = 148;
+
+__host__ __device__ inline int quant_max(int bits) { return (1 << (bits - 1)) - 1; }
+__host__ __device__ inline int gemm_max_inner(int bits) { return 1 << (31 - 2 * bits - 1); }
+
+// quantize.cpp:99-105 — caller guarantees max_abs finite and >= 0.
+__device__ __forceinline__ double compute_scale(double max_abs, int bits) {
+    return max_abs == 0.0 ? 1.0 : __ddiv_rn((double)quant_max(bits), max_abs);
+}
+
+// quantize.cpp:13-24.  llround (ties away from zero) or the "Floor" path
+// (4-eps nudge away from zero, then truncation).  Out-of-range conversions
+// reproduce x86-64's LLONG_MIN result, which the clamp sends to -qmax.
+__device__ __forceinline__ int quantize_scalar(double a, double lambda, int qmax, int rounding) {
+    double t = __dmul_rn(a, lambda);
+    if (rounding == kFloor) {
+        const double nudge = __dmul_rn(4.0 * 2.220446049250313080847e-16, fabs(t));
+        t = __dadd_rn(t, copysign(nudge, t));
+        if (!(fabs(t) < 9223372036854775808.0)) return -qmax;
+        t = trunc(t);
+    } else {
+        if (!(fabs(t) < 9223372036854775808.0)) return -qmax;
+        t = round(t);  // half away from zero == llround
+    }
+    if (t < -(double)qmax) return -qmax;
+    if (t > (double)qmax) return qmax;
+    return (int)t;
+}
+
+// float(double(q) / lambda) — quantize.cpp:156.
+__device__ __forceinline__ float dequant_value(int q, double lambda) {
+    return __double2float_rn(__ddiv_rn((double)q, lambda));
+}
+
+// float(double(p) / (la * lb)) — quantize.cpp:183.
+__device__ __forceinline__ float dequant_product_value(int32_t p, double la, double lb) {
+    return __double2float_rn(__ddiv_rn((double)p, __dmul_rn(la, lb)));
+}
+
+// Non-negative float <-> order-preserving uint bits (for atomicMax / atomicMin).
+__device__ __forceinline__ uint32_t fbits(float x) { return __float_as_uint(x); }
+
+// ---------------------------------------------------------------- warp ops --
+template <class T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_maxf(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_sumd(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// --------------------------------------------------------------- PTX: misc --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
+// ------------------------------------------------------------ PTX: mbarrier --
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
+    uint32_t ok = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Blocking wait with a hang guard: a pipeline bug turns into a trapped launch
+// (cudaErrorLaunchFailure) after 20 s instead of a wedged GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    if (mbar_try_wait(a, parity)) return;
+    const uint64_t t0 = global_ns();
+    while (!mbar_try_wait(a, parity)) {
+        if (global_ns() - t0 > 20000000000ull) __trap();
+    }
+}
+
+// ----------------------------------------------------------------- PTX: TMA --
+__device__ __forceinline__ void tma_prefetch(const void* tmap) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_t* bar, int x,
+                                            int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+
+// ------------------------------------------------------------ PTX: tcgen05 --
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr),
+                 "r"(ncols)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// Arrive on `bar` once every previously issued tcgen05.mma of this thread retires.
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+// D[tmem] (+)= A[smem] x B[smem]^T, int8 x int8 -> s32, one CTA.
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns: thread t of the warp gets lane
+// (warp%4)*32+t, columns [col, col+32).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor for a K-major operand tile written by TMA
+// with 128-byte swizzling: rows of 128 bytes, 8-row (1024 B) swizzle atoms.
+//   bits  0-13 start address >> 4
+//   bits 16-29 leading byte offset >> 4 (unused for swizzled K-major; 1)
+//   bits 32-45 stride byte offset >> 4 (1024 B between 8-row groups)
+//   bits 46-47 descriptor version (1 on sm_100)
+//   bits 61-63 layout: 2 = SWIZZLE_128B
+__device__ __forceinline__ uint64_t smem_desc_k128(const void* p) {
+    const uint64_t addr = smem_u32(p);
+    return ((addr & 0x3FFFFull) >> 4) | (1ull << 16) | ((1024ull >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+
+// Instruction descriptor: s32 accumulator, signed int8 A and B, both K-major.
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n) {
+    return (2u << 4)             // D format s32
+           | (1u << 7)           // A signed 8-bit
+           | (1u << 10)          // B signed 8-bit
+           | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+}  // namespace xg

@@ -1,0 +1,88 @@
+// Host side of the tcgen05 GEMM: TMA tensor-map encoding and launch.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "gemm.h"
+#include "gemm_tc.cuh"
+
+namespace xg {
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2-D map over a rows x K int8 K-major operand: box {128 bytes, box_rows},
+// 128-byte swizzle (matches smem_desc_k128), zero fill out of bounds.
+void encode(CUtensorMap* m, const KOperand& op, int K, int box_rows) {
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)op.rows};
+    cuuint64_t strides[1] = {(cuuint64_t)op.ld};
+    cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)op.p, dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = kNumSMs;
+    }
+    return n;
+}
+
+template <int BN, int NACC, int EPI>
+void run(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, cudaStream_t s) {
+    using Cfg = GemmCfg<BN, NACC>;
+    TmaMaps maps;
+    std::memset(&maps, 0, sizeof maps);
+    for (int i = 0; i < nops; ++i) encode(&maps.m[i], ops[i], args.K, is_b[i] ? BN : Cfg::BM);
+    for (int i = nops; i < kMaxMaps; ++i) maps.m[i] = maps.m[0];
+    auto kern = k_gemm_i8_tc<BN, NACC, EPI>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+        attr_set = true;
+    }
+    const int tiles = ((args.M + Cfg::BM - 1) / Cfg::BM) * ((args.N + BN - 1) / BN);
+    const int grid = tiles < sm_count() ? tiles : sm_count();
+    kern<<<grid, 256, Cfg::SMEM_BYTES, s>>>(maps, args);
+}
+
+}  // namespace
+
+void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const GemmArgs& args,
+             cudaStream_t s) {
+    switch (epi) {
+        case EPI_S32: run<256, 1, EPI_S32>(ops, is_b, nops, args, s); break;
+        case EPI_DF: run<256, 1, EPI_DF>(ops, is_b, nops, args, s); break;
+        case EPI_COMP: run<128, 2, EPI_COMP>(ops, is_b, nops, args, s); break;
+        case EPI_FULL3: run<128, 3, EPI_FULL3>(ops, is_b, nops, args, s); break;
+        default: throw std::invalid_argument("gemm_i8: bad epilogue");
+    }
+}
+
+}  // namespace xg

@@ -1,0 +1,323 @@
+// K2 / K4+K5: persistent warp-specialised INT8 x INT8 -> INT32 GEMM on the
+// 5th-generation tensor cores (tcgen05.mma kind::i8), TMA-fed shared-memory
+// stages, accumulators in TMEM, and fused epilogues that apply the
+// reference's exact dequantisation / compensation arithmetic.
+//
+// Replaces the reference hot loops
+//   gemm_int          quantize.cpp:193-214   (i-k-j triple loop)
+//   dequant_product   quantize.cpp:169-187   (fused into EPI_DF)
+//   spmm_int x2       sparse.cpp:119-138 + pipeline.cpp:118-124 (masked-dense,
+//                     bit-identical integer sums; EPI_COMP)
+//   add_inplace x2    pipeline.cpp:141-145, axpby pipeline.cpp:195-202 (EPI_COMP)
+//
+// Operand layout: every operand is K-major int8 (A: rows x K, B^T: cols x K)
+// with a row pitch that is a multiple of 16 bytes; TMA zero-fills the ragged
+// edges so any M, N, K >= 1 runs through the same kernel.
+#pragma once
+
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace xg {
+
+enum EpiMode : int {
+    EPI_S32 = 0,   // store raw s32 accumulator
+    EPI_DF = 1,    // store float(acc / (la_i * lb_j))
+    EPI_COMP = 2,  // store ((D_F + float(acc0/(l1_i*l2_j))) + float(acc1/(l3_i*l4_j))), alpha/beta
+    EPI_FULL3 = 3  // full residual: ((float(acc0/s0) + float(acc1/s1)) + float(acc2/s2))
+};
+
+struct ScaleRef {  // per-row (stride 1) or per-tensor (stride 0) fp64 scales
+    const double* p;
+    int stride;
+    __device__ __forceinline__ double at(int i) const { return p[(int64_t)i * stride]; }
+};
+
+constexpr int kMaxMaps = 6;
+
+struct TmaMaps {
+    CUtensorMap m[kMaxMaps];
+};
+
+struct GemmArgs {
+    int M, N, K;
+    // operand map indices for accumulator a: [a][sel]
+    int amap[3][2];
+    int bmap[3][2];
+    const int* sel_ptr;  // device flag choosing column 1 of the index tables (nullable)
+    // epilogue
+    int32_t* out_s32;
+    float* out_f32;
+    const float* df_in;  // EPI_COMP: D_F (may alias out_f32)
+    const float* c_in;   // EPI_COMP: optional C for alpha*D + beta*C
+    float alpha, beta;
+    int has_c;
+    // row scales / col scales per accumulator, [acc][sel]
+    ScaleRef rs[3][2];
+    ScaleRef cs[3][2];
+};
+
+template <int BN, int NACC>
+struct GemmCfg {
+    static constexpr int BM = 128;
+    static constexpr int BK = 128;  // bytes == int8 elements; one 128B swizzle row
+    static constexpr int A_BYTES = BM * BK;
+    static constexpr int B_BYTES = BN * BK;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = (200 * 1024) / STAGE_BYTES;
+    static constexpr int ACC_COLS = NACC * BN;
+    static constexpr int ACC_BUFS = (512 / ACC_COLS) >= 2 ? 2 : 1;
+    static constexpr int TMEM_COLS = ACC_BUFS * ACC_COLS <= 256 ? 256 : 512;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int GROUP_M = 16;
+    static_assert(ACC_COLS * ACC_BUFS <= 512, "TMEM overflow");
+};
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group_m, int& mb,
+                                            int& nb) {
+    const int per_group = group_m * num_n;
+    const int g = t / per_group;
+    const int first = g * group_m;
+    const int gm = min(group_m, num_m - first);
+    const int w = t - g * per_group;
+    mb = first + w % gm;
+    nb = w / gm;
+}
+
+template <int NACC, int EPI>
+__device__ __forceinline__ void epilogue_chunk(const GemmArgs& args, int sel,
+                                               const uint32_t (&acc)[NACC][32], int row,
+                                               int col0, double r0, double r1, double r2) {
+    const int64_t obase = (int64_t)row * args.N + col0;
+    const int ncol = min(32, args.N - col0);
+    const bool full = ((args.N & 3) == 0) && ncol == 32;
+    if constexpr (EPI == EPI_S32) {
+        int32_t* o = args.out_s32 + obase;
+        if (full) {
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+                reinterpret_cast<int4*>(o)[v] = make_int4(acc[0][4 * v], acc[0][4 * v + 1],
+                                                          acc[0][4 * v + 2], acc[0][4 * v + 3]);
+        } else {
+            for (int j = 0; j < ncol; ++j) o[j] = (int32_t)acc[0][j];
+        }
+    } else {
+        float res[32];
+        if constexpr (EPI == EPI_DF) {
+            const ScaleRef cs = args.cs[0][sel];
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                res[j] = dequant_product_value((int32_t)acc[0][j], r0, cs.at(min(col0 + j, args.N - 1)));
+        } else if constexpr (EPI == EPI_COMP) {
+            float din[32], cin[32];
+            const float* dp = args.df_in + obase;
+            const float* cp = args.c_in + obase;
+            if (full) {
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    const float4 x = reinterpret_cast<const float4*>(dp)[v];
+                    din[4 * v] = x.x; din[4 * v + 1] = x.y; din[4 * v + 2] = x.z; din[4 * v + 3] = x.w;
+                }
+                if (args.has_c) {
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        const float4 x = reinterpret_cast<const float4*>(cp)[v];
+                        cin[4 * v] = x.x; cin[4 * v + 1] = x.y; cin[4 * v + 2] = x.z; cin[4 * v + 3] = x.w;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    din[j] = j < ncol ? dp[j] : 0.0f;
+                    cin[j] = (args.has_c && j < ncol) ? cp[j] : 0.0f;
+                }
+            }
+            const ScaleRef c0 = args.cs[0][sel], c1 = args.cs[1][sel];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int col = min(col0 + j, args.N - 1);
+                // pipeline.cpp:134-145: d_f += dr1; d_f += dr2 (fp32, this order)
+                const float t1 = dequant_product_value((int32_t)acc[0][j], r0, c0.at(col));
+                const float t2 = dequant_product_value((int32_t)acc[1 % NACC][j], r1, c1.at(col));
+                float v = __fadd_rn(__fadd_rn(din[j], t1), t2);
+                // pipeline.cpp:195-202 / matrix.cpp:102 (non-fused)
+                if (args.has_c) v = __fadd_rn(__fmul_rn(args.alpha, v), __fmul_rn(args.beta, cin[j]));
+                else if (args.alpha != 1.0f) v = __fmul_rn(v, args.alpha);
+                res[j] = v;
+            }
+        } else {  // EPI_FULL3
+            const ScaleRef c0 = args.cs[0][sel], c1 = args.cs[1][sel], c2 = args.cs[2][sel];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int col = min(col0 + j, args.N - 1);
+                const float t0 = dequant_product_value((int32_t)acc[0][j], r0, c0.at(col));
+                const float t1 = dequant_product_value((int32_t)acc[1 % NACC][j], r1, c1.at(col));
+                const float t2 = dequant_product_value((int32_t)acc[2 % NACC][j], r2, c2.at(col));
+                res[j] = __fadd_rn(__fadd_rn(t0, t1), t2);
+            }
+        }
+        float* o = args.out_f32 + obase;
+        if (full) {
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+                reinterpret_cast<float4*>(o)[v] =
+                    make_float4(res[4 * v], res[4 * v + 1], res[4 * v + 2], res[4 * v + 3]);
+        } else {
+            for (int j = 0; j < ncol; ++j) o[j] = res[j];
+        }
+    }
+}
+
+template <int BN, int NACC, int EPI>
+__global__ void __launch_bounds__(256, 1)
+    k_gemm_i8_tc(const __grid_constant__ TmaMaps maps, const GemmArgs args) {
+    using Cfg = GemmCfg<BN, NACC>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty = full + Cfg::STAGES;
+    uint64_t* tfull = empty + Cfg::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int num_m = (args.M + Cfg::BM - 1) / Cfg::BM;
+    const int num_n = (args.N + BN - 1) / BN;
+    const int num_tiles = num_m * num_n;
+    const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
+    const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < Cfg::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < kMaxMaps; ++i) tma_prefetch(&maps.m[i]);
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                int mb, nb;
+                tile_coords(t, num_m, num_n, Cfg::GROUP_M, mb, nb);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    for (int a = 0; a < NACC; ++a) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
+                        uint8_t* sB = sA + Cfg::A_BYTES;
+                        mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+                        tma_load_2d(sA, &maps.m[args.amap[a][sel]], &full[stage], kb * Cfg::BK,
+                                    mb * Cfg::BM);
+                        tma_load_2d(sB, &maps.m[args.bmap[a][sel]], &full[stage], kb * Cfg::BK,
+                                    nb * BN);
+                        if (++stage == Cfg::STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (one thread) =====================
+        if (elect_one()) {
+            constexpr uint32_t idesc = idesc_i8(Cfg::BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int buf = 0;
+            uint32_t bphase = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                mbar_wait(&tempty[buf], bphase ^ 1);
+                tc_fence_after();
+                const uint32_t dbase = tmem_base + buf * Cfg::ACC_COLS;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    for (int a = 0; a < NACC; ++a) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
+                        const uint64_t da = smem_desc_k128(sA);
+                        const uint64_t db = smem_desc_k128(sA + Cfg::A_BYTES);
+#pragma unroll
+                        for (int k = 0; k < Cfg::BK / 32; ++k) {
+                            // +32 bytes along K inside the 128B swizzle row: +2 in the
+                            // (addr >> 4) start-address field.
+                            mma_i8(dbase + a * BN, da + 2 * k, db + 2 * k, idesc,
+                                   (kb | k) != 0 ? 1u : 0u);
+                        }
+                        tc_commit(&empty[stage]);
+                        if (++stage == Cfg::STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+                tc_commit(&tfull[buf]);
+                if (++buf == Cfg::ACC_BUFS) {
+                    buf = 0;
+                    bphase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue (4 warps, 128 TMEM lanes) =====================
+        const int q = warp & 3;  // TMEM lane quadrant owned by this warp
+        int buf = 0;
+        uint32_t bphase = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            int mb, nb;
+            tile_coords(t, num_m, num_n, Cfg::GROUP_M, mb, nb);
+            mbar_wait(&tfull[buf], bphase);
+            tc_fence_after();
+            const int row = mb * Cfg::BM + q * 32 + lane;
+            const bool row_ok = row < args.M;
+            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * Cfg::ACC_COLS;
+            double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+            if (EPI != EPI_S32 && row_ok) {  // row scales are fixed per thread
+                r0 = args.rs[0][sel].at(row);
+                if (NACC > 1) r1 = args.rs[1][sel].at(row);
+                if (NACC > 2) r2 = args.rs[2][sel].at(row);
+            }
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t acc[NACC][32];
+#pragma unroll
+                for (int a = 0; a < NACC; ++a) tmem_ld32(tbase + a * BN + c * 32, acc[a]);
+                tmem_ld_wait();
+                const int col0 = nb * BN + c * 32;
+                if (row_ok && col0 < args.N) epilogue_chunk<NACC, EPI>(args, sel, acc, row, col0, r0, r1, r2);
+                __syncwarp();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+            if (++buf == Cfg::ACC_BUFS) {
+                buf = 0;
+                bphase ^= 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    }
+}
+
+}  // namespace xg

@@ -1,0 +1,100 @@
+// Internal host-side launch interfaces shared by the .cu translation units.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace xg {
+
+// Device-resident scalars of one pipeline run.  Zeroed at the start of a run;
+// every field is written by kernels only, read back once at the end.
+struct DevScalars {
+    uint32_t maxA, maxB;      // float bits of max|A|, max|B| (matrix.cpp:51-58)
+    uint32_t maxRA, maxRB;    // float bits of max|RA|, max|RB|
+    uint32_t retA, retB;      // float bits of max retained |a|, |b| (sparse.cpp:200-203)
+    int nonfinite;            // any non-finite input seen
+    int sel;                  // 1 -> sparse compensation path
+    unsigned long long nnzA, nnzB;
+    int nflag;                // AvgRule statistics needing the exact sequential sum
+    int pad0;
+    double lamA, lamB;        // per-tensor scales (PerTensor scheme)
+    double lamRA, lamRB;      // residual per-tensor scales (pipeline.cpp:86-93)
+    double lamAred, lamBred;  // per-tensor scales of the reduced operands
+    double densA, densB;
+    int path;
+    int pad1;
+};
+
+struct QuantRowsArgs {
+    const float* x;
+    int rows, cols;
+    int64_t ld;
+    int bits, rounding;
+    int per_row;            // 1: PerRow scales computed here; 0: per-tensor from *tensor_max
+    const uint32_t* tensor_max;  // float bits (per-tensor)
+    double* lam_out;        // [rows] (per_row) — may be null
+    int8_t* q;              // [rows x ldq]
+    int64_t ldq;
+    uint32_t* gmax;         // atomicMax of max|x| (float bits), may be null
+    uint32_t* rmax;         // atomicMax of max|x - deq| (float bits), may be null
+    int* nonfinite;
+};
+
+struct QuantColsArgs {
+    const float* x;          // rows(K) x cols(N) row-major
+    int rows, cols;
+    int64_t ld;
+    int bits, rounding;
+    int per_col;
+    const uint32_t* colmax;  // float bits [cols] (per_col)
+    const uint32_t* tensor_max;
+    double* lam_out;         // [cols] (per_col)
+    int8_t* qT;              // [cols x ldq] transposed (K-major)
+    int64_t ldq;
+    uint32_t* rmax;
+};
+
+// K3: residual quantisation + threshold selection of the original operand.
+struct SelectArgs {
+    const float* x;
+    int rows, cols;          // A: M x K ; B: K x N
+    int64_t ld;
+    int bits, rounding;
+    int vec;                 // 1: per-row (A) / per-col (B) scales in lam; 0: per-tensor
+    const double* lam;       // [rows] (A) / [cols] (B)
+    const uint32_t* tensor_max;  // float bits of max|X| for the per-tensor scale
+    const uint32_t* rmax;    // float bits of max|R| -> lambda_R
+    int do_select;
+    const float* stat;       // row stats (A) / column stats (B)
+    double thr_m;
+    int policy;
+    const uint32_t* other_max;  // float bits of max|other operand| (MinRule scale_other)
+    int8_t* rq;              // residual ints (A: rows x ldq; B: transposed cols x ldq)
+    int8_t* red;             // reduced operand ints (same layout), null if !do_select
+    int64_t ldq;
+    unsigned long long* nnz;
+    uint32_t* retmax;
+    // fix-up mode: rewrite `red` with the retained-max scale when it differs
+    int fix_mode;
+};
+
+void launch_absmax_global(const float* x, int64_t n, uint32_t* gmax, int* nonfinite,
+                          cudaStream_t s);
+void launch_absmax_cols(const float* x, int rows, int cols, int64_t ld, uint32_t* colmax,
+                        uint32_t* gmax, int* nonfinite, cudaStream_t s);
+void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s);
+void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s);
+void launch_select_rows(const SelectArgs& a, cudaStream_t s);
+void launch_select_cols_T(const SelectArgs& a, cudaStream_t s);
+void launch_lambdas(DevScalars* sc, int bits, cudaStream_t s);
+void launch_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, double density_limit,
+                     int reduce, cudaStream_t s);
+
+// statistics over D_F (pipeline.cpp:215-247)
+void launch_stats(const float* d, int rows, int cols, int policy, float* row_stat,
+                  float* col_stat, double* row_sum, double* col_sum, int* flags, int* nflag,
+                  cudaStream_t s);
+
+void fill_u32(uint32_t* p, uint32_t v, int64_t n, cudaStream_t s);
+
+}  // namespace xg

@@ -1,0 +1,177 @@
+// Row / column statistics of |D_F| that drive the threshold reduction
+// (pipeline.cpp:215-247, selected at :98-101).
+//
+// MinRule is order-free (float min): exact with atomicMin on the bit pattern.
+// AvgRule is an order-dependent fp64 sum in the reference (i outer, j inner).
+// We sum in any order on the GPU and prove the float mean equal to the
+// reference's with verified rounding: for n non-negative terms both orders lie
+// within gamma_{n-1} * S of the exact sum, so if RN_f(RN_d(S_lo/n)) ==
+// RN_f(RN_d(S_hi/n)) over the widened interval the reference's float is
+// pinned.  The rare ambiguous statistics (~1e-5 each) are recomputed with the
+// reference's exact sequential order.
+#include <cfloat>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace xg {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kSlabRows = 32;
+
+// One pass over D_F: each thread owns 4 adjacent columns of a 32-row slab.
+template <int POLICY>
+__global__ void __launch_bounds__(kThreads)
+    k_stats_slab(const float* __restrict__ d, int rows, int cols, double* row_sum,
+                 double* col_sum, uint32_t* row_min, uint32_t* col_min) {
+    const int c = (blockIdx.x * kThreads + threadIdx.x) * 4;
+    const int r0 = blockIdx.y * kSlabRows;
+    const int lane = threadIdx.x & 31;
+    const bool vec = (cols % 4 == 0) && c + 3 < cols;
+    double cs0 = 0, cs1 = 0, cs2 = 0, cs3 = 0;
+    float cm0 = FLT_MAX, cm1 = FLT_MAX, cm2 = FLT_MAX, cm3 = FLT_MAX;
+    for (int rr = 0; rr < kSlabRows; ++rr) {
+        const int r = r0 + rr;
+        if (r >= rows) break;  // uniform across the CTA
+        float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float* p = d + (int64_t)r * cols + c;
+        if (vec) {
+            f = __ldg(reinterpret_cast<const float4*>(p));
+        } else if (c < cols) {
+            f.x = p[0];
+            if (c + 1 < cols) f.y = p[1];
+            if (c + 2 < cols) f.z = p[2];
+            if (c + 3 < cols) f.w = p[3];
+        }
+        if (POLICY == kAvg) {
+            const double a0 = fabs((double)f.x), a1 = fabs((double)f.y), a2 = fabs((double)f.z),
+                         a3 = fabs((double)f.w);
+            cs0 = __dadd_rn(cs0, a0);
+            cs1 = __dadd_rn(cs1, a1);
+            cs2 = __dadd_rn(cs2, a2);
+            cs3 = __dadd_rn(cs3, a3);
+            double rs = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+            rs = warp_sumd(rs);
+            if (lane == 0) atomicAdd(row_sum + r, rs);
+        } else {
+            const bool in0 = c < cols, in1 = c + 1 < cols, in2 = c + 2 < cols, in3 = c + 3 < cols;
+            const float a0 = in0 ? fabsf(f.x) : FLT_MAX, a1 = in1 ? fabsf(f.y) : FLT_MAX,
+                        a2 = in2 ? fabsf(f.z) : FLT_MAX, a3 = in3 ? fabsf(f.w) : FLT_MAX;
+            cm0 = fminf(cm0, a0);
+            cm1 = fminf(cm1, a1);
+            cm2 = fminf(cm2, a2);
+            cm3 = fminf(cm3, a3);
+            float rm = fminf(fminf(a0, a1), fminf(a2, a3));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) rm = fminf(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+            if (lane == 0) atomicMin(row_min + r, fbits(rm));
+        }
+    }
+    if (c < cols) {
+        if (POLICY == kAvg) {
+            atomicAdd(col_sum + c, cs0);
+            if (c + 1 < cols) atomicAdd(col_sum + c + 1, cs1);
+            if (c + 2 < cols) atomicAdd(col_sum + c + 2, cs2);
+            if (c + 3 < cols) atomicAdd(col_sum + c + 3, cs3);
+        } else {
+            atomicMin(col_min + c, fbits(cm0));
+            if (c + 1 < cols) atomicMin(col_min + c + 1, fbits(cm1));
+            if (c + 2 < cols) atomicMin(col_min + c + 2, fbits(cm2));
+            if (c + 3 < cols) atomicMin(col_min + c + 3, fbits(cm3));
+        }
+    }
+}
+
+// float(S / n) with a proof that the reference's sequential sum rounds the
+// same; returns false when the interval straddles a float rounding boundary.
+__device__ __forceinline__ bool verified_mean(double S, int nterms, double n, float& out) {
+    const double u = 1.1102230246251565e-16;  // 2^-53
+    const double k = (double)(nterms > 1 ? nterms - 1 : 0);
+    const double gam = (k * u) / (1.0 - k * u);
+    const double delta = 4.0 * gam * S;
+    const float lo = __double2float_rn(__ddiv_rn(__dsub_rn(S, delta), n));
+    const float hi = __double2float_rn(__ddiv_rn(__dadd_rn(S, delta), n));
+    out = __double2float_rn(__ddiv_rn(S, n));
+    return lo == hi;
+}
+
+__global__ void k_finalize_avg(const double* row_sum, const double* col_sum, int rows, int cols,
+                               float* row_stat, float* col_stat, int* flags, int* nflag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows + cols) return;
+    float v;
+    bool ok;
+    if (i < rows) {
+        ok = verified_mean(row_sum[i], cols, (double)cols, v);
+        row_stat[i] = v;
+    } else {
+        ok = verified_mean(col_sum[i - rows], rows, (double)rows, v);
+        col_stat[i - rows] = v;
+    }
+    if (!ok) flags[atomicAdd(nflag, 1)] = i;
+}
+
+// Exact reference order for the flagged statistics: the CTA stages the slice
+// through shared memory, one thread adds sequentially (pipeline.cpp:219-229).
+constexpr int kChunk = 2048;
+__global__ void __launch_bounds__(kThreads)
+    k_fallback_avg(const float* __restrict__ d, int rows, int cols, const int* flags,
+                   const int* nflag, float* row_stat, float* col_stat) {
+    __shared__ float buf[kChunk];
+    const int nf = *nflag;
+    for (int f = blockIdx.x; f < nf; f += gridDim.x) {
+        const int idx = flags[f];
+        const bool is_row = idx < rows;
+        const int len = is_row ? cols : rows;
+        double s = 0.0;
+        for (int base = 0; base < len; base += kChunk) {
+            const int cnt = min(kChunk, len - base);
+            for (int t = threadIdx.x; t < cnt; t += kThreads) {
+                const int64_t off = is_row ? (int64_t)idx * cols + base + t
+                                           : (int64_t)(base + t) * cols + (idx - rows);
+                buf[t] = d[off];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int t = 0; t < cnt; ++t) s = __dadd_rn(s, fabs((double)buf[t]));
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            const float v = __double2float_rn(__ddiv_rn(s, (double)len));
+            if (is_row) row_stat[idx] = v;
+            else col_stat[idx - rows] = v;
+        }
+    }
+}
+
+__global__ void k_zero(double* a, int na, double* b, int nb, int* n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na) a[i] = 0.0;
+    if (i < nb) b[i] = 0.0;
+    if (i == 0) *n = 0;
+}
+
+}  // namespace
+
+void launch_stats(const float* d, int rows, int cols, int policy, float* row_stat, float* col_stat,
+                  double* row_sum, double* col_sum, int* flags, int* nflag, cudaStream_t s) {
+    dim3 grid((cols + kThreads * 4 - 1) / (kThreads * 4), (rows + kSlabRows - 1) / kSlabRows);
+    if (policy == kAvg) {
+        const int nz = rows > cols ? rows : cols;
+        k_zero<<<(nz + 255) / 256, 256, 0, s>>>(row_sum, rows, col_sum, cols, nflag);
+        k_stats_slab<kAvg><<<grid, kThreads, 0, s>>>(d, rows, cols, row_sum, col_sum, nullptr, nullptr);
+        k_finalize_avg<<<(rows + cols + 255) / 256, 256, 0, s>>>(row_sum, col_sum, rows, cols,
+                                                                 row_stat, col_stat, flags, nflag);
+        k_fallback_avg<<<64, kThreads, 0, s>>>(d, rows, cols, flags, nflag, row_stat, col_stat);
+    } else {
+        // the float bit patterns of |x| order like uints; FLT_MAX initial value (pipeline.cpp:237-238)
+        fill_u32(reinterpret_cast<uint32_t*>(row_stat), 0x7f7fffffu, rows, s);
+        fill_u32(reinterpret_cast<uint32_t*>(col_stat), 0x7f7fffffu, cols, s);
+        k_stats_slab<kMin><<<grid, kThreads, 0, s>>>(d, rows, cols, nullptr, nullptr,
+                                                      reinterpret_cast<uint32_t*>(row_stat),
+                                                      reinterpret_cast<uint32_t*>(col_stat));
+    }
+}
+
+}  // namespace xg

@@ -1,0 +1,260 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle
+(oracle/xigemm_oracle.c, itself pinned to the reference) and the golden vectors
+generated from the reference.  Integer stages, selected index sets and the
+final FP32 output are compared BIT-FOR-BIT (the north star allows 1e-5 on C;
+we hold the stricter bar)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle_lib as ol  # noqa: E402
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2403_06924_b200 as xg  # noqa: E402
+
+GOLD = ol.os.path.join(ol.ROOT, "tests", "golden")
+
+
+def beq(x, y):
+    x = np.asarray(x.cpu() if hasattr(x, "cpu") else x)
+    y = np.asarray(y.cpu() if hasattr(y, "cpu") else y)
+    if x.shape != y.shape:
+        return False
+    if x.dtype.kind == "f":
+        w = np.uint32 if x.dtype.itemsize == 4 else np.uint64
+        return np.array_equal(x.view(w), y.astype(x.dtype).view(w))
+    return np.array_equal(x, y)
+
+
+def cfg_from(c):
+    return xg.XigemmConfig(xg.QuantBits(c.bits), c.threshold, c.density_limit,
+                           xg.QuantScheme(c.scheme), xg.ReductionPolicy(c.policy),
+                           xg.RoundingMode(c.rounding))
+
+
+def test_device_and_library():
+    assert xg.lib().xg_device_ok() == 1
+
+
+@pytest.mark.parametrize("m,k,n", [(1, 1, 1), (3, 3, 3), (33, 17, 29), (128, 128, 128),
+                                   (129, 257, 300), (256, 1024, 512), (1000, 4096, 700),
+                                   (64, 16384, 48)])
+def test_gemm_i8_exact(m, k, n):
+    rng = np.random.default_rng(m * 7 + k * 3 + n)
+    a = rng.integers(-127, 128, size=(m, k), dtype=np.int8)
+    b = rng.integers(-127, 128, size=(k, n), dtype=np.int8)
+    c = xg.gemm_i8(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    ref = (a.astype(np.int64) @ b.astype(np.int64)).astype(np.int32)
+    assert beq(c, ref)
+
+
+def test_gemm_i8_int4_and_overflow_guard():
+    rng = np.random.default_rng(5)
+    a = rng.integers(-7, 8, size=(40, 300), dtype=np.int8)
+    b = rng.integers(-7, 8, size=(300, 70), dtype=np.int8)
+    c = xg.gemm_i8(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), 4, 4)
+    assert beq(c, (a.astype(np.int64) @ b.astype(np.int64)).astype(np.int32))
+    k = 16385
+    with pytest.raises(xg.InvalidArgument):
+        xg.gemm_i8(torch.zeros((1, k), dtype=torch.int8, device="cuda"),
+                   torch.zeros((k, 1), dtype=torch.int8, device="cuda"))
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("rounding", [0, 1])
+@pytest.mark.parametrize("scheme", [0, 1, 2])
+@pytest.mark.parametrize("shape", [(1, 1), (9, 7), (130, 1031), (64, 4100)])
+def test_quantize_exact(oracle, bits, rounding, scheme, shape):
+    a = ol.random_dense(*shape, seed=sum(shape) + bits + scheme, lo=-6, hi=6)
+    rc, q_ref, s_ref = oracle.quantize(a, bits, scheme, rounding)
+    q = xg.quantize(torch.from_numpy(a).cuda(), bits, scheme, rounding)
+    assert beq(q.data, q_ref) and beq(q.scales.values, s_ref)
+    d = xg.dequantize(q)
+    assert beq(d, oracle.dequantize(q_ref, s_ref, scheme)[1])
+    r = xg.residual(torch.from_numpy(a).cuda(), q)
+    assert beq(r, oracle.residual(a, q_ref, s_ref, scheme)[1])
+
+
+def test_quantize_edge_cases(oracle):
+    # all-zero (test_quant.cpp:45-52), scalar walkthrough (:27-43), huge scales
+    z = torch.zeros((3, 3), device="cuda")
+    q = xg.quantize(z, 8, 0, 0)
+    assert float(q.scales.values[0]) == 1.0 and int(q.data.abs().sum()) == 0
+    v = np.array([[1.0, 2.5, 4.0]], np.float32)
+    q = xg.quantize(torch.from_numpy(v).cuda(), 8, 0, 0)
+    assert q.data.cpu().tolist() == [[31, 79, 127]]
+    g = np.load(ol.os.path.join(GOLD, "known_answers.npz"))
+    x = torch.tensor([[1.0, -2.0, 3.0e-3, 0.0]], device="cuda")
+    for rnd in (0, 1):
+        qq = xg.quantize_with_scales(x, 8, xg.ScaleFactors(xg.ScaleScheme.PerTensor, [1e300]), rnd)
+        assert beq(qq.data, g[f"huge_{rnd}"])
+    with pytest.raises(xg.InvalidArgument):
+        xg.quantize(torch.tensor([[1.0, float("inf")]], device="cuda"))
+    with pytest.raises(xg.InvalidArgument):
+        xg.quantize_with_scales(torch.zeros((2, 2), device="cuda"), 8,
+                                xg.ScaleFactors(xg.ScaleScheme.PerTensor, [-2.0]), 1)
+
+
+def _golden_cases():
+    g = np.load(ol.os.path.join(GOLD, "pipeline_golden.npz"))
+    return g, sorted(k[: -len("_meta")] for k in g.files if k.endswith("_meta"))
+
+
+_G, _CASES = _golden_cases()
+
+
+@pytest.mark.parametrize("case", _CASES)
+def test_pipeline_golden(case):
+    g = _G
+    m, k, n, sa, sb, scheme, pol, rnd, bits, path, shape = (int(v) for v in g[case + "_meta"])
+    lo, hi, thr, s, da, db = g[case + "_fmeta"]
+    a = torch.from_numpy(g[f"shape{shape}_a"]).cuda()
+    b = torch.from_numpy(g[f"shape{shape}_b"]).cuda()
+    cfg = xg.XigemmConfig(xg.QuantBits(bits), float(thr), float(s), xg.QuantScheme(scheme),
+                          xg.ReductionPolicy(pol), xg.RoundingMode(rnd))
+    rep = xg.xigemm(a, b, cfg=cfg)
+    assert beq(rep.result, g[case + "_xigemm"])
+    assert int(rep.path) == path and rep.density_a == da and rep.density_b == db
+    assert beq(xg.quantized_gemm_full_residual(a, b, cfg), g[case + "_full"])
+    assert beq(xg.quantized_gemm_direct(a, b, cfg), g[case + "_direct"])
+
+
+def test_stage_golden():
+    g = np.load(ol.os.path.join(GOLD, "stages_golden.npz"))
+    pres = sorted({k.split("cfg")[0] for k in g.files if k.endswith("cfg")})
+    for pre in pres:
+        thr, s, scheme, pol, rnd, bits = g[pre + "cfg"]
+        cfg = xg.XigemmConfig(xg.QuantBits(int(bits)), float(thr), float(s),
+                              xg.QuantScheme(int(scheme)), xg.ReductionPolicy(int(pol)),
+                              xg.RoundingMode(int(rnd)))
+        rep, d = xg.xigemm_dump(torch.from_numpy(g[pre + "a"]).cuda(),
+                                torch.from_numpy(g[pre + "b"]).cuda(), cfg)
+        for name in ("aq", "aq_scales", "bq", "bq_scales", "d_f", "raq", "rbq", "row_stat",
+                     "col_stat", "a_red", "b_red"):
+            assert beq(d[name], g[pre + name]), (pre, name)
+        assert beq(d["raq_scale"], g[pre + "raq_scale"]) and beq(d["rbq_scale"], g[pre + "rbq_scale"])
+        # retained index sets: nnz counts equal the reference's (density is
+        # nnz / size and bit-equal), values equal on every retained entry
+        assert rep.nnz_a == int(g[pre + "a_mask"].sum()) and rep.nnz_b == int(g[pre + "b_mask"].sum())
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_pipeline_vs_oracle_random(oracle, seed):
+    rng = np.random.default_rng(1000 + seed)
+    m, k, n = (int(v) for v in rng.integers(1, 300, size=3))
+    a = ol.random_dense(m, k, seed * 2 + 11, -4, 4)
+    b = ol.random_dense(k, n, seed * 2 + 12, -4, 4)
+    cm = ol.random_dense(m, n, seed + 77, -1, 1)
+    for scheme in (0, 1):
+        for pol in (0, 1):
+            c = ol.cfg(bits=int(rng.choice([4, 8])), threshold=float(10 ** rng.uniform(-2.5, 0.3)),
+                       density_limit=float(rng.uniform(0.05, 1.0)), scheme=scheme, policy=pol,
+                       rounding=int(rng.integers(0, 2)))
+            rc, ref, orep = oracle.xigemm(a, b, c=cm, alpha=1.25, beta=-0.5, config=c)
+            assert rc == 0
+            rep = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                            torch.from_numpy(cm).cuda(), 1.25, -0.5, cfg_from(c))
+            assert beq(rep.result, ref), (m, k, n, scheme, pol)
+            assert (rep.density_a, rep.density_b, int(rep.path)) == \
+                   (orep.density_a, orep.density_b, orep.path)
+            rc, ref2, _ = oracle.xigemm(a, b, alpha=3.0, config=c)
+            rep2 = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), None, 3.0, 0.0,
+                             cfg_from(c))
+            assert beq(rep2.result, ref2)
+
+
+def test_pipeline_validation():
+    d = dict(device="cuda")
+    cfg = xg.XigemmConfig()
+    with pytest.raises(xg.InvalidArgument):
+        xg.xigemm(torch.zeros((2, 3), **d), torch.zeros((2, 3), **d), cfg=cfg)
+    bad = torch.zeros((2, 2), **d)
+    bad[0, 1] = float("nan")
+    with pytest.raises(xg.InvalidArgument):
+        xg.xigemm(bad, torch.zeros((2, 2), **d), cfg=cfg)
+    with pytest.raises(xg.InvalidArgument):
+        xg.xigemm(torch.zeros((2, 2), **d), torch.zeros((2, 2), **d), torch.zeros((3, 3), **d), 1, 1, cfg)
+    with pytest.raises(xg.InvalidArgument):
+        xg.xigemm(torch.zeros((2, 2), **d), torch.zeros((2, 2), **d), cfg=xg.XigemmConfig(threshold=0.0))
+    with pytest.raises(xg.InvalidArgument):
+        xg.xigemm(torch.zeros((2, 2), **d), torch.zeros((2, 2), **d), cfg=xg.XigemmConfig(density_limit=1.5))
+    with pytest.raises(xg.InvalidArgument):
+        xg.xigemm(torch.zeros((1, 16385), **d), torch.zeros((16385, 1), **d), cfg=cfg)
+
+
+def test_stats_and_sparse_api(oracle):
+    d = ol.random_dense(37, 301, 3, -5, 5)
+    dt = torch.from_numpy(d).cuda()
+    for f in ("avg_vectors", "abs_min_vectors"):
+        r, c = getattr(xg, "get_" + f)(dt)
+        _, rr, cr = getattr(oracle, f)(d)
+        assert beq(r, rr) and beq(c, cr)
+    for per_row in (True, False):
+        for pol in (0, 1):
+            st = np.abs(ol.random_dense(37 if per_row else 301, 1, 9, 0, 2)).ravel()
+            fn = xg.reduce_a if per_row else xg.reduce_b
+            s = fn(dt, torch.from_numpy(st).cuda(), 0.6, pol, 3.0)
+            _, rp, ci, v = oracle.reduce(d, st, 0.6, pol, 3.0, per_row)
+            assert beq(s.row_ptr, rp) and beq(s.col_idx, ci) and beq(s.values, v)
+            for scheme in (0, 1, 2):
+                q = xg.quantize_csr(s, 8, scheme, 1)
+                _, qv, qs = oracle.quantize_csr(37, 301, rp, ci, v, 8, scheme, 1)
+                assert beq(q.matrix.values, qv) and beq(q.scales.values, qs)
+            t = xg.csr_transpose(q.matrix)
+            _, trp, tci, tv = oracle.csr_transpose_i8(37, 301, rp, ci, qv)
+            assert beq(t.row_ptr, trp) and beq(t.col_idx, tci) and beq(t.values, tv)
+            dq = np.clip(np.round(ol.random_dense(301, 45, 4, -127, 127)), -127, 127).astype(np.int8)
+            dm = xg.QuantizedMatrix(301, 45, torch.from_numpy(dq).cuda(), xg.QuantBits.Int8,
+                                    xg.ScaleFactors(xg.ScaleScheme.PerTensor, [1.0]), xg.RoundingMode.Nearest)
+            assert beq(xg.spmm_int(q.matrix, dm), oracle.spmm_int(37, 301, rp, ci, qv, dq)[1])
+            df = ol.random_dense(301, 45, 5, -2, 2)
+            assert beq(xg.spmm(s, torch.from_numpy(df).cuda()), oracle.spmm_f32(37, 301, rp, ci, v, df)[1])
+            dense = np.zeros((37, 301), np.float32)
+            for i in range(37):
+                dense[i, ci[rp[i]:rp[i + 1]]] = v[rp[i]:rp[i + 1]]
+            assert beq(xg.densify(s), dense)
+
+
+def test_matrix_api(oracle):
+    a = ol.random_dense(33, 17, 5, -10, 10)
+    b = ol.random_dense(17, 29, 6, -10, 10)
+    assert beq(xg.gemm_f32(a, b), oracle.gemm_f32(a, b)[1])
+    d = torch.from_numpy(ol.random_dense(13, 6, 12, -3, 3)).cuda()
+    c = ol.random_dense(13, 6, 11, -3, 3)
+    ref = oracle.axpby(d.cpu().numpy(), 2.0, c, -0.5)[1]
+    assert beq(xg.axpby_inplace(d, 2.0, torch.from_numpy(c).cuda(), -0.5), ref)
+    p = np.random.default_rng(3).integers(-10**6, 10**6, size=(7, 9)).astype(np.int32)
+    sa = xg.ScaleFactors(xg.ScaleScheme.PerRow, np.linspace(0.5, 3.0, 7))
+    sb = xg.ScaleFactors(xg.ScaleScheme.PerColumn, np.linspace(1.5, 9.0, 9))
+    assert beq(xg.dequant_product(torch.from_numpy(p).cuda(), sa, sb),
+               oracle.dequant_product(p, sa.values, sb.values, 1, 2)[1])
+    with pytest.raises(xg.InvalidArgument):
+        xg.dequant_product(torch.from_numpy(p).cuda(), sb, sa)
+
+
+def test_c1_config_full_oracle(oracle):
+    """C1 (BASELINE.json configs[0]): 1024^3 uniform[-1,1], INT8 vector-wise,
+    threshold giving ~5% residual density; full oracle comparison."""
+    a = xg.generate("uniform", 1024, 1024, 1, -1.0, 1.0)
+    b = xg.generate("uniform", 1024, 1024, 2, -1.0, 1.0)
+    an, bn = a.cpu().numpy(), b.cpu().numpy()
+    assert beq(an, ol.random_dense(1024, 1024, 1, -1, 1))  # generator = test_support stream
+    c = ol.cfg(threshold=0.112, density_limit=0.3, scheme=1, policy=0, rounding=1)
+    rep = xg.xigemm(a, b, cfg=cfg_from(c))
+    rc, ref, orep = oracle.xigemm(an, bn, config=c)
+    assert rc == 0
+    assert beq(rep.result, ref)
+    assert (rep.density_a, rep.density_b, int(rep.path)) == (orep.density_a, orep.density_b, orep.path)
+    assert 0.03 < max(rep.density_a, rep.density_b) < 0.07 and int(rep.path) == 0
+
+
+def test_host_entry_point(oracle):
+    a = ol.random_dense(70, 90, 1, -2, 2)
+    b = ol.random_dense(90, 50, 2, -2, 2)
+    c = ol.cfg(threshold=0.2, scheme=1, policy=0)
+    out, rep = xg.xigemm_host(a, b, cfg=cfg_from(c))
+    assert beq(out, oracle.xigemm(a, b, config=c)[1])
