@@ -65,6 +65,8 @@ typedef struct {
     int64_t nnz_a, nnz_b;
     double ns_quant, ns_xxmm, ns_reduce, ns_package;
     int stats_fallbacks; /* AvgRule statistics recomputed in exact order */
+    double ns_gemm_df;   /* device time of the D_F GEMM launch (K2) */
+    double ns_gemm_comp; /* device time of the compensation GEMM launch (K4+K5) */
 } xg_report;
 
 /* Device pointers (reference row-major layouts) receiving pipeline

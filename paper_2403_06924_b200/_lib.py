@@ -31,7 +31,8 @@ class XgReport(C.Structure):
     _fields_ = [("density_a", C.c_double), ("density_b", C.c_double), ("path", C.c_int),
                 ("nnz_a", C.c_int64), ("nnz_b", C.c_int64), ("ns_quant", C.c_double),
                 ("ns_xxmm", C.c_double), ("ns_reduce", C.c_double), ("ns_package", C.c_double),
-                ("stats_fallbacks", C.c_int)]
+                ("stats_fallbacks", C.c_int), ("ns_gemm_df", C.c_double),
+                ("ns_gemm_comp", C.c_double)]
 
 
 DUMP_FIELDS = ["aq", "aq_scales", "bq", "bq_scales", "d_f", "raq", "raq_scale", "rbq",

@@ -448,6 +448,8 @@ def _pipeline(a, b, c, alpha, beta, cfg: XigemmConfig, reduce: bool, dump: bool,
                         {"quant": int(rep.ns_quant), "xxmm": int(rep.ns_xxmm),
                          "reduce": int(rep.ns_reduce), "package": int(rep.ns_package)},
                         rep.nnz_a, rep.nnz_b, rep.stats_fallbacks)
+    report.timings["gemm_df"] = int(rep.ns_gemm_df)
+    report.timings["gemm_comp"] = int(rep.ns_gemm_comp)
     return (report, bufs) if dump else report
 
 

@@ -387,6 +387,8 @@ void run_pipeline(const float* a, const float* b, const float* c, float alpha, f
         rep->ns_reduce = tm.ns(2, 3);
         rep->ns_package = 0.0;
         rep->stats_fallbacks = h.nflag;
+        rep->ns_gemm_df = tm.ns(1, 2);
+        rep->ns_gemm_comp = tm.ns(3, 4);
     }
 }
 

@@ -48,6 +48,64 @@ __device__ __forceinline__ int quantize_scalar(double a, double lambda, int qmax
     return (int)t;
 }
 
+// Pipeline-only fast form of quantize_scalar, valid when |a*lambda| < 2^63
+// (always true inside the pipeline: lambda = qmax / max|slice| and |a| <= max,
+// so |t| <= qmax (1 + 2^-52)).  Clamping before rounding is then identical to
+// the reference's round-then-clamp, NaN clamps to -qmax like x86's LLONG_MIN,
+// and llround's ties-away is restored from rint's ties-even with an exact
+// correction.  ~8 instructions instead of libdevice round() + range tests.
+__device__ __forceinline__ int quantize_fast(double a, double lambda, double qmax_d, int rounding) {
+    double t = __dmul_rn(a, lambda);
+    if (rounding == kFloor) {
+        t = __dadd_rn(t, copysign(__dmul_rn(4.0 * 2.220446049250313080847e-16, fabs(t)), t));
+        t = fmin(fmax(t, -qmax_d), qmax_d);
+        return (int)t;  // truncation toward zero
+    }
+    t = fmin(fmax(t, -qmax_d), qmax_d);
+    double r = rint(t);
+    if (fabs(__dsub_rn(t, r)) == 0.5) r = __dadd_rn(t, copysign(0.5, t));
+    return (int)r;
+}
+
+// fp32 fast path with an exact fallback.  With lam32 = RN_f(lambda),
+// t32 = RN_f(a * lam32) differs from the reference's t = RN_d(a * lambda) by at
+// most |t| * 2^-23 (+ 2^-53) <= 1.6e-5 for |t| <= 128.  Nearest: llround(t)
+// equals rint(t32) unless t32 lies within 1e-4 of a half-integer; Floor:
+// trunc(t + nudge) equals trunc(t32) unless t32 lies within 2e-4 of an integer.
+// Those rare cases (~2e-4 of elements) take the exact fp64 path.  The rounding
+// itself uses the 1.5*2^23 magic constant, whose float bits hold the integer in
+// the low byte (two's complement), so no float->int conversion is needed.
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+// out-of-line so the rare exact path does not bloat every inlined call site
+static __device__ __noinline__ int quantize_slow(float a, double lambda, float qmaxf, int rounding) {
+    return quantize_fast((double)a, lambda, (double)qmaxf, rounding);
+}
+__device__ __forceinline__ int quantize32(float a, double lambda, float lam32, float qmaxf,
+                                          int rounding) {
+    const float t0 = __fmul_rn(a, lam32);
+    const float t = fminf(fmaxf(t0, -qmaxf), qmaxf);
+    const bool wild = !(fabsf(t0) <= 256.0f);  // NaN input, or lambda outside float range
+    if (rounding == kFloor) {
+        const float r = truncf(t);
+        const float d = fabsf(__fsub_rn(t, r));
+        if (wild || d < 2e-4f || d > 0.9998f) return quantize_slow(a, lambda, qmaxf, rounding);
+        return (int)r;
+    }
+    const float u = __fadd_rn(t, kMagic);
+    const float r = __fsub_rn(u, kMagic);
+    if (wild || fabsf(__fsub_rn(t, r)) >= 0.4999f) return quantize_slow(a, lambda, qmaxf, rounding);
+    return __float_as_int(u) - 0x4B400000;
+}
+
+// Smallest float strictly greater than the fp64 threshold t >= 0, so that the
+// reference's keep test fabs(double(v)) > t (sparse.cpp:65) becomes the float
+// compare |v| >= float_above(t) for float v.
+__device__ __forceinline__ float float_above(double t) {
+    float f = __double2float_ru(t);
+    if ((double)f == t) f = nextafterf(f, __int_as_float(0x7f800000));
+    return f;
+}
+
 // float(double(q) / lambda) — quantize.cpp:156.
 __device__ __forceinline__ float dequant_value(int q, double lambda) {
     return __double2float_rn(__ddiv_rn((double)q, lambda));
@@ -56,6 +114,35 @@ __device__ __forceinline__ float dequant_value(int q, double lambda) {
 // float(double(p) / (la * lb)) — quantize.cpp:183.
 __device__ __forceinline__ float dequant_product_value(int32_t p, double la, double lb) {
     return __double2float_rn(__ddiv_rn((double)p, __dmul_rn(la, lb)));
+}
+
+// ---- fast exact dequantisation -------------------------------------------
+// The reference rounds twice: q = RN_d(p / RN_d(la*lb)), then RN_f(q).  We
+// form y = RN(RN(p * ia) * ib) with ia = RN(1/la), ib = RN(1/lb); |y - q| is a
+// few double ulps (<= ~6u|y|).  RN_f is monotone, so when y lies more than 64
+// double ulps away from every float rounding boundary (a float midpoint sits
+// where the 29 discarded mantissa bits equal 2^28) and inside the float normal
+// range, RN_f(y) == RN_f(q) exactly.  Otherwise (probability ~2e-7) fall back
+// to the reference's own division.  Zero products are exact (+0).
+__device__ __forceinline__ bool float_round_safe(double y) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(y);
+    const unsigned e = (unsigned)(b >> 52) & 0x7ffu;
+    const int low = (int)((unsigned)b & 0x1fffffffu) - 0x10000000;
+    return e >= 1023u - 126u && e <= 1023u + 126u && (low > 64 || low < -64);
+}
+__device__ __forceinline__ float dequant_product_fast(int32_t p, double ia, double ib, double la,
+                                                      double lb) {
+    if (p == 0) return 0.0f;
+    const double y = __dmul_rn(__dmul_rn((double)p, ia), ib);
+    if (float_round_safe(y)) return __double2float_rn(y);
+    return dequant_product_value(p, la, lb);
+}
+// float(q / lambda) with il = RN(1/lambda)
+__device__ __forceinline__ float dequant_fast(int q, double il, double lambda) {
+    if (q == 0) return 0.0f;
+    const double y = __dmul_rn((double)q, il);
+    if (float_round_safe(y)) return __double2float_rn(y);
+    return dequant_value(q, lambda);
 }
 
 // Non-negative float <-> order-preserving uint bits (for atomicMax / atomicMin).
@@ -191,6 +278,64 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// ---- CTA-pair (cta_group::2) variants ------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+                 : "memory");
+}
+// TMA load whose completion is counted on the LEADER CTA's barrier (peer bit
+// of the shared::cta barrier address cleared).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, uint64_t* bar, int x,
+                                                 int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(tmap), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y)
+        : "memory");
+}
+// commit arriving on the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // 32 lanes x 32 consecutive 32-bit columns: thread t of the warp gets lane
 // (warp%4)*32+t, columns [col, col+32).
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {

@@ -2,6 +2,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -72,10 +73,44 @@ void run(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, c
     kern<<<grid, 256, Cfg::SMEM_BYTES, s>>>(maps, args);
 }
 
+template <int NACC, int EPI>
+void run2(const KOperand* ops, int nops, const GemmArgs& args, cudaStream_t s) {
+    using Cfg = Gemm2Cfg<NACC>;
+    TmaMaps maps;
+    std::memset(&maps, 0, sizeof maps);
+    for (int i = 0; i < nops; ++i) encode(&maps.m[i], ops[i], args.K, 128);
+    for (int i = nops; i < kMaxMaps; ++i) maps.m[i] = maps.m[0];
+    auto kern = k_gemm_i8_tc2<NACC, EPI>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+        attr_set = true;
+    }
+    const int tiles = ((args.M + 255) / 256) * ((args.N + 255) / 256);
+    const int pairs = sm_count() / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(maps, args);
+}
+
+bool use_pair_kernel(const GemmArgs& args) {
+    static const int env = [] {
+        const char* e = getenv("XG_GEMM_1CTA");
+        return e && *e == '1';
+    }();
+    return !env && args.M >= 256;
+}
+
 }  // namespace
 
 void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const GemmArgs& args,
              cudaStream_t s) {
+    if (use_pair_kernel(args) && epi != EPI_FULL3) {
+        switch (epi) {
+            case EPI_S32: run2<1, EPI_S32>(ops, nops, args, s); return;
+            case EPI_DF: run2<1, EPI_DF>(ops, nops, args, s); return;
+            case EPI_COMP: run2<2, EPI_COMP>(ops, nops, args, s); return;
+        }
+    }
     switch (epi) {
         case EPI_S32: run<256, 1, EPI_S32>(ops, is_b, nops, args, s); break;
         case EPI_DF: run<256, 1, EPI_DF>(ops, is_b, nops, args, s); break;

@@ -85,14 +85,30 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int gro
     nb = w / gm;
 }
 
+// Column j's scale and its reciprocal live in lane j of the warp (computed once
+// per 32-column chunk), fetched with a shuffle.
+struct ColScale {
+    double lam, inv;
+    __device__ __forceinline__ void load(const ScaleRef& s, int col) {
+        lam = s.at(col);
+        inv = __ddiv_rn(1.0, lam);
+    }
+    __device__ __forceinline__ double lam_of(int j) const { return __shfl_sync(0xffffffffu, lam, j); }
+    __device__ __forceinline__ double inv_of(int j) const { return __shfl_sync(0xffffffffu, inv, j); }
+};
+
 template <int NACC, int EPI>
 __device__ __forceinline__ void epilogue_chunk(const GemmArgs& args, int sel,
                                                const uint32_t (&acc)[NACC][32], int row,
-                                               int col0, double r0, double r1, double r2) {
+                                               int col0, double r0, double r1, double r2,
+                                               double i0, double i1, double i2, bool active) {
     const int64_t obase = (int64_t)row * args.N + col0;
     const int ncol = min(32, args.N - col0);
     const bool full = ((args.N & 3) == 0) && ncol == 32;
+    const int lane = threadIdx.x & 31;
+    const int mycol = min(col0 + lane, args.N - 1);
     if constexpr (EPI == EPI_S32) {
+        if (!active) return;
         int32_t* o = args.out_s32 + obase;
         if (full) {
 #pragma unroll
@@ -105,15 +121,24 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& args, int sel,
     } else {
         float res[32];
         if constexpr (EPI == EPI_DF) {
-            const ScaleRef cs = args.cs[0][sel];
+            ColScale c0;
+            c0.load(args.cs[0][sel], mycol);
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-                res[j] = dequant_product_value((int32_t)acc[0][j], r0, cs.at(min(col0 + j, args.N - 1)));
+                res[j] = dequant_product_fast((int32_t)acc[0][j], i0, c0.inv_of(j), r0, c0.lam_of(j));
+            if (!active) return;
         } else if constexpr (EPI == EPI_COMP) {
+            ColScale c0, c1;
+            c0.load(args.cs[0][sel], mycol);
+            c1.load(args.cs[1][sel], mycol);
+
             float din[32], cin[32];
             const float* dp = args.df_in + obase;
             const float* cp = args.c_in + obase;
-            if (full) {
+            if (!active) {  // rows past M: compute on zeros, store nothing
+#pragma unroll
+                for (int j = 0; j < 32; ++j) din[j] = cin[j] = 0.0f;
+            } else if (full) {
 #pragma unroll
                 for (int v = 0; v < 8; ++v) {
                     const float4 x = reinterpret_cast<const float4*>(dp)[v];
@@ -133,29 +158,31 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& args, int sel,
                     cin[j] = (args.has_c && j < ncol) ? cp[j] : 0.0f;
                 }
             }
-            const ScaleRef c0 = args.cs[0][sel], c1 = args.cs[1][sel];
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const int col = min(col0 + j, args.N - 1);
                 // pipeline.cpp:134-145: d_f += dr1; d_f += dr2 (fp32, this order)
-                const float t1 = dequant_product_value((int32_t)acc[0][j], r0, c0.at(col));
-                const float t2 = dequant_product_value((int32_t)acc[1 % NACC][j], r1, c1.at(col));
+                const float t1 = dequant_product_fast((int32_t)acc[0][j], i0, c0.inv_of(j), r0, c0.lam_of(j));
+                const float t2 = dequant_product_fast((int32_t)acc[1 % NACC][j], i1, c1.inv_of(j), r1, c1.lam_of(j));
                 float v = __fadd_rn(__fadd_rn(din[j], t1), t2);
                 // pipeline.cpp:195-202 / matrix.cpp:102 (non-fused)
                 if (args.has_c) v = __fadd_rn(__fmul_rn(args.alpha, v), __fmul_rn(args.beta, cin[j]));
                 else if (args.alpha != 1.0f) v = __fmul_rn(v, args.alpha);
                 res[j] = v;
             }
+            if (!active) return;
         } else {  // EPI_FULL3
-            const ScaleRef c0 = args.cs[0][sel], c1 = args.cs[1][sel], c2 = args.cs[2][sel];
+            ColScale c0, c1, c2;
+            c0.load(args.cs[0][sel], mycol);
+            c1.load(args.cs[1][sel], mycol);
+            c2.load(args.cs[2][sel], mycol);
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const int col = min(col0 + j, args.N - 1);
-                const float t0 = dequant_product_value((int32_t)acc[0][j], r0, c0.at(col));
-                const float t1 = dequant_product_value((int32_t)acc[1 % NACC][j], r1, c1.at(col));
-                const float t2 = dequant_product_value((int32_t)acc[2 % NACC][j], r2, c2.at(col));
+                const float t0 = dequant_product_fast((int32_t)acc[0][j], i0, c0.inv_of(j), r0, c0.lam_of(j));
+                const float t1 = dequant_product_fast((int32_t)acc[1 % NACC][j], i1, c1.inv_of(j), r1, c1.lam_of(j));
+                const float t2 = dequant_product_fast((int32_t)acc[2 % NACC][j], i2, c2.inv_of(j), r2, c2.lam_of(j));
                 res[j] = __fadd_rn(__fadd_rn(t0, t1), t2);
             }
+            if (!active) return;
         }
         float* o = args.out_f32 + obase;
         if (full) {
@@ -288,12 +315,13 @@ __global__ void __launch_bounds__(256, 1)
             const int row = mb * Cfg::BM + q * 32 + lane;
             const bool row_ok = row < args.M;
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * Cfg::ACC_COLS;
-            double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+            double r0 = 1.0, r1 = 1.0, r2 = 1.0;
             if (EPI != EPI_S32 && row_ok) {  // row scales are fixed per thread
                 r0 = args.rs[0][sel].at(row);
                 if (NACC > 1) r1 = args.rs[1][sel].at(row);
                 if (NACC > 2) r2 = args.rs[2][sel].at(row);
             }
+            const double i0 = __ddiv_rn(1.0, r0), i1 = __ddiv_rn(1.0, r1), i2 = __ddiv_rn(1.0, r2);
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t acc[NACC][32];
@@ -301,7 +329,8 @@ __global__ void __launch_bounds__(256, 1)
                 for (int a = 0; a < NACC; ++a) tmem_ld32(tbase + a * BN + c * 32, acc[a]);
                 tmem_ld_wait();
                 const int col0 = nb * BN + c * 32;
-                if (row_ok && col0 < args.N) epilogue_chunk<NACC, EPI>(args, sel, acc, row, col0, r0, r1, r2);
+                if (col0 < args.N)  // warp-uniform; per-thread row validity passed down
+                    epilogue_chunk<NACC, EPI>(args, sel, acc, row, col0, r0, r1, r2, i0, i1, i2, row_ok);
                 __syncwarp();
             }
             tc_fence_before();
@@ -317,6 +346,195 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    }
+}
+
+}  // namespace xg
+
+namespace xg {
+
+// ---------------------------------------------------------------------------
+// CTA-pair version (cta_group::2): a cluster of 2 CTAs on one TPC computes a
+// 256 x 256 tile with one tcgen05.mma.cta_group::2 (M=256, N=256, K=32)
+// issued by the leader.  Each CTA stages its own 128 rows of A and its own 128
+// rows of B^T, so per-SM operand traffic is (128+128) B per K byte instead of
+// (128+256) for the 1-CTA 128x256 tile: 64 B/clk/SM at full MMA rate.  The
+// accumulator rows 0-127 land in the leader's TMEM, 128-255 in the peer's.
+// 8 epilogue warps (two per TMEM lane quadrant, one per 128-column half).
+template <int NACC>
+struct Gemm2Cfg {
+    static constexpr int BM = 128;   // rows per CTA (pair M = 256)
+    static constexpr int BN = 256;   // pair N
+    static constexpr int BNH = 128;  // B^T rows staged per CTA
+    static constexpr int BK = 128;
+    static constexpr int A_BYTES = BM * BK;
+    static constexpr int B_BYTES = BNH * BK;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = 6;
+    static constexpr int ACC_COLS = NACC * BN;
+    static constexpr int ACC_BUFS = (512 / ACC_COLS) >= 2 ? 2 : 1;
+    static constexpr int TMEM_COLS = 512;
+    static constexpr int THREADS = 384;
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int GROUP_M = 8;  // in 256-row units
+    static_assert(ACC_COLS * ACC_BUFS <= 512, "TMEM overflow");
+};
+
+template <int NACC, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    k_gemm_i8_tc2(const __grid_constant__ TmaMaps maps, const GemmArgs args) {
+    using Cfg = Gemm2Cfg<NACC>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+    uint64_t* empty = full + Cfg::STAGES;
+    uint64_t* tfull = empty + Cfg::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int cluster_id = blockIdx.x >> 1;
+    const int nclusters = gridDim.x >> 1;
+    const int num_m = (args.M + 2 * Cfg::BM - 1) / (2 * Cfg::BM);
+    const int num_n = (args.N + Cfg::BN - 1) / Cfg::BN;
+    const int num_tiles = num_m * num_n;
+    const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
+    const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < Cfg::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 2 * Cfg::EPI_WARPS);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < kMaxMaps; ++i) tma_prefetch(&maps.m[i]);
+    }
+    if (warp == 2) tmem_alloc2(tmem_slot, Cfg::TMEM_COLS);
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer (both CTAs) =====================
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cluster_id; t < num_tiles; t += nclusters) {
+                int mb, nb;
+                tile_coords(t, num_m, num_n, Cfg::GROUP_M, mb, nb);
+                const int arow = mb * 2 * Cfg::BM + (int)rank * Cfg::BM;
+                const int brow = nb * Cfg::BN + (int)rank * Cfg::BNH;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    for (int a = 0; a < NACC; ++a) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
+                        uint8_t* sB = sA + Cfg::A_BYTES;
+                        if (leader) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+                        tma_load_2d_pair(sA, &maps.m[args.amap[a][sel]], &full[stage], kb * Cfg::BK, arow);
+                        tma_load_2d_pair(sB, &maps.m[args.bmap[a][sel]], &full[stage], kb * Cfg::BK, brow);
+                        if (++stage == Cfg::STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (leader CTA, one thread) =====================
+        if (leader && elect_one()) {
+            constexpr uint32_t idesc = idesc_i8(2 * Cfg::BM, Cfg::BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int buf = 0;
+            uint32_t bphase = 0;
+            for (int t = cluster_id; t < num_tiles; t += nclusters) {
+                mbar_wait(&tempty[buf], bphase ^ 1);
+                tc_fence_after();
+                const uint32_t dbase = tmem_base + buf * Cfg::ACC_COLS;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    for (int a = 0; a < NACC; ++a) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
+                        const uint64_t da = smem_desc_k128(sA);
+                        const uint64_t db = smem_desc_k128(sA + Cfg::A_BYTES);
+#pragma unroll
+                        for (int k = 0; k < Cfg::BK / 32; ++k)
+                            mma_i8_pair(dbase + a * Cfg::BN, da + 2 * k, db + 2 * k, idesc,
+                                        (kb | k) != 0 ? 1u : 0u);
+                        tc_commit_pair(&empty[stage]);
+                        if (++stage == Cfg::STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+                tc_commit_pair(&tfull[buf]);
+                if (++buf == Cfg::ACC_BUFS) {
+                    buf = 0;
+                    bphase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue (8 warps per CTA) =====================
+        const int q = warp & 3;          // TMEM lane quadrant
+        const int half = (warp - 4) >> 2;  // 128-column half of the tile
+        const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0);
+        int buf = 0;
+        uint32_t bphase = 0;
+        for (int t = cluster_id; t < num_tiles; t += nclusters) {
+            int mb, nb;
+            tile_coords(t, num_m, num_n, Cfg::GROUP_M, mb, nb);
+            mbar_wait(&tfull[buf], bphase);
+            tc_fence_after();
+            const int row = mb * 2 * Cfg::BM + (int)rank * Cfg::BM + q * 32 + lane;
+            const bool row_ok = row < args.M;
+            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * Cfg::ACC_COLS +
+                                   half * (Cfg::BN / 2);
+            double r0 = 1.0, r1 = 1.0, r2 = 1.0;
+            if (EPI != EPI_S32 && row_ok) {
+                r0 = args.rs[0][sel].at(row);
+                if (NACC > 1) r1 = args.rs[1][sel].at(row);
+            }
+            const double i0 = __ddiv_rn(1.0, r0), i1 = __ddiv_rn(1.0, r1), i2 = 1.0;
+#pragma unroll 1
+            for (int c = 0; c < Cfg::BN / 2 / 32; ++c) {
+                uint32_t acc[NACC][32];
+#pragma unroll
+                for (int a = 0; a < NACC; ++a) tmem_ld32(tbase + a * Cfg::BN + c * 32, acc[a]);
+                tmem_ld_wait();
+                const int col0 = nb * Cfg::BN + half * (Cfg::BN / 2) + c * 32;
+                if (col0 < args.N)
+                    epilogue_chunk<NACC, EPI>(args, sel, acc, row, col0, r0, r1, r2, i0, i1, i2, row_ok);
+                __syncwarp();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader0 + buf * 8);
+            if (++buf == Cfg::ACC_BUFS) {
+                buf = 0;
+                bphase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc2(tmem_base, Cfg::TMEM_COLS);
     }
 }
 

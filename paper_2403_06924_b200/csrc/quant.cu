@@ -1,8 +1,16 @@
 // K1 (quantiser) and K3 (residual quantisation + threshold selection).
 //
-// HBM-bound integer/byte work: 128-bit coalesced loads, rows held in registers
-// so each input byte leaves HBM once per pass, warp-shuffle + shared-memory
-// block reductions, one atomic per CTA for the global maxima.
+// HBM-bound byte work.  Design rules that the profile (profiles/) forced:
+//  * the per-element quantisation runs in fp32 with a proven error margin and
+//    an exact fp64 fallback (quantize.cpp:13-24 semantics) taken once per quad
+//    of elements, rounding mode is a template parameter (no per-element
+//    branches), and ints are packed from the float bit patterns;
+//  * dequantisation float(q / lambda) is a 255-entry table per scale: one per
+//    row for A (broadcast-ish LDS), column-interleaved lut[q][col] for B so the
+//    32 lanes (32 different columns) hit 32 different banks;
+//  * rows are held in registers (one HBM read per pass); B column tiles are
+//    staged transposed through conflict-free [64][33]-word shared arrays so the
+//    K-major int8 outputs leave as 16-byte stores.
 //
 // Replaces (reference, proj/src/):
 //   quantize / quantize_with_scales / slice_max_abs   quantize.cpp:28-36,107-150
@@ -21,6 +29,7 @@ namespace {
 
 constexpr int kThreads = 256;
 
+template <int NT = kThreads>
 __device__ __forceinline__ float block_max(float v, float* red) {
     v = warp_maxf(v);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -29,7 +38,7 @@ __device__ __forceinline__ float block_max(float v, float* red) {
     __syncthreads();
     float r = red[0];
 #pragma unroll
-    for (int i = 1; i < kThreads / 32; ++i) r = fmaxf(r, red[i]);
+    for (int i = 1; i < NT / 32; ++i) r = fmaxf(r, red[i]);
     return r;
 }
 
@@ -50,13 +59,41 @@ __device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v
 // pipeline's all_finite check rejects it; quantize() maps it to -qmax).
 __device__ __forceinline__ int not_finite(float x) { return isinf(x) ? 1 : (x != x ? 2 : 0); }
 
-// Row element e of this thread: column (v*256 + tid)*4 + (e%4).
-template <int VPT>
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+// ---- fp32 quantiser (see quantize32 in common.cuh for the error analysis) --
+// Valid for |x*lambda| <= qmax (1 + 2^-52) (always so inside the pipeline);
+// anything outside, NaN, or within the error margin of a rounding boundary
+// raises `slow`, and the caller redoes the quad exactly.
+template <int RND>
+__device__ __forceinline__ int q32(float x, float lam32, float qlim, bool& slow) {
+    const float t = __fmul_rn(x, lam32);
+    if (RND == kNearest) {
+        const float u = __fadd_rn(t, kMagic);  // rint, ties-even
+        const float d = fabsf(__fsub_rn(t, __fsub_rn(u, kMagic)));
+        slow |= !(d < 0.4999f) | !(fabsf(t) <= qlim);
+        return __float_as_int(u) - 0x4B400000;
+    } else {
+        const float r = truncf(t);
+        const float d = fabsf(__fsub_rn(t, r));
+        slow |= (!(d >= 2e-4f && d <= 0.9998f) & (fabsf(t) > 0.5f)) | !(fabsf(t) <= qlim);
+        return __float_as_int(__fadd_rn(r, kMagic)) - 0x4B400000;
+    }
+}
+
+__device__ __forceinline__ int qexact(float x, double lam, float qmaxf, int rnd) {
+    return quantize_slow(x, lam, qmaxf, rnd);
+}
+
+// Row element e of this thread: column (v*NT + tid)*4 + (e%4).
+template <int VPT, int NT>
 __device__ __forceinline__ void load_row(const float* __restrict__ row, int cols, bool vec,
                                          float (&x)[VPT * 4]) {
 #pragma unroll
     for (int v = 0; v < VPT; ++v) {
-        const int c = (v * kThreads + (int)threadIdx.x) * 4;
+        const int c = (v * NT + (int)threadIdx.x) * 4;
         if (vec && c + 3 < cols) {
             const float4 f = __ldg(reinterpret_cast<const float4*>(row + c));
             x[4 * v] = f.x;
@@ -70,47 +107,48 @@ __device__ __forceinline__ void load_row(const float* __restrict__ row, int cols
     }
 }
 
-template <int VPT>
-__device__ __forceinline__ void store_row_i8(int8_t* __restrict__ row, int cols, bool vec,
-                                             const int (&q)[VPT * 4]) {
+__device__ __forceinline__ void store_quad(int8_t* __restrict__ row, int c, int cols, bool vec,
+                                           uint32_t packed) {
+    if (vec && c + 3 < cols) {
+        *reinterpret_cast<uint32_t*>(row + c) = packed;
+    } else {
 #pragma unroll
-    for (int v = 0; v < VPT; ++v) {
-        const int c = (v * kThreads + (int)threadIdx.x) * 4;
-        if (vec && c + 3 < cols) {
-            const uint32_t p = (uint32_t)(q[4 * v] & 0xff) | ((uint32_t)(q[4 * v + 1] & 0xff) << 8) |
-                               ((uint32_t)(q[4 * v + 2] & 0xff) << 16) |
-                               ((uint32_t)(q[4 * v + 3] & 0xff) << 24);
-            *reinterpret_cast<uint32_t*>(row + c) = p;
-        } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (c + e < cols) row[c + e] = (int8_t)q[4 * v + e];
-        }
+        for (int e = 0; e < 4; ++e)
+            if (c + e < cols) row[c + e] = (int8_t)(packed >> (8 * e));
     }
 }
 
 // ------------------------------------------------------------------ K1 rows --
-// One CTA per row.  PerRow: row absmax -> lambda_i; quantize; residual via a
-// 255-entry per-row table of float(q / lambda_i); max|residual|.
-template <int VPT>
+// One CTA per row, the row held in registers.  PerRow: row absmax -> lambda_i;
+// quantise; residual through a 255-entry per-row table of float(q / lambda_i);
+// max|residual|.  Non-finite codes: bit 0 = an infinite slice max (the
+// reference's compute_scale throws), bit 1 = any NaN/inf (all_finite fails).
+template <int VPT, int RND>
 __global__ void __launch_bounds__(kThreads) k_quant_rows(const QuantRowsArgs a) {
     __shared__ float lut[256];
     __shared__ float red[kThreads / 32];
     const int qmax = quant_max(a.bits);
+    const float qmaxf = (float)qmax;
+    const float qlim = qmaxf + 0.25f;
     const bool vec = (a.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
                      (a.ldq % 4 == 0);
     float rmax_acc = 0.0f, gmax_acc = 0.0f;
     int bad = 0;
     for (int r = blockIdx.x; r < a.rows; r += gridDim.x) {
         float x[VPT * 4];
-        load_row<VPT>(a.x + (int64_t)r * a.ld, a.cols, vec, x);
-        float m = 0.0f;
+        load_row<VPT, kThreads>(a.x + (int64_t)r * a.ld, a.cols, vec, x);
+        float m = 0.0f, s = 0.0f;
 #pragma unroll
         for (int e = 0; e < VPT * 4; ++e) {
             m = fmaxf(m, fabsf(x[e]));
-            bad |= not_finite(x[e]);
+            s = __fadd_rn(s, x[e]);  // NaN / inf propagate (finite overflow is re-checked)
+        }
+        if (!(fabsf(s) <= FLT_MAX)) {
+#pragma unroll
+            for (int e = 0; e < VPT * 4; ++e) bad |= fabsf(x[e]) <= FLT_MAX ? 0 : 2;
         }
         m = block_max(m, red);
+        bad |= m > FLT_MAX ? 1 : 0;
         gmax_acc = fmaxf(gmax_acc, m);
         double lam;
         if (a.per_row) {
@@ -119,16 +157,25 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows(const QuantRowsArgs a) 
         } else {
             lam = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
         }
+        const float lam32 = __double2float_rn(lam);
         if (threadIdx.x <= 2 * qmax) lut[threadIdx.x] = dequant_value((int)threadIdx.x - qmax, lam);
         __syncthreads();
-        int q[VPT * 4];
         float rm = 0.0f;
+        int8_t* qrow = a.q + (int64_t)r * a.ldq;
 #pragma unroll
-        for (int e = 0; e < VPT * 4; ++e) {
-            q[e] = quantize_scalar((double)x[e], lam, qmax, a.rounding);
-            rm = fmaxf(rm, fabsf(__fsub_rn(x[e], lut[q[e] + qmax])));
+        for (int v = 0; v < VPT; ++v) {
+            bool slow = false;
+            int q[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) q[e] = q32<RND>(x[4 * v + e], lam32, qlim, slow);
+            if (slow) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) q[e] = qexact(x[4 * v + e], lam, qmaxf, RND);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[4 * v + e], lut[q[e] + qmax])));
+            store_quad(qrow, (v * kThreads + (int)threadIdx.x) * 4, a.cols, vec, pack4(q[0], q[1], q[2], q[3]));
         }
-        store_row_i8<VPT>(a.q + (int64_t)r * a.ldq, a.cols, vec, q);
         rmax_acc = fmaxf(rmax_acc, rm);
         __syncthreads();  // lut reuse
     }
@@ -141,7 +188,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows(const QuantRowsArgs a) 
 }
 
 // Generic (any column count) variant: two passes over the row, the second one
-// served from L2.
+// served from L2.  Exact scalar path throughout.
 __global__ void __launch_bounds__(kThreads) k_quant_rows_generic(const QuantRowsArgs a) {
     __shared__ float lut[256];
     __shared__ float red[kThreads / 32];
@@ -154,9 +201,10 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows_generic(const QuantRows
         for (int c = threadIdx.x; c < a.cols; c += kThreads) {
             const float v = row[c];
             m = fmaxf(m, fabsf(v));
-            bad |= not_finite(v);
+            bad |= fabsf(v) <= FLT_MAX ? 0 : 2;
         }
         m = block_max(m, red);
+        bad |= m > FLT_MAX ? 1 : 0;
         gmax_acc = fmaxf(gmax_acc, m);
         double lam;
         if (a.per_row) {
@@ -170,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows_generic(const QuantRows
         float rm = 0.0f;
         for (int c = threadIdx.x; c < a.cols; c += kThreads) {
             const float v = row[c];
-            const int q = quantize_scalar((double)v, lam, qmax, a.rounding);
+            const int q = quantize_fast((double)v, lam, (double)qmax, a.rounding);
             a.q[(int64_t)r * a.ldq + c] = (int8_t)q;
             rm = fmaxf(rm, fabsf(__fsub_rn(v, lut[q + qmax])));
         }
@@ -250,76 +298,112 @@ __global__ void __launch_bounds__(kThreads)
     if (bad) atomicOr(nonfinite, bad);
 }
 
-// ------------------------------------------------------------- K1 columns --
-// Tile of 128 rows (K) x 64 columns (N) of a row-major matrix: quantise with
-// per-column (or per-tensor) scales and write the ints transposed (N x K,
-// K-major) through shared memory — the layout the tensor-core B operand wants.
-constexpr int kTK = 128, kTN = 64;
+// ---------------------------------------------------- column tiles (B side) --
+// ---------------------------------------------------- column tiles (B side) --
+// Tiles of 64 columns (N) x 128 rows (K) of a row-major K x N matrix whose ints
+// are written transposed (N x K, K-major: the tensor-core B layout).  Warp w
+// owns rows [16w, 16w+16) of the tile, lane l owns columns l and 32+l, so every
+// global load is a coalesced 128-byte row segment and every thread packs 4
+// consecutive K bytes into one 32-bit shared-memory word; the [64][33]-word
+// staging array makes both the packed writes and the row-wise read-out
+// bank-conflict free.  A CTA walks kColSub such tiles down the columns so the
+// per-column dequant tables (built once per CTA) are amortised.
+constexpr int kTK = 128, kTN = 64, kTW = kTK / 4 + 1;
+constexpr int kColSub = 8;
+constexpr int kColTileRows = kTK * kColSub;
+constexpr int kLutBytes = 256 * kTN * 4;  // lut[q + qmax][column]
 
-__device__ __forceinline__ void store_T_tile(const int8_t (*tq)[kTK + 16], int8_t* dst,
-                                             int64_t ldq, int n0, int k0, int cols, int rows) {
-    // 64 rows x 128 bytes; thread -> (row c = tid/4, 32-byte chunk (tid%4))
-    const int c = threadIdx.x >> 2;
-    const int kk = (threadIdx.x & 3) * 32;
-    if (n0 + c >= cols) return;
-    int8_t* d = dst + (int64_t)(n0 + c) * ldq + k0 + kk;
-    const int kval = rows - (k0 + kk);  // valid bytes in this chunk
+__device__ __forceinline__ void store_T_tile(const uint32_t (*t)[kTW], int8_t* dst, int64_t ldq,
+                                             int n0, int k0, int cols, int rows) {
+    const int r = threadIdx.x >> 2;     // 0..63 output row (column n of the input)
+    const int seg = threadIdx.x & 3;    // 32-byte segment of the 128-byte row
+    if (n0 + r >= cols) return;
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = t[r][seg * 8 + i];
+    int8_t* d = dst + (int64_t)(n0 + r) * ldq + k0 + seg * 32;
+    const int kval = rows - (k0 + seg * 32);
     if (kval >= 32 && (ldq % 16) == 0) {
-        const int4* s = reinterpret_cast<const int4*>(&tq[c][kk]);
-        reinterpret_cast<int4*>(d)[0] = s[0];
-        reinterpret_cast<int4*>(d)[1] = s[1];
-    } else {
-        for (int j = 0; j < 32 && j < kval; ++j) d[j] = tq[c][kk + j];
+        reinterpret_cast<uint4*>(d)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        reinterpret_cast<uint4*>(d)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else if (kval > 0) {
+        for (int j = 0; j < 32 && j < kval; ++j) d[j] = (int8_t)(w[j >> 2] >> (8 * (j & 3)));
     }
 }
 
+// v[c][i] = X[k0 + 16w + i][n0 + 32c + lane]
+__device__ __forceinline__ void load_col_tile(const float* __restrict__ x, int rows, int cols,
+                                              int64_t ld, int n0, int k0, float (&v)[2][16]) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int n = n0 + 32 * c + lane;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int k = k0 + 16 * w + i;
+            v[c][i] = (n < cols && k < rows) ? __ldg(x + (int64_t)k * ld + n) : 0.0f;
+        }
+    }
+}
+
+__device__ __forceinline__ void build_col_luts(float (*lut)[kTN], const double* lam_s, int qmax) {
+    for (int i = threadIdx.x; i < (2 * qmax + 1) * kTN; i += kThreads) {
+        const int e = i / kTN, c = i % kTN;
+        lut[e][c] = dequant_value(e - qmax, lam_s[c]);
+    }
+}
+
+template <int RND>
 __global__ void __launch_bounds__(kThreads) k_quant_cols_T(const QuantColsArgs a) {
-    __shared__ __align__(16) int8_t tq[kTN][kTK + 16];
+    extern __shared__ float4 dyn_smem[];
+    float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
+    __shared__ uint32_t tq[kTN][kTW];
     __shared__ double lam_s[kTN];
     __shared__ float red[kThreads / 32];
-    const int n0 = blockIdx.x * kTN, k0 = blockIdx.y * kTK;
+    const int n0 = blockIdx.x * kTN;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qmax = quant_max(a.bits);
+    const float qmaxf = (float)qmax, qlim = qmaxf + 0.25f;
     if (threadIdx.x < kTN) {
-        const int c = min(n0 + (int)threadIdx.x, a.cols - 1);
-        double lam;
-        if (a.per_col) {
-            lam = compute_scale((double)__uint_as_float(a.colmax[c]), a.bits);
-            if (blockIdx.y == 0 && a.lam_out && n0 + (int)threadIdx.x < a.cols) a.lam_out[c] = lam;
-        } else {
-            lam = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
-        }
+        const int n = min(n0 + (int)threadIdx.x, a.cols - 1);
+        const double lam = a.per_col ? compute_scale((double)__uint_as_float(a.colmax[n]), a.bits)
+                                     : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
         lam_s[threadIdx.x] = lam;
+        if (a.per_col && blockIdx.y == 0 && a.lam_out && n0 + (int)threadIdx.x < a.cols) a.lam_out[n] = lam;
     }
     __syncthreads();
-    const int cg = (threadIdx.x & 15) * 4;  // 4 columns
-    const bool vec = (a.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
-                     (n0 + cg + 3 < a.cols);
+    build_col_luts(lut, lam_s, qmax);
+    const double lamc[2] = {lam_s[lane], lam_s[32 + lane]};
+    const float l32[2] = {__double2float_rn(lamc[0]), __double2float_rn(lamc[1])};
+    __syncthreads();
     float rm = 0.0f;
-#pragma unroll 4
-    for (int i = 0; i < kTK / 16; ++i) {
-        const int kr = (threadIdx.x >> 4) + 16 * i;
-        const int k = k0 + kr;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (k < a.rows) {
-            const float* p = a.x + (int64_t)k * a.ld + n0 + cg;
-            if (vec) {
-                const float4 f = __ldg(reinterpret_cast<const float4*>(p));
-                v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-            } else {
+    for (int sub = 0; sub < kColSub; ++sub) {
+        const int k0 = blockIdx.y * kColTileRows + sub * kTK;
+        if (k0 >= a.rows) break;  // uniform
+        float v[2][16];
+        load_col_tile(a.x, a.rows, a.cols, a.ld, n0, k0, v);
 #pragma unroll
-                for (int e = 0; e < 4; ++e) v[e] = (n0 + cg + e < a.cols) ? p[e] : 0.f;
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                bool slow = false;
+                int q[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) q[e] = q32<RND>(v[c][4 * g + e], l32[c], qlim, slow);
+                if (slow) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) q[e] = qexact(v[c][4 * g + e], lamc[c], qmaxf, RND);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    rm = fmaxf(rm, fabsf(__fsub_rn(v[c][4 * g + e], lut[q[e] + qmax][32 * c + lane])));
+                tq[32 * c + lane][4 * w + g] = pack4(q[0], q[1], q[2], q[3]);
             }
         }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const double lam = lam_s[cg + e];
-            const int q = quantize_scalar((double)v[e], lam, qmax, a.rounding);
-            tq[cg + e][kr] = (int8_t)q;
-            rm = fmaxf(rm, fabsf(__fsub_rn(v[e], dequant_value(q, lam))));
-        }
+        __syncthreads();
+        store_T_tile(tq, a.qT, a.ldq, n0, k0, a.cols, a.rows);
+        __syncthreads();
     }
-    __syncthreads();
-    store_T_tile(tq, a.qT, a.ldq, n0, k0, a.cols, a.rows);
     rm = block_max(rm, red);
     if (threadIdx.x == 0 && a.rmax) atomicMax(a.rmax, fbits(rm));
 }
@@ -328,7 +412,8 @@ __global__ void __launch_bounds__(kThreads) k_quant_cols_T(const QuantColsArgs a
 // Per row i of A: RAq = quantize(a - deq(aq), lambda_RA) and the reduced
 // operand A'q = (|a| > t_i) ? aq : 0 (quantize_csr values equal aq under
 // PerRow scales; under PerTensor the retained-max scale is checked afterwards
-// and a fix-up pass rewrites A'q if it differs).
+// and a fix-up pass rewrites A'q if it differs).  No row reduction precedes the
+// element work, so the row is streamed (low registers, full occupancy).
 __device__ __forceinline__ double threshold_of(int policy, double thr_m, float stat,
                                                double scale_other, int inner) {
     // sparse.cpp:49-55
@@ -336,60 +421,92 @@ __device__ __forceinline__ double threshold_of(int policy, double thr_m, float s
     return __ddiv_rn(__dmul_rn(__dmul_rn(thr_m, scale_other), (double)stat), (double)inner);
 }
 
-template <int VPT>
+// One quad of the selection: q (main scale), rq (residual scale), red (kept q).
+template <int RND>
+__device__ __forceinline__ void select_quad(const float (&x)[4], const float* lutp, int lstride,
+                                            double lam, float lam32, double lam_r, float lam_r32,
+                                            float tf, float qmaxf, float qlim, int qmax,
+                                            uint32_t& pq, uint32_t& pr, unsigned long long& cnt,
+                                            float& ret) {
+    bool slow = false;
+    int q[4], rq[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) q[e] = q32<RND>(x[e], lam32, qlim, slow);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        rq[e] = q32<RND>(__fsub_rn(x[e], lutp[(q[e] + qmax) * lstride]), lam_r32, qlim, slow);
+    if (slow) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            q[e] = qexact(x[e], lam, qmaxf, RND);
+            rq[e] = qexact(__fsub_rn(x[e], lutp[(q[e] + qmax) * lstride]), lam_r, qmaxf, RND);
+        }
+    }
+    int d[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const bool keep = fabsf(x[e]) >= tf;
+        d[e] = keep ? q[e] : 0;
+        cnt += keep;
+        ret = fmaxf(ret, keep ? fabsf(x[e]) : 0.0f);
+    }
+    pq = pack4(rq[0], rq[1], rq[2], rq[3]);
+    pr = pack4(d[0], d[1], d[2], d[3]);
+}
+
+template <int RND>
 __global__ void __launch_bounds__(kThreads) k_select_rows(const SelectArgs a) {
     __shared__ float lut[256];
     __shared__ float red[kThreads / 32];
     __shared__ unsigned long long redu[kThreads / 32];
     const int qmax = quant_max(a.bits);
+    const float qmaxf = (float)qmax, qlim = qmaxf + 0.25f;
     const bool vec = (a.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
-                     (a.ldq % 4 == 0);
+                     (a.ldq % 4 == 0) && (a.cols % 4 == 0);
     const double lam_r = compute_scale((double)__uint_as_float(*a.rmax), a.bits);
+    const float lam_r32 = __double2float_rn(lam_r);
     const double lam_t = a.vec ? 0.0 : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
     const double scale_other =
         a.do_select && a.policy == kMin ? compute_scale((double)__uint_as_float(*a.other_max), a.bits)
                                         : 1.0;
-    double lam_fix = 0.0;
-    if (a.fix_mode) {
-        // PerTensor reduced operand: lambda' over the retained values (sparse.cpp:198-203)
-        lam_fix = compute_scale((double)__uint_as_float(*a.retmax), a.bits);
-        if (lam_fix == lam_t) return;  // usual case: A'q already correct
-    }
     unsigned long long cnt = 0;
     float ret = 0.0f;
     for (int r = blockIdx.x; r < a.rows; r += gridDim.x) {
-        float x[VPT * 4];
-        load_row<VPT>(a.x + (int64_t)r * a.ld, a.cols, vec, x);
+        const float* row = a.x + (int64_t)r * a.ld;
+        int8_t* rq_row = a.rq + (int64_t)r * a.ldq;
+        int8_t* rd_row = a.do_select ? a.red + (int64_t)r * a.ldq : nullptr;
         const double lam = a.vec ? a.lam[r] : lam_t;
-        const double t = a.do_select ? threshold_of(a.policy, a.thr_m, a.stat[r], scale_other, a.cols)
-                                     : 0.0;
-        if (!a.fix_mode) {
-            if (threadIdx.x <= 2 * qmax) lut[threadIdx.x] = dequant_value((int)threadIdx.x - qmax, lam);
-            __syncthreads();
-        }
-        int rq[VPT * 4], rd[VPT * 4];
-#pragma unroll
-        for (int e = 0; e < VPT * 4; ++e) {
-            const int c = (e / 4 * kThreads + (int)threadIdx.x) * 4 + (e & 3);
-            const bool in = c < a.cols;
-            const bool keep = a.do_select && in && fabs((double)x[e]) > t;
-            if (a.fix_mode) {
-                rd[e] = keep ? quantize_scalar((double)x[e], lam_fix, qmax, a.rounding) : 0;
-                rq[e] = 0;
-            } else {
-                const int q = quantize_scalar((double)x[e], lam, qmax, a.rounding);
-                const float res = __fsub_rn(x[e], lut[q + qmax]);
-                rq[e] = quantize_scalar((double)res, lam_r, qmax, a.rounding);
-                rd[e] = keep ? q : 0;
-                cnt += keep;
-                if (keep) ret = fmaxf(ret, fabsf(x[e]));
+        const float lam32 = __double2float_rn(lam);
+        const float tf = a.do_select
+                             ? float_above(threshold_of(a.policy, a.thr_m, a.stat[r], scale_other, a.cols))
+                             : __int_as_float(0x7f800000);
+        if (threadIdx.x <= 2 * qmax) lut[threadIdx.x] = dequant_value((int)threadIdx.x - qmax, lam);
+        __syncthreads();
+        if (vec) {
+#pragma unroll 2
+            for (int c = threadIdx.x * 4; c < a.cols; c += kThreads * 4) {
+                const float4 f = __ldg(reinterpret_cast<const float4*>(row + c));
+                const float x[4] = {f.x, f.y, f.z, f.w};
+                uint32_t pq, pr;
+                select_quad<RND>(x, lut, 1, lam, lam32, lam_r, lam_r32, tf, qmaxf, qlim, qmax, pq, pr,
+                                 cnt, ret);
+                *reinterpret_cast<uint32_t*>(rq_row + c) = pq;
+                if (rd_row) *reinterpret_cast<uint32_t*>(rd_row + c) = pr;
+            }
+        } else {
+            for (int c = threadIdx.x; c < a.cols; c += kThreads) {
+                const float v = row[c];
+                const int q = quantize_fast((double)v, lam, (double)qmax, RND);
+                rq_row[c] = (int8_t)quantize_fast((double)__fsub_rn(v, lut[q + qmax]), lam_r, (double)qmax, RND);
+                const bool keep = fabsf(v) >= tf;
+                if (rd_row) rd_row[c] = (int8_t)(keep ? q : 0);
+                cnt += keep && a.do_select;
+                ret = fmaxf(ret, keep ? fabsf(v) : 0.0f);
             }
         }
-        if (!a.fix_mode) store_row_i8<VPT>(a.rq + (int64_t)r * a.ldq, a.cols, vec, rq);
-        if (a.do_select) store_row_i8<VPT>(a.red + (int64_t)r * a.ldq, a.cols, vec, rd);
-        if (!a.fix_mode) __syncthreads();
+        __syncthreads();
     }
-    if (!a.fix_mode && a.do_select) {
+    if (a.do_select) {
         cnt = block_sum_u64(cnt, redu);
         ret = block_max(ret, red);
         if (threadIdx.x == 0) {
@@ -399,133 +516,434 @@ __global__ void __launch_bounds__(kThreads) k_select_rows(const SelectArgs a) {
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_select_rows_generic(const SelectArgs a) {
-    __shared__ float lut[256];
-    __shared__ float red[kThreads / 32];
-    __shared__ unsigned long long redu[kThreads / 32];
+// PerTensor reduced operand whose retained-max scale differs from the operand
+// scale (sparse.cpp:198-203): rewrite the kept ints with lambda'.  Exits at
+// once in the usual case lambda' == lambda.  Exact scalar path (rare).
+__global__ void __launch_bounds__(kThreads) k_fix_rows(const SelectArgs a) {
+    const double lam_t = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
+    const double lam_fix = compute_scale((double)__uint_as_float(*a.retmax), a.bits);
+    if (lam_fix == lam_t) return;
     const int qmax = quant_max(a.bits);
-    const double lam_r = compute_scale((double)__uint_as_float(*a.rmax), a.bits);
-    const double lam_t = a.vec ? 0.0 : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
-    const double scale_other =
-        a.do_select && a.policy == kMin ? compute_scale((double)__uint_as_float(*a.other_max), a.bits)
-                                        : 1.0;
-    double lam_fix = 0.0;
-    if (a.fix_mode) {
-        lam_fix = compute_scale((double)__uint_as_float(*a.retmax), a.bits);
-        if (lam_fix == lam_t) return;
-    }
-    unsigned long long cnt = 0;
-    float ret = 0.0f;
+    const double so = a.policy == kMin ? compute_scale((double)__uint_as_float(*a.other_max), a.bits) : 1.0;
     for (int r = blockIdx.x; r < a.rows; r += gridDim.x) {
-        const float* row = a.x + (int64_t)r * a.ld;
-        const double lam = a.vec ? a.lam[r] : lam_t;
-        const double t = a.do_select ? threshold_of(a.policy, a.thr_m, a.stat[r], scale_other, a.cols)
-                                     : 0.0;
-        if (!a.fix_mode) {
-            if (threadIdx.x <= 2 * qmax) lut[threadIdx.x] = dequant_value((int)threadIdx.x - qmax, lam);
-            __syncthreads();
-        }
+        const float tf = float_above(threshold_of(a.policy, a.thr_m, a.stat[r], so, a.cols));
         for (int c = threadIdx.x; c < a.cols; c += kThreads) {
-            const float v = row[c];
-            const bool keep = a.do_select && fabs((double)v) > t;
-            if (a.fix_mode) {
-                a.red[(int64_t)r * a.ldq + c] =
-                    (int8_t)(keep ? quantize_scalar((double)v, lam_fix, qmax, a.rounding) : 0);
-            } else {
-                const int q = quantize_scalar((double)v, lam, qmax, a.rounding);
-                a.rq[(int64_t)r * a.ldq + c] = (int8_t)quantize_scalar(
-                    (double)__fsub_rn(v, lut[q + qmax]), lam_r, qmax, a.rounding);
-                if (a.do_select) a.red[(int64_t)r * a.ldq + c] = (int8_t)(keep ? q : 0);
-                cnt += keep;
-                if (keep) ret = fmaxf(ret, fabsf(v));
-            }
+            const float v = a.x[(int64_t)r * a.ld + c];
+            a.red[(int64_t)r * a.ldq + c] =
+                (int8_t)(fabsf(v) >= tf ? quantize_fast((double)v, lam_fix, (double)qmax, a.rounding) : 0);
         }
-        if (!a.fix_mode) __syncthreads();
     }
-    if (!a.fix_mode && a.do_select) {
-        cnt = block_sum_u64(cnt, redu);
-        ret = block_max(ret, red);
-        if (threadIdx.x == 0) {
-            if (cnt) atomicAdd(a.nnz, cnt);
-            atomicMax(a.retmax, fbits(ret));
+}
+
+// B side: column j of the reduced operand is row j of B'q^T.
+__global__ void __launch_bounds__(kThreads) k_fix_cols_T(const SelectArgs a) {
+    const double lam_t = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
+    const double lam_fix = compute_scale((double)__uint_as_float(*a.retmax), a.bits);
+    if (lam_fix == lam_t) return;
+    const int qmax = quant_max(a.bits);
+    const double so = a.policy == kMin ? compute_scale((double)__uint_as_float(*a.other_max), a.bits) : 1.0;
+    for (int n = blockIdx.x; n < a.cols; n += gridDim.x) {
+        const float tf = float_above(threshold_of(a.policy, a.thr_m, a.stat[n], so, a.rows));
+        for (int k = threadIdx.x; k < a.rows; k += kThreads) {
+            const float v = a.x[(int64_t)k * a.ld + n];
+            a.red[(int64_t)n * a.ldq + k] =
+                (int8_t)(fabsf(v) >= tf ? quantize_fast((double)v, lam_fix, (double)qmax, a.rounding) : 0);
         }
     }
 }
 
 // ----------------------------------------------------------- K3 columns --
 // B side: RBq^T and B'q^T (both N x K, K-major), column thresholds t_j.
+template <int RND>
 __global__ void __launch_bounds__(kThreads) k_select_cols_T(const SelectArgs a) {
-    __shared__ __align__(16) int8_t trq[kTN][kTK + 16];
-    __shared__ __align__(16) int8_t tred[kTN][kTK + 16];
+    extern __shared__ float4 dyn_smem[];
+    float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
+    __shared__ uint32_t trq[kTN][kTW];
+    __shared__ uint32_t tred[kTN][kTW];
     __shared__ double lam_s[kTN];
-    __shared__ double thr_s[kTN];
     __shared__ float red[kThreads / 32];
     __shared__ unsigned long long redu[kThreads / 32];
-    const int n0 = blockIdx.x * kTN, k0 = blockIdx.y * kTK;
+    const int n0 = blockIdx.x * kTN;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qmax = quant_max(a.bits);
+    const float qmaxf = (float)qmax, qlim = qmaxf + 0.25f;
     const double lam_r = compute_scale((double)__uint_as_float(*a.rmax), a.bits);
+    const float lam_r32 = __double2float_rn(lam_r);
     const double lam_t = a.vec ? 0.0 : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
-    double lam_fix = 0.0;
-    if (a.fix_mode) {
-        lam_fix = compute_scale((double)__uint_as_float(*a.retmax), a.bits);
-        if (lam_fix == lam_t) return;
-    }
+    const double so = a.do_select && a.policy == kMin
+                          ? compute_scale((double)__uint_as_float(*a.other_max), a.bits)
+                          : 1.0;
     if (threadIdx.x < kTN) {
-        const int c = min(n0 + (int)threadIdx.x, a.cols - 1);
-        lam_s[threadIdx.x] = a.vec ? a.lam[c] : lam_t;
-        if (a.do_select) {
-            const double so = a.policy == kMin
-                                  ? compute_scale((double)__uint_as_float(*a.other_max), a.bits)
-                                  : 1.0;
-            thr_s[threadIdx.x] = threshold_of(a.policy, a.thr_m, a.stat[c], so, a.rows);
-        }
+        const int n = min(n0 + (int)threadIdx.x, a.cols - 1);
+        lam_s[threadIdx.x] = a.vec ? a.lam[n] : lam_t;
     }
     __syncthreads();
-    const int cg = (threadIdx.x & 15) * 4;
-    const bool vec = (a.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
-                     (n0 + cg + 3 < a.cols);
+    build_col_luts(lut, lam_s, qmax);
+    double lamc[2];
+    float l32[2], tf[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int nraw = n0 + 32 * c + lane;
+        const int n = min(nraw, a.cols - 1);
+        lamc[c] = lam_s[32 * c + lane];
+        l32[c] = __double2float_rn(lamc[c]);
+        tf[c] = (a.do_select && nraw < a.cols)
+                    ? float_above(threshold_of(a.policy, a.thr_m, a.stat[n], so, a.rows))
+                    : __int_as_float(0x7f800000);
+    }
+    __syncthreads();
     unsigned long long cnt = 0;
     float ret = 0.0f;
-#pragma unroll 2
-    for (int i = 0; i < kTK / 16; ++i) {
-        const int kr = (threadIdx.x >> 4) + 16 * i;
-        const int k = k0 + kr;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (k < a.rows) {
-            const float* p = a.x + (int64_t)k * a.ld + n0 + cg;
-            if (vec) {
-                const float4 f = __ldg(reinterpret_cast<const float4*>(p));
-                v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-            } else {
+    for (int sub = 0; sub < kColSub; ++sub) {
+        const int k0 = blockIdx.y * kColTileRows + sub * kTK;
+        if (k0 >= a.rows) break;  // uniform
+        float v[2][16];
+        load_col_tile(a.x, a.rows, a.cols, a.ld, n0, k0, v);  // rows past K load as 0: never kept
 #pragma unroll
-                for (int e = 0; e < 4; ++e) v[e] = (n0 + cg + e < a.cols) ? p[e] : 0.f;
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                const float x[4] = {v[c][4 * g], v[c][4 * g + 1], v[c][4 * g + 2], v[c][4 * g + 3]};
+                uint32_t pq, pr;
+                select_quad<RND>(x, &lut[0][32 * c + lane], kTN, lamc[c], l32[c], lam_r, lam_r32, tf[c],
+                                 qmaxf, qlim, qmax, pq, pr, cnt, ret);
+                trq[32 * c + lane][4 * w + g] = pq;
+                tred[32 * c + lane][4 * w + g] = pr;
             }
         }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const bool in = k < a.rows && n0 + cg + e < a.cols;
-            const bool keep = a.do_select && in && fabs((double)v[e]) > thr_s[cg + e];
-            if (a.fix_mode) {
-                tred[cg + e][kr] = (int8_t)(keep ? quantize_scalar((double)v[e], lam_fix, qmax, a.rounding) : 0);
-            } else {
-                const double lam = lam_s[cg + e];
-                const int q = quantize_scalar((double)v[e], lam, qmax, a.rounding);
-                const float res = __fsub_rn(v[e], dequant_value(q, lam));
-                trq[cg + e][kr] = (int8_t)quantize_scalar((double)res, lam_r, qmax, a.rounding);
-                tred[cg + e][kr] = (int8_t)(keep ? q : 0);
-                cnt += keep;
-                if (keep) ret = fmaxf(ret, fabsf(v[e]));
-            }
-        }
+        __syncthreads();
+        store_T_tile(trq, a.rq, a.ldq, n0, k0, a.cols, a.rows);
+        if (a.do_select) store_T_tile(tred, a.red, a.ldq, n0, k0, a.cols, a.rows);
+        __syncthreads();
     }
-    __syncthreads();
-    if (!a.fix_mode) store_T_tile(trq, a.rq, a.ldq, n0, k0, a.cols, a.rows);
-    if (a.do_select) store_T_tile(tred, a.red, a.ldq, n0, k0, a.cols, a.rows);
-    if (!a.fix_mode && a.do_select) {
+    if (a.do_select) {
         cnt = block_sum_u64(cnt, redu);
         ret = block_max(ret, red);
         if (threadIdx.x == 0) {
             if (cnt) atomicAdd(a.nnz, cnt);
+            atomicMax(a.retmax, fbits(ret));
+        }
+    }
+}
+
+
+// =================================================================== fast path
+// Nearest rounding (the pipeline default), per-element cost ~15 instructions.
+// Inside the pipeline |x * lambda| <= qmax (1 + 2^-52) because lambda is
+// qmax / max|slice|, so no range test is needed: u = RN(t + 1.5*2^23) holds
+// rint(t) in its low mantissa bits, |t - rint(t)| is accumulated with one
+// FMNMX per element and a quad whose maximum reaches 0.4999 (a possible
+// llround tie within the fp32 error bound) is redone exactly.  Rows / columns
+// whose lambda32 is not a finite float, or that contain a NaN, take the exact
+// path as a whole (uniform branch).  Table lookups address shared memory
+// straight from the u bit pattern.
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t qn(float x, float lam32, float& dmax) {
+    const float t = __fmul_rn(x, lam32);
+    const float u = __fadd_rn(t, kMagic);
+    dmax = fmaxf(dmax, fabsf(__fsub_rn(t, __fsub_rn(u, kMagic))));
+    return __float_as_uint(u);
+}
+__device__ __forceinline__ uint32_t ubits(int q) { return (uint32_t)(q + 0x4B400000); }
+__device__ __forceinline__ uint32_t pack4u(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+template <int VPT, int NT>
+__global__ void __launch_bounds__(NT) k_quant_rows_fast(const QuantRowsArgs a) {
+    __shared__ float lut[256];
+    __shared__ float red[NT / 32];
+    const int qmax = quant_max(a.bits);
+    const float qmaxf = (float)qmax;
+    const bool vec = (a.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) &&
+                     (a.ldq % 4 == 0);
+    // lut[q + qmax] at smem address (u_bits << 2) + adj
+    const uint32_t adj = smem_u32(lut) + 4u * (uint32_t)qmax - 4u * 0x4B400000u;
+    float rmax_acc = 0.0f, gmax_acc = 0.0f;
+    int bad = 0;
+    for (int r = blockIdx.x; r < a.rows; r += gridDim.x) {
+        float x[VPT * 4];
+        load_row<VPT, NT>(a.x + (int64_t)r * a.ld, a.cols, vec, x);
+        float m = 0.0f, s = 0.0f;
+#pragma unroll
+        for (int e = 0; e < VPT * 4; ++e) {
+            m = fmaxf(m, fabsf(x[e]));
+            s = __fadd_rn(s, x[e]);  // NaN / inf propagate (finite overflow only costs the exact path)
+        }
+        const bool odd = !(fabsf(s) <= FLT_MAX);
+        if (odd) {
+#pragma unroll
+            for (int e = 0; e < VPT * 4; ++e) bad |= fabsf(x[e]) <= FLT_MAX ? 0 : 2;
+        }
+        m = block_max<NT>(m, red);
+        bad |= m > FLT_MAX ? 1 : 0;
+        gmax_acc = fmaxf(gmax_acc, m);
+        double lam;
+        if (a.per_row) {
+            lam = compute_scale((double)m, a.bits);
+            if (threadIdx.x == 0 && a.lam_out) a.lam_out[r] = lam;
+        } else {
+            lam = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
+        }
+        const float lam32 = __double2float_rn(lam);
+        const bool exact = odd || !(lam32 <= FLT_MAX);
+        if (threadIdx.x <= 2 * qmax) lut[threadIdx.x] = dequant_value((int)threadIdx.x - qmax, lam);
+        __syncthreads();
+        float rm = 0.0f;
+        int8_t* qrow = a.q + (int64_t)r * a.ldq;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            uint32_t u[4];
+            float dmax = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) u[e] = qn(x[4 * v + e], lam32, dmax);
+            if (exact || !(dmax < 0.4999f)) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(x[4 * v + e], lam, qmaxf, kNearest));
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[4 * v + e], lds_f32((u[e] << 2) + adj))));
+            store_quad(qrow, (v * NT + (int)threadIdx.x) * 4, a.cols, vec, pack4u(u[0], u[1], u[2], u[3]));
+        }
+        rmax_acc = fmaxf(rmax_acc, rm);
+        __syncthreads();  // lut reuse
+    }
+    rmax_acc = block_max<NT>(rmax_acc, red);
+    if (threadIdx.x == 0) {
+        if (a.rmax) atomicMax(a.rmax, fbits(rmax_acc));
+        if (a.gmax) atomicMax(a.gmax, fbits(gmax_acc));
+    }
+    if (bad && a.nonfinite) atomicOr(a.nonfinite, bad);
+}
+
+// Selection quad, Nearest.  lut_adj: smem address of lut entry q = adj + (u << shift).
+template <int SHIFT>
+__device__ __forceinline__ void select_quad_n(const float (&x)[4], uint32_t lut_adj, double lam,
+                                              float lam32, double lam_r, float lam_r32, float tf,
+                                              float qmaxf, bool exact, uint32_t& pq, uint32_t& pr,
+                                              unsigned& cnt, float& lmax) {
+    uint32_t u[4], ur[4];
+    float dmax = 0.0f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) u[e] = qn(x[e], lam32, dmax);
+    float res[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        res[e] = __fsub_rn(x[e], lds_f32((u[e] << SHIFT) + lut_adj));
+        ur[e] = qn(res[e], lam_r32, dmax);
+    }
+    if (exact || !(dmax < 0.4999f)) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            u[e] = ubits(qexact(x[e], lam, qmaxf, kNearest));
+            res[e] = __fsub_rn(x[e], lds_f32((u[e] << SHIFT) + lut_adj));
+            ur[e] = ubits(qexact(res[e], lam_r, qmaxf, kNearest));
+        }
+    }
+    uint32_t d[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float ax = fabsf(x[e]);
+        const bool keep = ax >= tf;
+        d[e] = keep ? u[e] : 0u;
+        cnt += keep ? 1u : 0u;
+        lmax = fmaxf(lmax, ax);
+    }
+    pq = pack4u(ur[0], ur[1], ur[2], ur[3]);
+    pr = pack4u(d[0], d[1], d[2], d[3]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_select_rows_fast(const SelectArgs a) {
+    __shared__ float lut[256];
+    __shared__ float red[kThreads / 32];
+    __shared__ unsigned long long redu[kThreads / 32];
+    const int qmax = quant_max(a.bits);
+    const float qmaxf = (float)qmax;
+    const uint32_t adj = smem_u32(lut) + 4u * (uint32_t)qmax - 4u * 0x4B400000u;
+    const double lam_r = compute_scale((double)__uint_as_float(*a.rmax), a.bits);
+    const float lam_r32 = __double2float_rn(lam_r);
+    const double lam_t = a.vec ? 0.0 : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
+    const double scale_other =
+        a.do_select && a.policy == kMin ? compute_scale((double)__uint_as_float(*a.other_max), a.bits)
+                                        : 1.0;
+    unsigned cnt = 0;
+    float ret = 0.0f;
+    for (int r = blockIdx.x; r < a.rows; r += gridDim.x) {
+        const float* row = a.x + (int64_t)r * a.ld;
+        int8_t* rq_row = a.rq + (int64_t)r * a.ldq;
+        int8_t* rd_row = a.red + (int64_t)r * a.ldq;
+        const double lam = a.vec ? a.lam[r] : lam_t;
+        const float lam32 = __double2float_rn(lam);
+        const bool exact = !(lam32 <= FLT_MAX) || !(lam_r32 <= FLT_MAX);
+        const float tf = a.do_select
+                             ? float_above(threshold_of(a.policy, a.thr_m, a.stat[r], scale_other, a.cols))
+                             : __int_as_float(0x7f800000);
+        if (threadIdx.x <= 2 * qmax) lut[threadIdx.x] = dequant_value((int)threadIdx.x - qmax, lam);
+        __syncthreads();
+        float lmax = 0.0f;
+#pragma unroll 4
+        for (int c = threadIdx.x * 4; c < a.cols; c += kThreads * 4) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(row + c));
+            const float x[4] = {f.x, f.y, f.z, f.w};
+            uint32_t pq, pr;
+            select_quad_n<2>(x, adj, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, pq, pr, cnt, lmax);
+            *reinterpret_cast<uint32_t*>(rq_row + c) = pq;
+            if (a.do_select) *reinterpret_cast<uint32_t*>(rd_row + c) = pr;
+        }
+        // kept max of this thread's part of the row: its max if that is kept
+        ret = fmaxf(ret, lmax >= tf ? lmax : 0.0f);
+        __syncthreads();
+    }
+    if (a.do_select) {
+        const unsigned long long c64 = block_sum_u64(cnt, redu);
+        ret = block_max(ret, red);
+        if (threadIdx.x == 0) {
+            if (c64) atomicAdd(a.nnz, c64);
+            atomicMax(a.retmax, fbits(ret));
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_quant_cols_T_fast(const QuantColsArgs a) {
+    extern __shared__ float4 dyn_smem[];
+    float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
+    __shared__ uint32_t tq[kTN][kTW];
+    __shared__ double lam_s[kTN];
+    __shared__ float red[kThreads / 32];
+    const int n0 = blockIdx.x * kTN;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qmax = quant_max(a.bits);
+    const float qmaxf = (float)qmax;
+    if (threadIdx.x < kTN) {
+        const int n = min(n0 + (int)threadIdx.x, a.cols - 1);
+        const double lam = a.per_col ? compute_scale((double)__uint_as_float(a.colmax[n]), a.bits)
+                                     : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
+        lam_s[threadIdx.x] = lam;
+        if (a.per_col && blockIdx.y == 0 && a.lam_out && n0 + (int)threadIdx.x < a.cols) a.lam_out[n] = lam;
+    }
+    __syncthreads();
+    build_col_luts(lut, lam_s, qmax);
+    double lamc[2];
+    float l32[2];
+    uint32_t adj[2];
+    bool exact[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        lamc[c] = lam_s[32 * c + lane];
+        l32[c] = __double2float_rn(lamc[c]);
+        exact[c] = !(l32[c] <= FLT_MAX);
+        // lut[q + qmax][32c + lane] = base + 256 (q + qmax) + 4 (32c + lane)
+        adj[c] = smem_u32(lut) + 4u * (32 * c + lane) + 256u * (uint32_t)qmax - 256u * 0x4B400000u;
+    }
+    __syncthreads();
+    float rm = 0.0f;
+    for (int sub = 0; sub < kColSub; ++sub) {
+        const int k0 = blockIdx.y * kColTileRows + sub * kTK;
+        if (k0 >= a.rows) break;  // uniform
+        float v[2][16];
+        load_col_tile(a.x, a.rows, a.cols, a.ld, n0, k0, v);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                uint32_t u[4];
+                float dmax = 0.0f;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) u[e] = qn(v[c][4 * g + e], l32[c], dmax);
+                if (exact[c] || !(dmax < 0.4999f)) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(v[c][4 * g + e], lamc[c], qmaxf, kNearest));
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    rm = fmaxf(rm, fabsf(__fsub_rn(v[c][4 * g + e], lds_f32((u[e] << 8) + adj[c]))));
+                tq[32 * c + lane][4 * w + g] = pack4u(u[0], u[1], u[2], u[3]);
+            }
+        }
+        __syncthreads();
+        store_T_tile(tq, a.qT, a.ldq, n0, k0, a.cols, a.rows);
+        __syncthreads();
+    }
+    rm = block_max(rm, red);
+    if (threadIdx.x == 0 && a.rmax) atomicMax(a.rmax, fbits(rm));
+}
+
+__global__ void __launch_bounds__(kThreads) k_select_cols_T_fast(const SelectArgs a) {
+    extern __shared__ float4 dyn_smem[];
+    float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
+    __shared__ uint32_t trq[kTN][kTW];
+    __shared__ uint32_t tred[kTN][kTW];
+    __shared__ double lam_s[kTN];
+    __shared__ float red[kThreads / 32];
+    __shared__ unsigned long long redu[kThreads / 32];
+    const int n0 = blockIdx.x * kTN;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qmax = quant_max(a.bits);
+    const float qmaxf = (float)qmax;
+    const double lam_r = compute_scale((double)__uint_as_float(*a.rmax), a.bits);
+    const float lam_r32 = __double2float_rn(lam_r);
+    const double lam_t = a.vec ? 0.0 : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
+    const double so = a.do_select && a.policy == kMin
+                          ? compute_scale((double)__uint_as_float(*a.other_max), a.bits)
+                          : 1.0;
+    if (threadIdx.x < kTN) {
+        const int n = min(n0 + (int)threadIdx.x, a.cols - 1);
+        lam_s[threadIdx.x] = a.vec ? a.lam[n] : lam_t;
+    }
+    __syncthreads();
+    build_col_luts(lut, lam_s, qmax);
+    double lamc[2];
+    float l32[2], tf[2];
+    uint32_t adj[2];
+    bool exact[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const int nraw = n0 + 32 * c + lane;
+        const int n = min(nraw, a.cols - 1);
+        lamc[c] = lam_s[32 * c + lane];
+        l32[c] = __double2float_rn(lamc[c]);
+        exact[c] = !(l32[c] <= FLT_MAX) || !(lam_r32 <= FLT_MAX);
+        adj[c] = smem_u32(lut) + 4u * (32 * c + lane) + 256u * (uint32_t)qmax - 256u * 0x4B400000u;
+        tf[c] = (a.do_select && nraw < a.cols)
+                    ? float_above(threshold_of(a.policy, a.thr_m, a.stat[n], so, a.rows))
+                    : __int_as_float(0x7f800000);
+    }
+    __syncthreads();
+    unsigned cnt = 0;
+    float ret = 0.0f;
+    for (int sub = 0; sub < kColSub; ++sub) {
+        const int k0 = blockIdx.y * kColTileRows + sub * kTK;
+        if (k0 >= a.rows) break;  // uniform
+        float v[2][16];
+        load_col_tile(a.x, a.rows, a.cols, a.ld, n0, k0, v);  // rows past K load as 0: never kept
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            float lmax = 0.0f;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                const float x[4] = {v[c][4 * g], v[c][4 * g + 1], v[c][4 * g + 2], v[c][4 * g + 3]};
+                uint32_t pq, pr;
+                select_quad_n<8>(x, adj[c], lamc[c], l32[c], lam_r, lam_r32, tf[c], qmaxf, exact[c], pq, pr,
+                                 cnt, lmax);
+                trq[32 * c + lane][4 * w + g] = pq;
+                tred[32 * c + lane][4 * w + g] = pr;
+            }
+            ret = fmaxf(ret, lmax >= tf[c] ? lmax : 0.0f);
+        }
+        __syncthreads();
+        store_T_tile(trq, a.rq, a.ldq, n0, k0, a.cols, a.rows);
+        if (a.do_select) store_T_tile(tred, a.red, a.ldq, n0, k0, a.cols, a.rows);
+        __syncthreads();
+    }
+    if (a.do_select) {
+        const unsigned long long c64 = block_sum_u64(cnt, redu);
+        ret = block_max(ret, red);
+        if (threadIdx.x == 0) {
+            if (c64) atomicAdd(a.nnz, c64);
             atomicMax(a.retmax, fbits(ret));
         }
     }
@@ -583,36 +1001,72 @@ void launch_absmax_cols(const float* x, int rows, int cols, int64_t ld, uint32_t
     k_absmax_cols<<<grid, kThreads, 0, s>>>(x, rows, cols, ld, colmax, gmax, nonfinite);
 }
 
-void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
+template <int RND>
+void quant_rows_rnd(const QuantRowsArgs& a, cudaStream_t s) {
     const int g = grid_rows(a.rows);
     const int vpt = (a.cols + kThreads * 4 - 1) / (kThreads * 4);
-    if (vpt <= 1) k_quant_rows<1><<<g, kThreads, 0, s>>>(a);
-    else if (vpt <= 2) k_quant_rows<2><<<g, kThreads, 0, s>>>(a);
-    else if (vpt <= 4) k_quant_rows<4><<<g, kThreads, 0, s>>>(a);
-    else if (vpt <= 8) k_quant_rows<8><<<g, kThreads, 0, s>>>(a);
-    else if (vpt <= 16) k_quant_rows<16><<<g, kThreads, 0, s>>>(a);
+    if (vpt <= 1) k_quant_rows<1, RND><<<g, kThreads, 0, s>>>(a);
+    else if (vpt <= 2) k_quant_rows<2, RND><<<g, kThreads, 0, s>>>(a);
+    else if (vpt <= 4) k_quant_rows<4, RND><<<g, kThreads, 0, s>>>(a);
+    else if (vpt <= 8) k_quant_rows<8, RND><<<g, kThreads, 0, s>>>(a);
+    else if (vpt <= 16) k_quant_rows<16, RND><<<g, kThreads, 0, s>>>(a);
     else k_quant_rows_generic<<<g, kThreads, 0, s>>>(a);
 }
 
+void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
+    if (a.rounding == kNearest) {
+        const int g = grid_rows(a.rows);
+        const int vpt = (a.cols + kThreads * 4 - 1) / (kThreads * 4);
+        if (vpt <= 1) k_quant_rows_fast<1, 256><<<g, 256, 0, s>>>(a);
+        else if (vpt <= 2) k_quant_rows_fast<2, 256><<<g, 256, 0, s>>>(a);
+        else if (vpt <= 4) k_quant_rows_fast<2, 512><<<g, 512, 0, s>>>(a);
+        else if (vpt <= 8) k_quant_rows_fast<4, 512><<<g, 512, 0, s>>>(a);
+        else if (vpt <= 16) k_quant_rows_fast<8, 512><<<g, 512, 0, s>>>(a);
+        else k_quant_rows_generic<<<g, kThreads, 0, s>>>(a);
+    } else {
+        quant_rows_rnd<kFloor>(a, s);
+    }
+}
+
+template <class K>
+void set_dyn_smem(K kern, int bytes) {
+    // cheap; the kernels are distinct template instances of the same type
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
 void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {
-    dim3 grid((a.cols + kTN - 1) / kTN, (a.rows + kTK - 1) / kTK);
-    k_quant_cols_T<<<grid, kThreads, 0, s>>>(a);
+    dim3 grid((a.cols + kTN - 1) / kTN, (a.rows + kColTileRows - 1) / kColTileRows);
+    if (a.rounding == kNearest) {
+        set_dyn_smem(k_quant_cols_T_fast, kLutBytes);
+        k_quant_cols_T_fast<<<grid, kThreads, kLutBytes, s>>>(a);
+    } else {
+        set_dyn_smem(k_quant_cols_T<kFloor>, kLutBytes);
+        k_quant_cols_T<kFloor><<<grid, kThreads, kLutBytes, s>>>(a);
+    }
 }
 
 void launch_select_rows(const SelectArgs& a, cudaStream_t s) {
-    const int g = grid_rows(a.rows);
-    const int vpt = (a.cols + kThreads * 4 - 1) / (kThreads * 4);
-    if (vpt <= 1) k_select_rows<1><<<g, kThreads, 0, s>>>(a);
-    else if (vpt <= 2) k_select_rows<2><<<g, kThreads, 0, s>>>(a);
-    else if (vpt <= 4) k_select_rows<4><<<g, kThreads, 0, s>>>(a);
-    else if (vpt <= 8) k_select_rows<8><<<g, kThreads, 0, s>>>(a);
-    else if (vpt <= 16) k_select_rows<16><<<g, kThreads, 0, s>>>(a);
-    else k_select_rows_generic<<<g, kThreads, 0, s>>>(a);
+    if (a.fix_mode) k_fix_rows<<<grid_rows(a.rows), kThreads, 0, s>>>(a);
+    else if (a.rounding == kNearest && (a.ld % 4 == 0) && (a.ldq % 4 == 0) && (a.cols % 4 == 0) &&
+             ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0))
+        k_select_rows_fast<<<grid_rows(a.rows), kThreads, 0, s>>>(a);
+    else if (a.rounding == kNearest) k_select_rows<kNearest><<<grid_rows(a.rows), kThreads, 0, s>>>(a);
+    else k_select_rows<kFloor><<<grid_rows(a.rows), kThreads, 0, s>>>(a);
 }
 
 void launch_select_cols_T(const SelectArgs& a, cudaStream_t s) {
-    dim3 grid((a.cols + kTN - 1) / kTN, (a.rows + kTK - 1) / kTK);
-    k_select_cols_T<<<grid, kThreads, 0, s>>>(a);
+    if (a.fix_mode) {
+        k_fix_cols_T<<<grid_rows(a.cols), kThreads, 0, s>>>(a);
+        return;
+    }
+    dim3 grid((a.cols + kTN - 1) / kTN, (a.rows + kColTileRows - 1) / kColTileRows);
+    if (a.rounding == kNearest) {
+        set_dyn_smem(k_select_cols_T_fast, kLutBytes);
+        k_select_cols_T_fast<<<grid, kThreads, kLutBytes, s>>>(a);
+    } else {
+        set_dyn_smem(k_select_cols_T<kFloor>, kLutBytes);
+        k_select_cols_T<kFloor><<<grid, kThreads, kLutBytes, s>>>(a);
+    }
 }
 
 void launch_lambdas(DevScalars* sc, int bits, cudaStream_t s) { k_lambdas<<<1, 1, 0, s>>>(sc, bits); }

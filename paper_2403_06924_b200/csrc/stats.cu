@@ -31,41 +31,55 @@ __global__ void __launch_bounds__(kThreads)
     const bool vec = (cols % 4 == 0) && c + 3 < cols;
     double cs0 = 0, cs1 = 0, cs2 = 0, cs3 = 0;
     float cm0 = FLT_MAX, cm1 = FLT_MAX, cm2 = FLT_MAX, cm3 = FLT_MAX;
-    for (int rr = 0; rr < kSlabRows; ++rr) {
-        const int r = r0 + rr;
-        if (r >= rows) break;  // uniform across the CTA
-        float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
-        const float* p = d + (int64_t)r * cols + c;
-        if (vec) {
-            f = __ldg(reinterpret_cast<const float4*>(p));
-        } else if (c < cols) {
-            f.x = p[0];
-            if (c + 1 < cols) f.y = p[1];
-            if (c + 2 < cols) f.z = p[2];
-            if (c + 3 < cols) f.w = p[3];
-        }
-        if (POLICY == kAvg) {
-            const double a0 = fabs((double)f.x), a1 = fabs((double)f.y), a2 = fabs((double)f.z),
-                         a3 = fabs((double)f.w);
-            cs0 = __dadd_rn(cs0, a0);
-            cs1 = __dadd_rn(cs1, a1);
-            cs2 = __dadd_rn(cs2, a2);
-            cs3 = __dadd_rn(cs3, a3);
-            double rs = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
-            rs = warp_sumd(rs);
-            if (lane == 0) atomicAdd(row_sum + r, rs);
-        } else {
-            const bool in0 = c < cols, in1 = c + 1 < cols, in2 = c + 2 < cols, in3 = c + 3 < cols;
-            const float a0 = in0 ? fabsf(f.x) : FLT_MAX, a1 = in1 ? fabsf(f.y) : FLT_MAX,
-                        a2 = in2 ? fabsf(f.z) : FLT_MAX, a3 = in3 ? fabsf(f.w) : FLT_MAX;
-            cm0 = fminf(cm0, a0);
-            cm1 = fminf(cm1, a1);
-            cm2 = fminf(cm2, a2);
-            cm3 = fminf(cm3, a3);
-            float rm = fminf(fminf(a0, a1), fminf(a2, a3));
+    constexpr int kBatch = 8;  // rows loaded ahead of the (serialising) reductions
+    for (int rb = 0; rb < kSlabRows; rb += kBatch) {
+        if (r0 + rb >= rows) break;  // uniform across the CTA
+        float4 fv[kBatch];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) rm = fminf(rm, __shfl_xor_sync(0xffffffffu, rm, o));
-            if (lane == 0) atomicMin(row_min + r, fbits(rm));
+        for (int u = 0; u < kBatch; ++u) {
+            const int r = r0 + rb + u;
+            float4 f = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float* p = d + (int64_t)r * cols + c;
+            if (r < rows) {
+                if (vec) {
+                    f = __ldg(reinterpret_cast<const float4*>(p));
+                } else if (c < cols) {
+                    f.x = p[0];
+                    if (c + 1 < cols) f.y = p[1];
+                    if (c + 2 < cols) f.z = p[2];
+                    if (c + 3 < cols) f.w = p[3];
+                }
+            }
+            fv[u] = f;
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int r = r0 + rb + u;
+            const float4 f = fv[u];
+            if (POLICY == kAvg) {
+                const double a0 = fabs((double)f.x), a1 = fabs((double)f.y), a2 = fabs((double)f.z),
+                             a3 = fabs((double)f.w);
+                cs0 = __dadd_rn(cs0, a0);
+                cs1 = __dadd_rn(cs1, a1);
+                cs2 = __dadd_rn(cs2, a2);
+                cs3 = __dadd_rn(cs3, a3);
+                double rs = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+                rs = warp_sumd(rs);
+                if (lane == 0 && r < rows) atomicAdd(row_sum + r, rs);
+            } else {
+                const bool in0 = c < cols, in1 = c + 1 < cols, in2 = c + 2 < cols, in3 = c + 3 < cols;
+                const bool rin = r < rows;
+                const float a0 = in0 && rin ? fabsf(f.x) : FLT_MAX, a1 = in1 && rin ? fabsf(f.y) : FLT_MAX,
+                            a2 = in2 && rin ? fabsf(f.z) : FLT_MAX, a3 = in3 && rin ? fabsf(f.w) : FLT_MAX;
+                cm0 = fminf(cm0, a0);
+                cm1 = fminf(cm1, a1);
+                cm2 = fminf(cm2, a2);
+                cm3 = fminf(cm3, a3);
+                float rm = fminf(fminf(a0, a1), fminf(a2, a3));
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) rm = fminf(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+                if (lane == 0 && rin) atomicMin(row_min + r, fbits(rm));
+            }
         }
     }
     if (c < cols) {
@@ -133,8 +147,10 @@ __global__ void __launch_bounds__(kThreads)
                 buf[t] = d[off];
             }
             __syncthreads();
-            if (threadIdx.x == 0)
+            if (threadIdx.x == 0) {
+#pragma unroll 16
                 for (int t = 0; t < cnt; ++t) s = __dadd_rn(s, fabs((double)buf[t]));
+            }
             __syncthreads();
         }
         if (threadIdx.x == 0) {
