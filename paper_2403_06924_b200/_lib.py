@@ -53,6 +53,7 @@ _F = C.c_float
 _SIGS = {
     "xg_last_error": (C.c_char_p, []),
     "xg_version": (_I, []),
+    "xg_config_default": (XgConfig, []),
     "xg_device_ok": (_I, []),
     "xg_workspace_release": (_I, []),
     "xg_launch_count": (_I64, [_I]),
