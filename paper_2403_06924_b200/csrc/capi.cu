@@ -615,6 +615,63 @@ xg_status xg_gemm_i8(const int8_t* a, const int8_t* b, int m, int k, int n, int 
     });
 }
 
+// Development probe (not part of the reference API): times the DF GEMM kernel
+// on zero operands with debug flags (1: no TMA loads, 2: no epilogue).
+extern "C" int xg_generate(int kind, double p1, double p2, uint64_t seed, int64_t n, float* out,
+                           void* stream);
+extern "C" double xg_debug_gemm_df(int m, int n, int k, int flags, int iters) {
+    double ms_out = -1.0;
+    guarded([&] {
+        cudaStream_t s = nullptr;
+        Scratch S(s);
+        const int64_t ldk = pad16(k);
+        int8_t* a = S.get<int8_t>(m * ldk);
+        int8_t* bt = S.get<int8_t>(n * ldk);
+        float* out = S.get<float>((int64_t)m * n);
+        double* la = S.get<double>(m);
+        double* lb = S.get<double>(n);
+        // random int8 operands in [-127, 127] (flag 16: zeros), scales 1.0
+        if (flags & 16) {
+            ck(cudaMemsetAsync(a, 0, m * ldk, s), "memset");
+            ck(cudaMemsetAsync(bt, 0, n * ldk, s), "memset");
+        } else {
+            xg::random_i8(a, m * ldk, 11, s);
+            xg::random_i8(bt, n * ldk, 12, s);
+        }
+        {   // scales of realistic magnitude: lambda = 127 / max (~30), not powers of two
+            std::vector<double> h((size_t)(m > n ? m : n));
+            for (size_t i = 0; i < h.size(); ++i) h[i] = 127.0 / (3.0 + 0.001 * (double)(i % 977));
+            ck(cudaMemcpyAsync(la, h.data(), 8 * (size_t)m, cudaMemcpyHostToDevice, s), "h2d");
+            ck(cudaMemcpyAsync(lb, h.data(), 8 * (size_t)n, cudaMemcpyHostToDevice, s), "h2d");
+            ck(cudaStreamSynchronize(s), "sync");
+        }
+        xg::KOperand ops[2] = {{a, m, ldk}, {bt, n, ldk}};
+        int isb[2] = {0, 1};
+        xg::GemmArgs g{};
+        g.M = m; g.N = n; g.K = k;
+        g.amap[0][0] = g.amap[0][1] = 0;
+        g.bmap[0][0] = g.bmap[0][1] = 1;
+        g.out_f32 = out;
+        g.rs[0][0] = g.rs[0][1] = sref(la, 1);
+        g.cs[0][0] = g.cs[0][1] = sref(lb, 1);
+        g.debug = flags;
+        for (int i = 0; i < 2; ++i) xg::gemm_i8(xg::EPI_DF, ops, isb, 2, g, s);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, s);
+        for (int i = 0; i < iters; ++i) xg::gemm_i8(xg::EPI_DF, ops, isb, 2, g, s);
+        cudaEventRecord(e1, s);
+        ck(cudaEventSynchronize(e1), "sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ms_out = ms / iters;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+    return ms_out;
+}
+
 xg_status xg_gemm_direct_q(const int8_t* aq, int scheme_a, const double* sa, const int8_t* bq,
                            int scheme_b, const double* sb, int m, int k, int n, int bits_a,
                            int bits_b, float* out, xg_stream s) {

@@ -137,6 +137,36 @@ __device__ __forceinline__ float dequant_product_fast(int32_t p, double ia, doub
     if (float_round_safe(y)) return __double2float_rn(y);
     return dequant_product_value(p, la, lb);
 }
+// Same with the column scale fetched only on the (rare) slow path.
+__device__ __forceinline__ float dequant_product_fast2(int32_t p, double ia, double ib, double la,
+                                                       const double* lb_ptr) {
+    if (p == 0) return 0.0f;
+    const double y = __dmul_rn(__dmul_rn((double)p, ia), ib);
+    if (float_round_safe(y)) return __double2float_rn(y);
+    return dequant_product_value(p, la, *lb_ptr);
+}
+// Conversion-free variant.  On this part I2F.F64 and F2F.F32.F64 issue at
+// ~16 and ~12 per clock per SM (measured, tools/microbench/pipes.cu) against
+// 62 DMUL, so: p -> double exactly via the 2^52 + 2^31 magic constant (one
+// DADD), and once float_round_safe has proven y is not near a float rounding
+// boundary, RN_f(y) is assembled from y's bits with integer ops (exponent
+// rebias by xor, 23-bit mantissa by a funnel shift, round bit added with carry).
+// Returns the float; sets `slow` if the exact division is required.
+__device__ __forceinline__ float dq_bits(int32_t p, double ia, double ib, bool& slow) {
+    const double pd = __dsub_rn(__hiloint2double(0x43300000, (int)((uint32_t)p ^ 0x80000000u)),
+                                4503601774854144.0);  // 2^52 + 2^31
+    const double y = __dmul_rn(__dmul_rn(pd, ia), ib);
+    const uint32_t hi = (uint32_t)__double2hiint(y), lo = (uint32_t)__double2loint(y);
+    const uint32_t e = (hi >> 20) & 0x7ffu;
+    const int low = (int)(lo & 0x1fffffffu) - 0x10000000;
+    const bool ok = e >= 1023u - 126u && e <= 1023u + 126u && (low > 64 || low < -64);
+    slow |= !ok && p != 0;
+    uint32_t f = __funnelshift_l(lo, hi, 3);                     // hi[28:0] . lo[31:29]
+    f = ((f ^ 0x40000000u) & 0x7fffffffu) | (hi & 0x80000000u);  // exponent 1023 -> 127 bias
+    f += (lo >> 28) & 1u;                                        // round to nearest (not a tie)
+    return p == 0 ? 0.0f : __uint_as_float(f);
+}
+
 // float(q / lambda) with il = RN(1/lambda)
 __device__ __forceinline__ float dequant_fast(int q, double il, double lambda) {
     if (q == 0) return 0.0f;
@@ -242,6 +272,36 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_
         : "memory");
 }
 
+// 1-D bulk copy global -> shared (size and addresses multiples of 16 bytes).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// order prior generic-proxy shared accesses before subsequent async-proxy ones
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// TMA 2-D store shared -> global (bulk-group completion).
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap),
+                 "r"(smem_u32(src)), "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N committed bulk groups still read their shared source
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ------------------------------------------------------------ PTX: tcgen05 --
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -316,6 +376,24 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, ui
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
         "l"(tmap), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y)
+        : "memory");
+}
+// 2SM TMA load multicast to the CTAs in `mask`; completion is counted on the
+// pair-leader barrier of each destination.
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const void* tmap, uint64_t* bar, int x, int y,
+                                                    uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(tmap), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y), "h"(mask)
+        : "memory");
+}
+// commit arriving on the barrier at the same offset in every CTA of `mask`
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
         : "memory");
 }
 // commit arriving on the barrier at the same offset in both CTAs of the pair

@@ -44,6 +44,19 @@ void encode(CUtensorMap* m, const KOperand& op, int K, int box_rows) {
         throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
+// fp32 M x N row-major matrix, 32x32 boxes, 128-byte swizzle (epilogue tiles)
+void encode_f32_sw128(CUtensorMap* m, const float* p, int rows, int cols) {
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw std::runtime_error("cuTensorMapEncodeTiled (f32) failed: " + std::to_string((int)r));
+}
+
 int sm_count() {
     static int n = 0;
     if (!n) {
@@ -73,23 +86,48 @@ void run(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, c
     kern<<<grid, 256, Cfg::SMEM_BYTES, s>>>(maps, args);
 }
 
-template <int NACC, int EPI>
-void run2(const KOperand* ops, int nops, const GemmArgs& args, cudaStream_t s) {
+template <int NACC, int EPI, int PAIRS>
+void run2(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, cudaStream_t s) {
     using Cfg = Gemm2Cfg<NACC>;
     TmaMaps maps;
     std::memset(&maps, 0, sizeof maps);
-    for (int i = 0; i < nops; ++i) encode(&maps.m[i], ops[i], args.K, 128);
+    for (int i = 0; i < nops; ++i) encode(&maps.m[i], ops[i], args.K, is_b[i] ? 128 / PAIRS : 128);
     for (int i = nops; i < kMaxMaps; ++i) maps.m[i] = maps.m[0];
-    auto kern = k_gemm_i8_tc2<NACC, EPI>;
+    auto kern = k_gemm_i8_tc2<NACC, EPI, PAIRS>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
         attr_set = true;
     }
-    const int tiles = ((args.M + 255) / 256) * ((args.N + 255) / 256);
-    const int pairs = sm_count() / 2;
-    const int grid = 2 * (tiles < pairs ? tiles : pairs);
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(maps, args);
+    const int csize = 2 * PAIRS;
+    const int tiles = ((args.M + 256 * PAIRS - 1) / (256 * PAIRS)) * ((args.N + 255) / 256);
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(Cfg::THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    // persistent grid: only as many clusters as can be co-resident (4-CTA
+    // clusters cannot use every SM), so no cluster waits for a second wave
+    static int max_clusters = 0;
+    if (!max_clusters) {
+        cfg.gridDim = dim3(csize * 512);
+        if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters <= 0) {
+            cudaGetLastError();
+            max_clusters = sm_count() / csize;
+        }
+    }
+    cfg.gridDim = dim3(csize * (tiles < max_clusters ? tiles : max_clusters));
+    EpiMaps em;
+    std::memset(&em, 0, sizeof em);
+    encode_f32_sw128(&em.out, args.out_f32, args.M, args.N);
+    encode_f32_sw128(&em.din, EPI == EPI_COMP ? args.df_in : args.out_f32, args.M, args.N);
+    cudaLaunchKernelEx(&cfg, kern, maps, args, em);
 }
 
 bool use_pair_kernel(const GemmArgs& args) {
@@ -100,15 +138,37 @@ bool use_pair_kernel(const GemmArgs& args) {
     return !env && args.M >= 256;
 }
 
+int pair_count(const GemmArgs& args) {
+    static const int env = [] {
+        const char* e = getenv("XG_GEMM_PAIRS");
+        return e ? atoi(e) : 0;
+    }();
+    if (env == 1 || env == 2) return env;
+    return 1;  // 4-CTA multicast measured slower on B200 (fewer co-resident clusters); opt-in only
+}
+
 }  // namespace
+
+bool make_tmap_f32(void* tmap, const float* p, int rows, int cols, int64_t ld, int box_cols,
+                   int box_rows) {
+    if ((reinterpret_cast<uintptr_t>(p) & 15) || ((ld * 4) % 16)) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return encode_fn()(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims,
+                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const GemmArgs& args,
              cudaStream_t s) {
-    if (use_pair_kernel(args) && epi != EPI_FULL3) {
+    // the pair kernel's TMA-store epilogue needs 16-byte row pitch for the fp32 maps
+    if (use_pair_kernel(args) && (epi == EPI_DF || epi == EPI_COMP) && (args.N % 4) == 0) {
+        const bool mc = pair_count(args) == 2;
         switch (epi) {
-            case EPI_S32: run2<1, EPI_S32>(ops, nops, args, s); return;
-            case EPI_DF: run2<1, EPI_DF>(ops, nops, args, s); return;
-            case EPI_COMP: run2<2, EPI_COMP>(ops, nops, args, s); return;
+            case EPI_DF: mc ? run2<1, EPI_DF, 2>(ops, is_b, nops, args, s) : run2<1, EPI_DF, 1>(ops, is_b, nops, args, s); return;
+            case EPI_COMP: mc ? run2<2, EPI_COMP, 2>(ops, is_b, nops, args, s) : run2<2, EPI_COMP, 1>(ops, is_b, nops, args, s); return;
         }
     }
     switch (epi) {

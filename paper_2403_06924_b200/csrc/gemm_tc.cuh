@@ -40,6 +40,12 @@ struct TmaMaps {
     CUtensorMap m[kMaxMaps];
 };
 
+// fp32 M x N output (and D_F input) maps: 32x32 boxes, 128-byte swizzle.
+struct EpiMaps {
+    CUtensorMap out;
+    CUtensorMap din;
+};
+
 struct GemmArgs {
     int M, N, K;
     // operand map indices for accumulator a: [a][sel]
@@ -56,6 +62,7 @@ struct GemmArgs {
     // row scales / col scales per accumulator, [acc][sel]
     ScaleRef rs[3][2];
     ScaleRef cs[3][2];
+    int debug;  // probes: bit 0 skip TMA loads (MMA on stale smem), bit 1 skip epilogue work
 };
 
 template <int BN, int NACC>
@@ -370,36 +377,56 @@ struct Gemm2Cfg {
     static constexpr int A_BYTES = BM * BK;
     static constexpr int B_BYTES = BNH * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = 6;
+    static constexpr int STAGES = NACC == 1 ? 5 : 4;
     static constexpr int ACC_COLS = NACC * BN;
     static constexpr int ACC_BUFS = (512 / ACC_COLS) >= 2 ? 2 : 1;
     static constexpr int TMEM_COLS = 512;
     static constexpr int THREADS = 384;
     static constexpr int EPI_WARPS = 8;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+    // per epilogue warp: NSTG staging tiles of 32x32 fp32 (128B-swizzled, TMA
+    // store / load) and NACC x 32 fp64 column reciprocals
+    static constexpr int NSTG = NACC == 1 ? 1 : 2;
+    static constexpr int STG_BYTES = 32 * 32 * 4;
+    static constexpr int EPI_BYTES = EPI_WARPS * NSTG * STG_BYTES;
+    static constexpr int SCL_BYTES = EPI_WARPS * NACC * 32 * 8;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + SCL_BYTES + 1024 + 512;
     static constexpr int GROUP_M = 8;  // in 256-row units
     static_assert(ACC_COLS * ACC_BUFS <= 512, "TMEM overflow");
 };
 
-template <int NACC, int EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
-    k_gemm_i8_tc2(const __grid_constant__ TmaMaps maps, const GemmArgs args) {
+// PAIRS = 2: a 4-CTA cluster of two pairs stacked along M sharing B^T tiles
+// through TMA multicast (opt-in: measured slower on B200, fewer co-resident
+// clusters).  Stages may only be overwritten once BOTH pairs' MMAs are done, so
+// the MMA commits that free stages are multicast to all four CTAs.
+//
+// Epilogue: TMEM -> registers -> exact dequant -> 128B-swizzled smem tile ->
+// TMA store; EPI_COMP prefetches its D_F tile by TMA into the same staging
+// tile while the accumulator is still being produced.
+template <int NACC, int EPI, int PAIRS>
+__global__ void __launch_bounds__(384, 1)
+    k_gemm_i8_tc2(const __grid_constant__ TmaMaps maps, const GemmArgs args,
+                  const __grid_constant__ EpiMaps emaps) {
     using Cfg = Gemm2Cfg<NACC>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+    float* epi_stage = (float*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);  // 1024-aligned
+    double* epi_scale = (double*)((uint8_t*)epi_stage + Cfg::EPI_BYTES);
+    uint64_t* full = (uint64_t*)((uint8_t*)epi_scale + Cfg::SCL_BYTES);
     uint64_t* empty = full + Cfg::STAGES;
     uint64_t* tfull = empty + Cfg::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    uint64_t* dbar = tempty + 2;  // [EPI_WARPS][2] D_F tile loads
+    uint32_t* tmem_slot = (uint32_t*)(dbar + 2 * Cfg::EPI_WARPS);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
-    const bool leader = rank == 0;
-    const int cluster_id = blockIdx.x >> 1;
-    const int nclusters = gridDim.x >> 1;
-    const int num_m = (args.M + 2 * Cfg::BM - 1) / (2 * Cfg::BM);
+    const uint32_t prank = rank & 1;                 // rank inside the pair
+    const uint32_t pair = rank >> 1;                 // pair inside the cluster
+    const bool leader = prank == 0;                  // pair leader issues the MMA
+    const int cluster_id = blockIdx.x / (2 * PAIRS);
+    const int nclusters = gridDim.x / (2 * PAIRS);
+    const int num_m = (args.M + 2 * PAIRS * Cfg::BM - 1) / (2 * PAIRS * Cfg::BM);
     const int num_n = (args.N + Cfg::BN - 1) / Cfg::BN;
     const int num_tiles = num_m * num_n;
     const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
@@ -408,16 +435,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < Cfg::STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], PAIRS);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 2 * Cfg::EPI_WARPS);
         }
+        for (int b = 0; b < 2 * Cfg::EPI_WARPS; ++b) mbar_init(&dbar[b], 1);
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < kMaxMaps; ++i) tma_prefetch(&maps.m[i]);
+        tma_prefetch(&emaps.out);
+        tma_prefetch(&emaps.din);
     }
     if (warp == 2) tmem_alloc2(tmem_slot, Cfg::TMEM_COLS);
     tc_fence_before();
@@ -433,16 +463,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             for (int t = cluster_id; t < num_tiles; t += nclusters) {
                 int mb, nb;
                 tile_coords(t, num_m, num_n, Cfg::GROUP_M, mb, nb);
-                const int arow = mb * 2 * Cfg::BM + (int)rank * Cfg::BM;
-                const int brow = nb * Cfg::BN + (int)rank * Cfg::BNH;
+                const int arow = (mb * PAIRS + (int)pair) * 2 * Cfg::BM + (int)prank * Cfg::BM;
+                const int brow = nb * Cfg::BN + (int)prank * Cfg::BNH + (int)pair * (Cfg::BNH / PAIRS);
                 for (int kb = 0; kb < nkb; ++kb) {
                     for (int a = 0; a < NACC; ++a) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
                         uint8_t* sB = sA + Cfg::A_BYTES;
-                        if (leader) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
-                        tma_load_2d_pair(sA, &maps.m[args.amap[a][sel]], &full[stage], kb * Cfg::BK, arow);
-                        tma_load_2d_pair(sB, &maps.m[args.bmap[a][sel]], &full[stage], kb * Cfg::BK, brow);
+                        if (args.debug & 1) {  // probe: MMA on stale smem
+                            if (leader) mbar_arrive(&full[stage]);
+                        } else {
+                            if (leader) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+                            tma_load_2d_pair(sA, &maps.m[args.amap[a][sel]], &full[stage], kb * Cfg::BK, arow);
+                            if (PAIRS == 1) {
+                                tma_load_2d_pair(sB, &maps.m[args.bmap[a][sel]], &full[stage], kb * Cfg::BK, brow);
+                            } else {
+                                tma_load_2d_pair_mc(sB + pair * (Cfg::B_BYTES / PAIRS), &maps.m[args.bmap[a][sel]],
+                                                    &full[stage], kb * Cfg::BK, brow,
+                                                    (uint16_t)((1u << rank) | (1u << (rank ^ 2u))));
+                            }
+                        }
                         if (++stage == Cfg::STAGES) {
                             stage = 0;
                             phase ^= 1;
@@ -474,14 +514,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                         for (int k = 0; k < Cfg::BK / 32; ++k)
                             mma_i8_pair(dbase + a * Cfg::BN, da + 2 * k, db + 2 * k, idesc,
                                         (kb | k) != 0 ? 1u : 0u);
-                        tc_commit_pair(&empty[stage]);
+                        if (PAIRS == 1) tc_commit_pair(&empty[stage]);
+                        else tc_commit_mc(&empty[stage], (uint16_t)0xF);
                         if (++stage == Cfg::STAGES) {
                             stage = 0;
                             phase ^= 1;
                         }
                     }
                 }
-                tc_commit_pair(&tfull[buf]);
+                if (PAIRS == 1) tc_commit_pair(&tfull[buf]);
+                else tc_commit_mc(&tfull[buf], (uint16_t)(3u << (2 * pair)));
                 if (++buf == Cfg::ACC_BUFS) {
                     buf = 0;
                     bphase ^= 1;
@@ -490,45 +532,139 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         }
     } else if (warp >= 4) {
         // ===================== epilogue (8 warps per CTA) =====================
-        const int q = warp & 3;          // TMEM lane quadrant
+        const int q = warp & 3;            // TMEM lane quadrant
         const int half = (warp - 4) >> 2;  // 128-column half of the tile
-        const uint32_t tempty_leader0 = mapa_shared(&tempty[0], 0);
+        const int we = warp - 4;           // epilogue warp index 0..7
+        const uint32_t tempty_leader0 = mapa_shared(&tempty[0], rank & ~1u);
+        float* stg[2] = {epi_stage + we * Cfg::NSTG * 1024,
+                         epi_stage + (we * Cfg::NSTG + Cfg::NSTG - 1) * 1024};
+        double* scw = epi_scale + we * NACC * 32;
+        uint64_t* mybar = dbar + 2 * we;
+        uint32_t dph[2] = {0, 0};
+        const int sw = lane & 7;  // 128B swizzle: chunk k of row `lane` sits at k ^ (lane & 7)
         int buf = 0;
         uint32_t bphase = 0;
         for (int t = cluster_id; t < num_tiles; t += nclusters) {
             int mb, nb;
             tile_coords(t, num_m, num_n, Cfg::GROUP_M, mb, nb);
+            const int rowbase = (mb * PAIRS + (int)pair) * 2 * Cfg::BM + (int)prank * Cfg::BM + q * 32;
+            const int row = rowbase + lane;
+            const bool row_ok = row < args.M;
+            const int colbase = nb * Cfg::BN + half * (Cfg::BN / 2);
+            const int nchunk = (args.debug & 2) ? 0 : min(Cfg::BN / 2 / 32, (args.N - colbase + 31) / 32);
+            if (EPI == EPI_COMP && lane == 0 && nchunk > 0) {  // D_F chunk 0 while the MMA still runs
+                bulk_wait_read<0>();
+                mbar_expect_tx(&mybar[0], Cfg::STG_BYTES);
+                tma_load_2d(stg[0], &emaps.din, &mybar[0], colbase, rowbase);
+            }
             mbar_wait(&tfull[buf], bphase);
             tc_fence_after();
-            const int row = mb * 2 * Cfg::BM + (int)rank * Cfg::BM + q * 32 + lane;
-            const bool row_ok = row < args.M;
-            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * Cfg::ACC_COLS +
-                                   half * (Cfg::BN / 2);
-            double r0 = 1.0, r1 = 1.0, r2 = 1.0;
-            if (EPI != EPI_S32 && row_ok) {
+            double r0 = 1.0, r1 = 1.0;
+            if (row_ok) {
                 r0 = args.rs[0][sel].at(row);
                 if (NACC > 1) r1 = args.rs[1][sel].at(row);
             }
-            const double i0 = __ddiv_rn(1.0, r0), i1 = __ddiv_rn(1.0, r1), i2 = 1.0;
+            const double i0 = __ddiv_rn(1.0, r0), i1 = __ddiv_rn(1.0, r1);
+            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * Cfg::ACC_COLS +
+                                   half * (Cfg::BN / 2);
 #pragma unroll 1
-            for (int c = 0; c < Cfg::BN / 2 / 32; ++c) {
+            for (int c = 0; c < nchunk; ++c) {
+                const int col0 = colbase + c * 32;
+                const int sb = (Cfg::NSTG == 2) ? (c & 1) : 0;
+                float* tile = stg[sb];
+                if (EPI == EPI_COMP && lane == 0 && c + 1 < nchunk) {  // prefetch the next D_F chunk
+                    bulk_wait_read<0>();
+                    mbar_expect_tx(&mybar[(c + 1) & 1], Cfg::STG_BYTES);
+                    tma_load_2d(stg[(c + 1) & 1], &emaps.din, &mybar[(c + 1) & 1], col0 + 32, rowbase);
+                }
+                // column reciprocals of this chunk, broadcast through shared memory
+                const int mycol = min(col0 + lane, args.N - 1);
+                scw[lane] = __ddiv_rn(1.0, args.cs[0][sel].at(mycol));
+                if (NACC > 1) scw[32 + lane] = __ddiv_rn(1.0, args.cs[1][sel].at(mycol));
                 uint32_t acc[NACC][32];
 #pragma unroll
                 for (int a = 0; a < NACC; ++a) tmem_ld32(tbase + a * Cfg::BN + c * 32, acc[a]);
                 tmem_ld_wait();
-                const int col0 = nb * Cfg::BN + half * (Cfg::BN / 2) + c * 32;
-                if (col0 < args.N)
-                    epilogue_chunk<NACC, EPI>(args, sel, acc, row, col0, r0, r1, r2, i0, i1, i2, row_ok);
+                if (c == nchunk - 1) {  // accumulator drained: hand TMEM back to the MMA early
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tempty_leader0 + buf * 8);
+                }
+                if (EPI == EPI_COMP) {
+                    mbar_wait(&mybar[sb], dph[sb]);
+                    dph[sb] ^= 1;
+                } else if (lane == 0) {
+                    bulk_wait_read<0>();  // staging tile free again
+                }
+                __syncwarp();
+                float4* rowp = reinterpret_cast<float4*>(tile + lane * 32);
+                float res[32];
+                if constexpr (EPI == EPI_DF) {
+                    bool slow = false;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) res[j] = dq_bits((int32_t)acc[0][j], i0, scw[j], slow);
+                    if (slow) {  // rare: redo the chunk with the reference's fp64 division
+                        const ScaleRef c0 = args.cs[0][sel];
+                        for (int j = 0; j < 32; ++j)
+                            res[j] = dequant_product_value((int32_t)acc[0][j], r0,
+                                                           c0.at(min(col0 + j, args.N - 1)));
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const float4 d = rowp[k ^ sw];
+                        res[4 * k] = d.x; res[4 * k + 1] = d.y; res[4 * k + 2] = d.z; res[4 * k + 3] = d.w;
+                    }
+                    const ScaleRef c0 = args.cs[0][sel], c1 = args.cs[1][sel];
+                    const float* cin = args.c_in + (int64_t)row * args.N + col0;
+                    float t1[32], t2[32];
+                    bool slow = false;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        t1[j] = dq_bits((int32_t)acc[0][j], i0, scw[j], slow);
+                        t2[j] = dq_bits((int32_t)acc[1 % NACC][j], i1, scw[32 + j], slow);
+                    }
+                    if (slow) {  // rare: redo the chunk with the reference's fp64 division
+                        for (int j = 0; j < 32; ++j) {
+                            const int cj = min(col0 + j, args.N - 1);
+                            t1[j] = dequant_product_value((int32_t)acc[0][j], r0, c0.at(cj));
+                            t2[j] = dequant_product_value((int32_t)acc[1 % NACC][j], r1, c1.at(cj));
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        float v = __fadd_rn(__fadd_rn(res[j], t1[j]), t2[j]);  // pipeline.cpp:141-145
+                        if (args.has_c) {                                // pipeline.cpp:195-202
+                            const float cv = (row_ok && col0 + j < args.N) ? cin[j] : 0.0f;
+                            v = __fadd_rn(__fmul_rn(args.alpha, v), __fmul_rn(args.beta, cv));
+                        } else if (args.alpha != 1.0f) {
+                            v = __fmul_rn(v, args.alpha);
+                        }
+                        res[j] = v;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    rowp[k ^ sw] = make_float4(res[4 * k], res[4 * k + 1], res[4 * k + 2], res[4 * k + 3]);
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&emaps.out, tile, col0, rowbase);
+                    bulk_commit();
+                }
                 __syncwarp();
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(tempty_leader0 + buf * 8);
+            if (nchunk <= 0) {  // nothing to store (N edge / probe): still release the accumulator
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tempty_leader0 + buf * 8);
+            }
             if (++buf == Cfg::ACC_BUFS) {
                 buf = 0;
                 bphase ^= 1;
             }
         }
+        if (lane == 0) bulk_wait<0>();  // every store landed before exit
     }
     tc_fence_before();
     cluster_sync_all();

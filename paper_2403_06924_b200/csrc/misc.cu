@@ -271,7 +271,20 @@ __global__ void k_finite_max(const float* __restrict__ x, int64_t n, uint32_t* m
     }
 }
 
+__global__ void k_random_i8(int8_t* p, int64_t n, uint64_t seed) {
+    GRID_STRIDE(i, n) {
+        uint64_t z = seed + (uint64_t)i * 0x9E3779B97F4A7C15ULL;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        p[i] = (int8_t)((int)((z ^ (z >> 31)) % 255) - 127);
+    }
+}
+
 }  // namespace
+
+void random_i8(int8_t* p, int64_t n, uint64_t seed, cudaStream_t s) {
+    k_random_i8<<<blocks_for(n), kT, 0, s>>>(p, n, seed);
+}
 
 void transpose_i8(const int8_t* src, int rows, int cols, int64_t lds, int8_t* dst, int64_t ldd,
                   cudaStream_t s) {

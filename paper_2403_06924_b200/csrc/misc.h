@@ -38,6 +38,7 @@ void spmm_i8(int rows, const int32_t* rp, const int32_t* ci, const int8_t* v, co
              int d_cols, int32_t* out, cudaStream_t s);
 void spmm_f32(int rows, const int32_t* rp, const int32_t* ci, const float* v, const float* d,
               int d_cols, float* out, cudaStream_t s);
+void random_i8(int8_t* p, int64_t n, uint64_t seed, cudaStream_t s);  // uniform in [-127, 127]
 void densify(int rows, int cols, const int32_t* rp, const int32_t* ci, const float* v, float* out,
              cudaStream_t s);
 
