@@ -18,6 +18,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -257,6 +258,42 @@ void gemm_comp(Pipe& p, float* out, const float* c, float alpha, float beta) {
     KOperand ops[6] = {{p.aq, p.M, p.ldk},  {p.ared, p.M, p.ldk}, {p.rbqT, p.N, p.ldk},
                        {p.raq, p.M, p.ldk}, {p.bqT, p.N, p.ldk},  {p.bredT, p.N, p.ldk}};
     int isb[6] = {0, 0, 1, 0, 1, 1};
+    // dr1 = X1 * RBq : left scale (aq or a_red) per row / per tensor, right lambda_RB
+    const ScaleRef r1d = p.vw ? sref(p.la, 1) : sref(&p.sc->lamA, 0);
+    const ScaleRef r1s = p.vw ? sref(p.la, 1) : sref(&p.sc->lamAred, 0);
+    const ScaleRef c1 = sref(&p.sc->lamRB, 0);
+    // dr2 = RAq * Y2 : lambda_RA, right scale (bq or b_red)
+    const ScaleRef r2 = sref(&p.sc->lamRA, 0);
+    const ScaleRef c2d = p.vw ? sref(p.lb, 1) : sref(&p.sc->lamB, 0);
+    const ScaleRef c2s = p.vw ? sref(p.lb, 1) : sref(&p.sc->lamBred, 0);
+    if (p.M >= 256 && (p.N % 4) == 0 && !getenv("XG_GEMM_1CTA")) {
+        // Two single-accumulator pair GEMMs with double-buffered TMEM (pipeline.cpp:141-145
+        // order): out = fl(D_F + deq(dr1)), then out = fl(out + deq(dr2)) and alpha/beta.
+        GemmArgs g{};
+        g.M = p.M; g.N = p.N; g.K = p.K;
+        g.sel_ptr = &p.sc->sel;
+        g.out_f32 = out;
+        g.df_in = out;
+        g.c_in = c;
+        g.has_c = c != nullptr;
+        g.alpha = alpha;
+        g.beta = beta;
+        g.amap[0][0] = 0; g.amap[0][1] = 1;
+        g.bmap[0][0] = 2; g.bmap[0][1] = 2;
+        g.rs[0][0] = r1d; g.rs[0][1] = r1s;
+        g.cs[0][0] = c1; g.cs[0][1] = c1;
+        g.finalize = 0;
+        gemm_i8(EPI_ACC, ops, isb, 6, g, p.s);
+        check_launch("gemm compensate dr1");
+        g.amap[0][0] = 3; g.amap[0][1] = 3;
+        g.bmap[0][0] = 4; g.bmap[0][1] = 5;
+        g.rs[0][0] = r2; g.rs[0][1] = r2;
+        g.cs[0][0] = c2d; g.cs[0][1] = c2s;
+        g.finalize = 1;
+        gemm_i8(EPI_ACC, ops, isb, 6, g, p.s);
+        check_launch("gemm compensate dr2");
+        return;
+    }
     GemmArgs g{};
     g.M = p.M; g.N = p.N; g.K = p.K;
     g.amap[0][0] = 0; g.amap[0][1] = 1;   // X1: dense Aq | sparse A'q
@@ -270,14 +307,10 @@ void gemm_comp(Pipe& p, float* out, const float* c, float alpha, float beta) {
     g.has_c = c != nullptr;
     g.alpha = alpha;
     g.beta = beta;
-    // dr1 = X1 * RBq : left scale (aq or a_red) per row / per tensor, right lambda_RB
-    g.rs[0][0] = p.vw ? sref(p.la, 1) : sref(&p.sc->lamA, 0);
-    g.rs[0][1] = p.vw ? sref(p.la, 1) : sref(&p.sc->lamAred, 0);
-    g.cs[0][0] = g.cs[0][1] = sref(&p.sc->lamRB, 0);
-    // dr2 = RAq * Y2 : lambda_RA, right scale (bq or b_red)
-    g.rs[1][0] = g.rs[1][1] = sref(&p.sc->lamRA, 0);
-    g.cs[1][0] = p.vw ? sref(p.lb, 1) : sref(&p.sc->lamB, 0);
-    g.cs[1][1] = p.vw ? sref(p.lb, 1) : sref(&p.sc->lamBred, 0);
+    g.rs[0][0] = r1d; g.rs[0][1] = r1s;
+    g.cs[0][0] = g.cs[0][1] = c1;
+    g.rs[1][0] = g.rs[1][1] = r2;
+    g.cs[1][0] = c2d; g.cs[1][1] = c2s;
     gemm_i8(EPI_COMP, ops, isb, 6, g, p.s);
     check_launch("gemm compensate");
 }

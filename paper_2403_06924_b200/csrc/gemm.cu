@@ -88,7 +88,7 @@ void run(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, c
 
 template <int NACC, int EPI, int PAIRS>
 void run2(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, cudaStream_t s) {
-    using Cfg = Gemm2Cfg<NACC>;
+    using Cfg = Gemm2Cfg<NACC, EPI>;
     TmaMaps maps;
     std::memset(&maps, 0, sizeof maps);
     for (int i = 0; i < nops; ++i) encode(&maps.m[i], ops[i], args.K, is_b[i] ? 128 / PAIRS : 128);
@@ -126,7 +126,7 @@ void run2(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, 
     EpiMaps em;
     std::memset(&em, 0, sizeof em);
     encode_f32_sw128(&em.out, args.out_f32, args.M, args.N);
-    encode_f32_sw128(&em.din, EPI == EPI_COMP ? args.df_in : args.out_f32, args.M, args.N);
+    encode_f32_sw128(&em.din, (EPI == EPI_COMP || EPI == EPI_ACC) ? args.df_in : args.out_f32, args.M, args.N);
     cudaLaunchKernelEx(&cfg, kern, maps, args, em);
 }
 
@@ -164,11 +164,12 @@ bool make_tmap_f32(void* tmap, const float* p, int rows, int cols, int64_t ld, i
 void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const GemmArgs& args,
              cudaStream_t s) {
     // the pair kernel's TMA-store epilogue needs 16-byte row pitch for the fp32 maps
-    if (use_pair_kernel(args) && (epi == EPI_DF || epi == EPI_COMP) && (args.N % 4) == 0) {
+    if (use_pair_kernel(args) && (epi == EPI_DF || epi == EPI_COMP || epi == EPI_ACC) && (args.N % 4) == 0) {
         const bool mc = pair_count(args) == 2;
         switch (epi) {
             case EPI_DF: mc ? run2<1, EPI_DF, 2>(ops, is_b, nops, args, s) : run2<1, EPI_DF, 1>(ops, is_b, nops, args, s); return;
             case EPI_COMP: mc ? run2<2, EPI_COMP, 2>(ops, is_b, nops, args, s) : run2<2, EPI_COMP, 1>(ops, is_b, nops, args, s); return;
+            case EPI_ACC: run2<1, EPI_ACC, 1>(ops, is_b, nops, args, s); return;
         }
     }
     switch (epi) {
@@ -176,6 +177,7 @@ void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const Gemm
         case EPI_DF: run<256, 1, EPI_DF>(ops, is_b, nops, args, s); break;
         case EPI_COMP: run<128, 2, EPI_COMP>(ops, is_b, nops, args, s); break;
         case EPI_FULL3: run<128, 3, EPI_FULL3>(ops, is_b, nops, args, s); break;
+        case EPI_ACC: throw std::invalid_argument("gemm_i8: EPI_ACC needs the pair kernel");
         default: throw std::invalid_argument("gemm_i8: bad epilogue");
     }
 }

@@ -25,7 +25,8 @@ enum EpiMode : int {
     EPI_S32 = 0,   // store raw s32 accumulator
     EPI_DF = 1,    // store float(acc / (la_i * lb_j))
     EPI_COMP = 2,  // store ((D_F + float(acc0/(l1_i*l2_j))) + float(acc1/(l3_i*l4_j))), alpha/beta
-    EPI_FULL3 = 3  // full residual: ((float(acc0/s0) + float(acc1/s1)) + float(acc2/s2))
+    EPI_FULL3 = 3, // full residual: ((float(acc0/s0) + float(acc1/s1)) + float(acc2/s2))
+    EPI_ACC = 4    // out = float(din + float(acc/(l_i*l_j))), then alpha/beta if `finalize`
 };
 
 struct ScaleRef {  // per-row (stride 1) or per-tensor (stride 0) fp64 scales
@@ -63,6 +64,7 @@ struct GemmArgs {
     ScaleRef rs[3][2];
     ScaleRef cs[3][2];
     int debug;  // probes: bit 0 skip TMA loads (MMA on stale smem), bit 1 skip epilogue work
+    int finalize;  // EPI_ACC: apply the alpha/beta tail (pipeline.cpp:195-202)
 };
 
 template <int BN, int NACC>
@@ -368,7 +370,7 @@ namespace xg {
 // (128+256) for the 1-CTA 128x256 tile: 64 B/clk/SM at full MMA rate.  The
 // accumulator rows 0-127 land in the leader's TMEM, 128-255 in the peer's.
 // 8 epilogue warps (two per TMEM lane quadrant, one per 128-column half).
-template <int NACC>
+template <int NACC, int EPI = EPI_DF>
 struct Gemm2Cfg {
     static constexpr int BM = 128;   // rows per CTA (pair M = 256)
     static constexpr int BN = 256;   // pair N
@@ -377,7 +379,8 @@ struct Gemm2Cfg {
     static constexpr int A_BYTES = BM * BK;
     static constexpr int B_BYTES = BNH * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = NACC == 1 ? 5 : 4;
+    static constexpr bool LOADS_DIN = EPI == EPI_COMP || EPI == EPI_ACC;
+    static constexpr int STAGES = LOADS_DIN ? 4 : 5;
     static constexpr int ACC_COLS = NACC * BN;
     static constexpr int ACC_BUFS = (512 / ACC_COLS) >= 2 ? 2 : 1;
     static constexpr int TMEM_COLS = 512;
@@ -385,7 +388,7 @@ struct Gemm2Cfg {
     static constexpr int EPI_WARPS = 8;
     // per epilogue warp: NSTG staging tiles of 32x32 fp32 (128B-swizzled, TMA
     // store / load) and NACC x 32 fp64 column reciprocals
-    static constexpr int NSTG = NACC == 1 ? 1 : 2;
+    static constexpr int NSTG = LOADS_DIN ? 2 : 1;
     static constexpr int STG_BYTES = 32 * 32 * 4;
     static constexpr int EPI_BYTES = EPI_WARPS * NSTG * STG_BYTES;
     static constexpr int SCL_BYTES = EPI_WARPS * NACC * 32 * 8;
@@ -406,7 +409,7 @@ template <int NACC, int EPI, int PAIRS>
 __global__ void __launch_bounds__(384, 1)
     k_gemm_i8_tc2(const __grid_constant__ TmaMaps maps, const GemmArgs args,
                   const __grid_constant__ EpiMaps emaps) {
-    using Cfg = Gemm2Cfg<NACC>;
+    using Cfg = Gemm2Cfg<NACC, EPI>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     float* epi_stage = (float*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);  // 1024-aligned
@@ -552,7 +555,7 @@ __global__ void __launch_bounds__(384, 1)
             const bool row_ok = row < args.M;
             const int colbase = nb * Cfg::BN + half * (Cfg::BN / 2);
             const int nchunk = (args.debug & 2) ? 0 : min(Cfg::BN / 2 / 32, (args.N - colbase + 31) / 32);
-            if (EPI == EPI_COMP && lane == 0 && nchunk > 0) {  // D_F chunk 0 while the MMA still runs
+            if (Cfg::LOADS_DIN && lane == 0 && nchunk > 0) {  // D_F chunk 0 while the MMA still runs
                 bulk_wait_read<0>();
                 mbar_expect_tx(&mybar[0], Cfg::STG_BYTES);
                 tma_load_2d(stg[0], &emaps.din, &mybar[0], colbase, rowbase);
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(384, 1)
                 const int col0 = colbase + c * 32;
                 const int sb = (Cfg::NSTG == 2) ? (c & 1) : 0;
                 float* tile = stg[sb];
-                if (EPI == EPI_COMP && lane == 0 && c + 1 < nchunk) {  // prefetch the next D_F chunk
+                if (Cfg::LOADS_DIN && lane == 0 && c + 1 < nchunk) {  // prefetch the next D_F chunk
                     bulk_wait_read<0>();
                     mbar_expect_tx(&mybar[(c + 1) & 1], Cfg::STG_BYTES);
                     tma_load_2d(stg[(c + 1) & 1], &emaps.din, &mybar[(c + 1) & 1], col0 + 32, rowbase);
@@ -590,7 +593,7 @@ __global__ void __launch_bounds__(384, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(tempty_leader0 + buf * 8);
                 }
-                if (EPI == EPI_COMP) {
+                if (Cfg::LOADS_DIN) {
                     mbar_wait(&mybar[sb], dph[sb]);
                     dph[sb] ^= 1;
                 } else if (lane == 0) {
@@ -608,6 +611,36 @@ __global__ void __launch_bounds__(384, 1)
                         for (int j = 0; j < 32; ++j)
                             res[j] = dequant_product_value((int32_t)acc[0][j], r0,
                                                            c0.at(min(col0 + j, args.N - 1)));
+                    }
+                } else if constexpr (EPI == EPI_ACC) {
+                    // pipeline.cpp:141-145 one term at a time: out = fl(din + deq(acc))
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const float4 d = rowp[k ^ sw];
+                        res[4 * k] = d.x; res[4 * k + 1] = d.y; res[4 * k + 2] = d.z; res[4 * k + 3] = d.w;
+                    }
+                    float t1[32];
+                    bool slow = false;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) t1[j] = dq_bits((int32_t)acc[0][j], i0, scw[j], slow);
+                    if (slow) {
+                        const ScaleRef c0 = args.cs[0][sel];
+                        for (int j = 0; j < 32; ++j)
+                            t1[j] = dequant_product_value((int32_t)acc[0][j], r0, c0.at(min(col0 + j, args.N - 1)));
+                    }
+                    const float* cin = args.c_in + (int64_t)row * args.N + col0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        float v = __fadd_rn(res[j], t1[j]);
+                        if (args.finalize) {  // pipeline.cpp:195-202 (non-fused)
+                            if (args.has_c) {
+                                const float cv = (row_ok && col0 + j < args.N) ? cin[j] : 0.0f;
+                                v = __fadd_rn(__fmul_rn(args.alpha, v), __fmul_rn(args.beta, cv));
+                            } else if (args.alpha != 1.0f) {
+                                v = __fmul_rn(v, args.alpha);
+                            }
+                        }
+                        res[j] = v;
                     }
                 } else {
 #pragma unroll
