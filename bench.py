@@ -328,7 +328,7 @@ def run_b200(args, world, rank, local):
                      "gemm_df_ms": t_df * 1e3, "gemm_comp_ms": t_cp * 1e3},
         "clocks": clk.summary(),
         "gpu_launches": launches,
-        "stage_ns": {kk: int(vv) for kk, vv in rep.timings.items()},
+        "stage_ns": {kk: int(vv) for kk, vv in r.timings.items()},  # last timed call
     }
     if cpu:
         line["cpu_baseline"] = cpu

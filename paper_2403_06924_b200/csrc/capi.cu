@@ -705,6 +705,35 @@ extern "C" double xg_debug_gemm_df(int m, int n, int k, int flags, int iters) {
     return ms_out;
 }
 
+// Development probe (not part of the reference API): the float-float exact
+// dequantisation of the GEMM epilogues applied elementwise, so tests can check
+// it against fp64 division on arbitrary (p, la, lb).  flags[x] = 1 where the
+// exact fallback was taken.
+namespace {
+__global__ void k_debug_dq_ff(const int32_t* p, const double* la, const double* lb, int64_t n,
+                              float* out, int* flags) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        // exactly the epilogue sequence: dq_ff24, then dq_slow for flagged elements
+        const float2 a = xg::ff_recip(la[x]), b = xg::ff_recip(lb[x]);
+        uint32_t sm = 0;
+        const float f = xg::dq_ff24(p[x], a, b, sm, 1u);
+        bool slow2 = false;
+        if (sm) xg::dq_ff(p[x], a, b, slow2);
+        out[x] = sm ? xg::dq_slow(p[x], a, b, la[x], lb[x]) : f;
+        flags[x] = (sm ? 1 : 0) + (slow2 ? 2 : 0);
+    }
+}
+}  // namespace
+
+extern "C" xg_status xg_debug_dq_ff(const int32_t* p, const double* la, const double* lb, int64_t n,
+                                    float* out, int* flags, xg_stream s) {
+    return guarded([&] {
+        k_debug_dq_ff<<<592, 256, 0, st(s)>>>(p, la, lb, n, out, flags);
+        check_launch("debug_dq_ff");
+    });
+}
+
 xg_status xg_gemm_direct_q(const int8_t* aq, int scheme_a, const double* sa, const int8_t* bq,
                            int scheme_b, const double* sb, int m, int k, int n, int bits_a,
                            int bits_b, float* out, xg_stream s) {

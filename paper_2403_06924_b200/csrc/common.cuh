@@ -167,6 +167,93 @@ __device__ __forceinline__ float dq_bits(int32_t p, double ia, double ib, bool& 
     return p == 0 ? 0.0f : __uint_as_float(f);
 }
 
+// FP64-free variant for the tensor-core epilogues.  On B200 DMUL/DADD issued
+// by the epilogue warps slow the concurrently running tcgen05.mma by ~20%
+// (tools/gemm_ceiling.py: 426 us with dq_bits vs 352 us without dequant math,
+// 354 us with fp32 math of the same shape), so the exact dequantisation runs in
+// float-float arithmetic:
+//   1/la ~ ah + al, 1/lb ~ bh + bl            (ff_recip, once per row/column)
+//   c = (ah+al)(bh+bl) ~ ch + cl              (|rel err| < 2^-45)
+//   p = ph + pl, ph = p & ~255, pl = p & 255  (both exact floats)
+//   y = p*c = s + lo with ph*ch, pl*ch exact (FMA) and Fast2Sum
+//   f = RN_f(s + lo); r = (s - f) + lo  (signed distance y - f, Sterbenz-exact)
+// The reference's q = RN_d(p / RN_d(la*lb)) is within 2^-51|q| of p/(la*lb);
+// y is within 2^-42.5|y|.  If |r| + 2^(E-40) < 2^(E-24) (half an ulp of f,
+// E = f's biased exponent) both lie strictly on f's side of the float
+// midpoints, so RN_f(q) == f.  Powers of two (the ulp halves below them),
+// tiny/huge values and non-finite scales fall back to the exact division
+// (probability ~2^-16 per element).  Zero products give +0 like the reference.
+__device__ __forceinline__ float2 ff_recip(double lam) {
+    const double ia = __ddiv_rn(1.0, lam);
+    const float h = __double2float_rn(ia);
+    const float l = __double2float_rn(__dsub_rn(ia, (double)h));
+    const float ah = fabsf(h);
+    // keep ch = ah*bh in [2^-100, 2^100] so cl and the FMA error terms stay normal
+    if (!(ah >= 0x1p-50f && ah <= 0x1p50f)) return make_float2(__int_as_float(0x7fc00000), 0.0f);
+    return make_float2(h, l);
+}
+
+__device__ __forceinline__ float dq_ff(int32_t p, float2 a, float2 b, bool& slow) {
+    const float ch = __fmul_rn(a.x, b.x);
+    const float ce = __fmaf_rn(a.x, b.x, -ch);
+    const float cl = __fmaf_rn(a.x, b.y, __fmaf_rn(a.y, b.x, ce));
+    const int32_t phi = p & ~255;
+    const float ph = __int2float_rn(phi);                                          // exact: 23 bits
+    const float pl = __fsub_rn(__int_as_float(0x4b000000 | (p & 255)), 8388608.0f);  // exact: 8 bits
+    const float t1 = __fmul_rn(ph, ch);
+    const float e1 = __fmaf_rn(ph, ch, -t1);
+    const float t3 = __fmul_rn(pl, ch);
+    const float e3 = __fmaf_rn(pl, ch, -t3);
+    const float s = __fadd_rn(t1, t3);  // Fast2Sum: |t1| >= |t3| or t1 == 0
+    const float es = __fsub_rn(t3, __fsub_rn(s, t1));
+    const float lo = __fadd_rn(__fmaf_rn(ph, cl, __fmaf_rn(pl, cl, e3)), __fadd_rn(e1, es));
+    const float f = __fadd_rn(s, lo);
+    const float r = __fadd_rn(__fsub_rn(s, f), lo);
+    const uint32_t fb = __float_as_uint(f);
+    const uint32_t ef = fb & 0x7f800000u;
+    const float half = __uint_as_float(ef - (24u << 23));
+    const float marg = __uint_as_float(ef - (40u << 23));
+    const bool ok = ef >= (42u << 23) && ef <= (253u << 23) && (fb & 0x007fffffu) != 0u &&
+                    __fadd_rn(fabsf(r), marg) < half;
+    slow |= !ok && p != 0;
+    return f;
+}
+
+// Epilogue fast form for |p| < 2^24 (p exact as a float, the common case: a
+// K=8192 int8 product of random data stays near 1e5): y = pf*(ch + cl) with
+// pf*ch exact as t1 + e1, |y - p/(la*lb)| <= 2^-44.5|y|.  The midpoint test is
+// done on the float bit patterns: |r| < 2^(e-24) - 2^(e-40) with e = f's
+// exponent (ulp(f)/2 minus a margin 8x the error bound).  Elements that fail
+// (|p| >= 2^24, power-of-two f, out-of-range magnitude, ~2^-15 of random
+// ones) set their bit in `slowmask` and are redone by dq_slow.
+__device__ __forceinline__ float dq_ff24(int32_t p, float2 a, float2 b, uint32_t& slowmask,
+                                         uint32_t bit) {
+    const float ch = __fmul_rn(a.x, b.x);
+    const float ce = __fmaf_rn(a.x, b.x, -ch);
+    const float cl = __fmaf_rn(a.x, b.y, __fmaf_rn(a.y, b.x, ce));
+    const float pf = __int2float_rn(p);
+    const float t1 = __fmul_rn(pf, ch);
+    const float e1 = __fmaf_rn(pf, ch, -t1);
+    const float lo = __fmaf_rn(pf, cl, e1);
+    const float f = __fadd_rn(t1, lo);
+    const float r = __fadd_rn(__fsub_rn(t1, f), lo);
+    const uint32_t fb = __float_as_uint(f);
+    const uint32_t ef = fb & 0x7f800000u;
+    const bool ok = (ef - (42u << 23)) < (212u << 23) && (fb << 9) != 0u &&
+                    (__float_as_uint(r) & 0x7fffffffu) < ef - (24u << 23) - 256u &&
+                    (uint32_t)(p + 0x1000000) < 0x2000000u;
+    slowmask |= (ok || p == 0) ? 0u : bit;
+    return f;
+}
+
+// Rare path of the epilogues: the full-range float-float form, then the
+// reference's own fp64 division.
+static __device__ __noinline__ float dq_slow(int32_t p, float2 a, float2 b, double la, double lb) {
+    bool slow = false;
+    const float f = dq_ff(p, a, b, slow);
+    return slow ? dequant_product_value(p, la, lb) : f;
+}
+
 // float(q / lambda) with il = RN(1/lambda)
 __device__ __forceinline__ float dequant_fast(int q, double il, double lambda) {
     if (q == 0) return 0.0f;
@@ -377,6 +464,13 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, ui
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
         "l"(tmap), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y)
         : "memory");
+}
+// L2-only prefetch of a 2-D tensor box (no shared memory, no barrier): hides
+// DRAM latency for loads issued later from the same box.
+__device__ __forceinline__ void tma_prefetch_l2(const void* tmap, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(tmap), "r"(x),
+                 "r"(y)
+                 : "memory");
 }
 // 2SM TMA load multicast to the CTAs in `mask`; completion is counted on the
 // pair-leader barrier of each destination.

@@ -57,6 +57,8 @@ void encode_f32_sw128(CUtensorMap* m, const float* p, int rows, int cols) {
         throw std::runtime_error("cuTensorMapEncodeTiled (f32) failed: " + std::to_string((int)r));
 }
 
+constexpr int kDefaultPrefetch = 0;
+
 int sm_count() {
     static int n = 0;
     if (!n) {
@@ -123,11 +125,16 @@ void run2(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, 
         }
     }
     cfg.gridDim = dim3(csize * (tiles < max_clusters ? tiles : max_clusters));
+    static const int env_gm = [] { const char* e = getenv("XG_GEMM_GROUP"); return e ? atoi(e) : 0; }();
+    static const int env_pf = [] { const char* e = getenv("XG_GEMM_PF"); return e ? atoi(e) : -1; }();
+    GemmArgs a2 = args;
+    if (a2.group_m <= 0) a2.group_m = env_gm;
+    if (a2.pf_dist <= 0) a2.pf_dist = env_pf >= 0 ? env_pf : kDefaultPrefetch;
     EpiMaps em;
     std::memset(&em, 0, sizeof em);
     encode_f32_sw128(&em.out, args.out_f32, args.M, args.N);
     encode_f32_sw128(&em.din, (EPI == EPI_COMP || EPI == EPI_ACC) ? args.df_in : args.out_f32, args.M, args.N);
-    cudaLaunchKernelEx(&cfg, kern, maps, args, em);
+    cudaLaunchKernelEx(&cfg, kern, maps, a2, em);
 }
 
 bool use_pair_kernel(const GemmArgs& args) {

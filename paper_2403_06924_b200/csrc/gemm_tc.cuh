@@ -65,6 +65,8 @@ struct GemmArgs {
     ScaleRef cs[3][2];
     int debug;  // probes: bit 0 skip TMA loads (MMA on stale smem), bit 1 skip epilogue work
     int finalize;  // EPI_ACC: apply the alpha/beta tail (pipeline.cpp:195-202)
+    int group_m;   // pair kernel: tile-raster group height in 256-row units (0: default)
+    int pf_dist;   // pair kernel: L2 prefetch distance in k-blocks (0: off)
 };
 
 template <int BN, int NACC>
@@ -393,7 +395,7 @@ struct Gemm2Cfg {
     static constexpr int EPI_BYTES = EPI_WARPS * NSTG * STG_BYTES;
     static constexpr int SCL_BYTES = EPI_WARPS * NACC * 32 * 8;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + SCL_BYTES + 1024 + 512;
-    static constexpr int GROUP_M = 8;  // in 256-row units
+    static constexpr int GROUP_M = 16;  // in 256-row units (measured: 16 > 8 > 32 at 8192^3)
     static_assert(ACC_COLS * ACC_BUFS <= 512, "TMEM overflow");
 };
 
@@ -434,6 +436,7 @@ __global__ void __launch_bounds__(384, 1)
     const int num_tiles = num_m * num_n;
     const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
     const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
+    const int gm = args.group_m > 0 ? args.group_m : Cfg::GROUP_M;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -463,12 +466,28 @@ __global__ void __launch_bounds__(384, 1)
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = cluster_id; t < num_tiles; t += nclusters) {
+            const int pf = args.pf_dist;
+            int it = 0;  // tiles already issued by this cluster
+            for (int t = cluster_id; t < num_tiles; t += nclusters, ++it) {
                 int mb, nb;
-                tile_coords(t, num_m, num_n, Cfg::GROUP_M, mb, nb);
+                tile_coords(t, num_m, num_n, gm, mb, nb);
                 const int arow = (mb * PAIRS + (int)pair) * 2 * Cfg::BM + (int)prank * Cfg::BM;
                 const int brow = nb * Cfg::BN + (int)prank * Cfg::BNH + (int)pair * (Cfg::BNH / PAIRS);
                 for (int kb = 0; kb < nkb; ++kb) {
+                    if (pf > 0 && !(args.debug & 1)) {  // L2 prefetch of the block `pf` ahead in this CTA's stream
+                        const int f = it * nkb + kb + pf;
+                        const int t2 = cluster_id + (f / nkb) * nclusters, kb2 = f % nkb;
+                        if (t2 < num_tiles) {
+                            int mb2, nb2;
+                            tile_coords(t2, num_m, num_n, gm, mb2, nb2);
+                            const int arow2 = (mb2 * PAIRS + (int)pair) * 2 * Cfg::BM + (int)prank * Cfg::BM;
+                            const int brow2 = nb2 * Cfg::BN + (int)prank * Cfg::BNH + (int)pair * (Cfg::BNH / PAIRS);
+                            for (int a = 0; a < NACC; ++a) {
+                                tma_prefetch_l2(&maps.m[args.amap[a][sel]], kb2 * Cfg::BK, arow2);
+                                tma_prefetch_l2(&maps.m[args.bmap[a][sel]], kb2 * Cfg::BK, brow2);
+                            }
+                        }
+                    }
                     for (int a = 0; a < NACC; ++a) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
@@ -514,9 +533,10 @@ __global__ void __launch_bounds__(384, 1)
                         const uint64_t da = smem_desc_k128(sA);
                         const uint64_t db = smem_desc_k128(sA + Cfg::A_BYTES);
 #pragma unroll
-                        for (int k = 0; k < Cfg::BK / 32; ++k)
-                            mma_i8_pair(dbase + a * Cfg::BN, da + 2 * k, db + 2 * k, idesc,
-                                        (kb | k) != 0 ? 1u : 0u);
+                        if (!(args.debug & 32))  // probe: skip the MMAs
+                            for (int k = 0; k < Cfg::BK / 32; ++k)
+                                mma_i8_pair(dbase + a * Cfg::BN, da + 2 * k, db + 2 * k, idesc,
+                                            (kb | k) != 0 ? 1u : 0u);
                         if (PAIRS == 1) tc_commit_pair(&empty[stage]);
                         else tc_commit_mc(&empty[stage], (uint16_t)0xF);
                         if (++stage == Cfg::STAGES) {
@@ -541,7 +561,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t tempty_leader0 = mapa_shared(&tempty[0], rank & ~1u);
         float* stg[2] = {epi_stage + we * Cfg::NSTG * 1024,
                          epi_stage + (we * Cfg::NSTG + Cfg::NSTG - 1) * 1024};
-        double* scw = epi_scale + we * NACC * 32;
+        float2* scw = reinterpret_cast<float2*>(epi_scale) + we * NACC * 32;
         uint64_t* mybar = dbar + 2 * we;
         uint32_t dph[2] = {0, 0};
         const int sw = lane & 7;  // 128B swizzle: chunk k of row `lane` sits at k ^ (lane & 7)
@@ -549,7 +569,7 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t bphase = 0;
         for (int t = cluster_id; t < num_tiles; t += nclusters) {
             int mb, nb;
-            tile_coords(t, num_m, num_n, Cfg::GROUP_M, mb, nb);
+            tile_coords(t, num_m, num_n, gm, mb, nb);
             const int rowbase = (mb * PAIRS + (int)pair) * 2 * Cfg::BM + (int)prank * Cfg::BM + q * 32;
             const int row = rowbase + lane;
             const bool row_ok = row < args.M;
@@ -567,7 +587,7 @@ __global__ void __launch_bounds__(384, 1)
                 r0 = args.rs[0][sel].at(row);
                 if (NACC > 1) r1 = args.rs[1][sel].at(row);
             }
-            const double i0 = __ddiv_rn(1.0, r0), i1 = __ddiv_rn(1.0, r1);
+            const float2 i0 = ff_recip(r0), i1 = ff_recip(r1);
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * Cfg::ACC_COLS +
                                    half * (Cfg::BN / 2);
 #pragma unroll 1
@@ -582,8 +602,8 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 // column reciprocals of this chunk, broadcast through shared memory
                 const int mycol = min(col0 + lane, args.N - 1);
-                scw[lane] = __ddiv_rn(1.0, args.cs[0][sel].at(mycol));
-                if (NACC > 1) scw[32 + lane] = __ddiv_rn(1.0, args.cs[1][sel].at(mycol));
+                scw[lane] = ff_recip(args.cs[0][sel].at(mycol));
+                if (NACC > 1) scw[32 + lane] = ff_recip(args.cs[1][sel].at(mycol));
                 uint32_t acc[NACC][32];
 #pragma unroll
                 for (int a = 0; a < NACC; ++a) tmem_ld32(tbase + a * Cfg::BN + c * 32, acc[a]);
@@ -593,6 +613,7 @@ __global__ void __launch_bounds__(384, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(tempty_leader0 + buf * 8);
                 }
+                if (args.debug & 4) continue;  // probe: TMEM drain only
                 if (Cfg::LOADS_DIN) {
                     mbar_wait(&mybar[sb], dph[sb]);
                     dph[sb] ^= 1;
@@ -604,43 +625,59 @@ __global__ void __launch_bounds__(384, 1)
                 float res[32];
                 if constexpr (EPI == EPI_DF) {
                     bool slow = false;
+                    if (args.debug & 64) {  // probe: no dequant math
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) res[j] = dq_bits((int32_t)acc[0][j], i0, scw[j], slow);
-                    if (slow) {  // rare: redo the chunk with the reference's fp64 division
-                        const ScaleRef c0 = args.cs[0][sel];
-                        for (int j = 0; j < 32; ++j)
-                            res[j] = dequant_product_value((int32_t)acc[0][j], r0,
-                                                           c0.at(min(col0 + j, args.N - 1)));
+                        for (int j = 0; j < 32; ++j) res[j] = __int_as_float(acc[0][j]);
+                    } else if (args.debug & 128) {  // probe: fp32 math of similar count
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) res[j] = __fmul_rn(__fmul_rn((float)(int32_t)acc[0][j], i0.x), scw[j].x);
+                    } else {
+                        uint32_t sm = 0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) res[j] = dq_ff24((int32_t)acc[0][j], i0, scw[j], sm, 1u << j);
+                        if (sm) {  // rare: exact redo of the flagged elements
+                            const ScaleRef c0 = args.cs[0][sel];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (sm & (1u << j))
+                                    res[j] = dq_slow((int32_t)acc[0][j], i0, scw[j], r0, c0.at(min(col0 + j, args.N - 1)));
+                        }
                     }
+                    (void)slow;
                 } else if constexpr (EPI == EPI_ACC) {
-                    // pipeline.cpp:141-145 one term at a time: out = fl(din + deq(acc))
+                    // pipeline.cpp:141-145 one term at a time: out = fl(din + deq(acc)).
+                    // In place over res[] (register budget: 168/thread); the rare
+                    // exact redo re-reads din from the staging tile.
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const float4 d = rowp[k ^ sw];
                         res[4 * k] = d.x; res[4 * k + 1] = d.y; res[4 * k + 2] = d.z; res[4 * k + 3] = d.w;
                     }
-                    float t1[32];
-                    bool slow = false;
+                    uint32_t sm = 0;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) t1[j] = dq_bits((int32_t)acc[0][j], i0, scw[j], slow);
-                    if (slow) {
+                    for (int j = 0; j < 32; ++j)
+                        res[j] = __fadd_rn(res[j], dq_ff24((int32_t)acc[0][j], i0, scw[j], sm, 1u << j));
+                    if (sm) {  // rare: exact redo of the flagged elements
                         const ScaleRef c0 = args.cs[0][sel];
-                        for (int j = 0; j < 32; ++j)
-                            t1[j] = dequant_product_value((int32_t)acc[0][j], r0, c0.at(min(col0 + j, args.N - 1)));
-                    }
-                    const float* cin = args.c_in + (int64_t)row * args.N + col0;
+                        const float* rowf = tile + lane * 32;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        float v = __fadd_rn(res[j], t1[j]);
-                        if (args.finalize) {  // pipeline.cpp:195-202 (non-fused)
+                        for (int j = 0; j < 32; ++j)
+                            if (sm & (1u << j))
+                                res[j] = __fadd_rn(rowf[(((j >> 2) ^ sw) << 2) | (j & 3)],
+                                                   dq_slow((int32_t)acc[0][j], i0, scw[j], r0,
+                                                           c0.at(min(col0 + j, args.N - 1))));
+                    }
+                    if (args.finalize) {  // pipeline.cpp:195-202 (non-fused)
+                        const float* cin = args.c_in + (int64_t)row * args.N + col0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
                             if (args.has_c) {
                                 const float cv = (row_ok && col0 + j < args.N) ? cin[j] : 0.0f;
-                                v = __fadd_rn(__fmul_rn(args.alpha, v), __fmul_rn(args.beta, cv));
+                                res[j] = __fadd_rn(__fmul_rn(args.alpha, res[j]), __fmul_rn(args.beta, cv));
                             } else if (args.alpha != 1.0f) {
-                                v = __fmul_rn(v, args.alpha);
+                                res[j] = __fmul_rn(res[j], args.alpha);
                             }
                         }
-                        res[j] = v;
                     }
                 } else {
 #pragma unroll
@@ -651,17 +688,18 @@ __global__ void __launch_bounds__(384, 1)
                     const ScaleRef c0 = args.cs[0][sel], c1 = args.cs[1][sel];
                     const float* cin = args.c_in + (int64_t)row * args.N + col0;
                     float t1[32], t2[32];
-                    bool slow = false;
+                    uint32_t sm1 = 0, sm2 = 0;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        t1[j] = dq_bits((int32_t)acc[0][j], i0, scw[j], slow);
-                        t2[j] = dq_bits((int32_t)acc[1 % NACC][j], i1, scw[32 + j], slow);
+                        t1[j] = dq_ff24((int32_t)acc[0][j], i0, scw[j], sm1, 1u << j);
+                        t2[j] = dq_ff24((int32_t)acc[1 % NACC][j], i1, scw[32 + j], sm2, 1u << j);
                     }
-                    if (slow) {  // rare: redo the chunk with the reference's fp64 division
+                    if (sm1 | sm2) {  // rare: exact redo of the flagged elements
+#pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             const int cj = min(col0 + j, args.N - 1);
-                            t1[j] = dequant_product_value((int32_t)acc[0][j], r0, c0.at(cj));
-                            t2[j] = dequant_product_value((int32_t)acc[1 % NACC][j], r1, c1.at(cj));
+                            if (sm1 & (1u << j)) t1[j] = dq_slow((int32_t)acc[0][j], i0, scw[j], r0, c0.at(cj));
+                            if (sm2 & (1u << j)) t2[j] = dq_slow((int32_t)acc[1 % NACC][j], i1, scw[32 + j], r1, c1.at(cj));
                         }
                     }
 #pragma unroll
@@ -681,7 +719,7 @@ __global__ void __launch_bounds__(384, 1)
                     rowp[k ^ sw] = make_float4(res[4 * k], res[4 * k + 1], res[4 * k + 2], res[4 * k + 3]);
                 fence_proxy_async();
                 __syncwarp();
-                if (lane == 0) {
+                if (lane == 0 && !(args.debug & 8)) {  // bit 3 probe: no store
                     tma_store_2d(&emaps.out, tile, col0, rowbase);
                     bulk_commit();
                 }

@@ -258,3 +258,64 @@ def test_host_entry_point(oracle):
     c = ol.cfg(threshold=0.2, scheme=1, policy=0)
     out, rep = xg.xigemm_host(a, b, cfg=cfg_from(c))
     assert beq(out, oracle.xigemm(a, b, config=c)[1])
+
+
+def _dq_ff(p, la, lb):
+    import ctypes as C
+    f = xg.lib().xg_debug_dq_ff
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+    pt = torch.from_numpy(p).cuda()
+    at = torch.from_numpy(la).cuda()
+    bt = torch.from_numpy(lb).cuda()
+    out = torch.empty(len(p), dtype=torch.float32, device="cuda")
+    flags = torch.empty(len(p), dtype=torch.int32, device="cuda")
+    assert f(pt.data_ptr(), at.data_ptr(), bt.data_ptr(), len(p), out.data_ptr(), flags.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), flags.cpu().numpy()
+
+
+def _dq_ref(p, la, lb):
+    # quantize.cpp:183: static_cast<float>(p / (la * scales_b.col_scale(j))) in fp64
+    return (p.astype(np.float64) / (la * lb)).astype(np.float32)
+
+
+def test_dq_ff_random_exact():
+    """The FP64-free epilogue dequantisation equals float(p / (la*lb)) bit for bit."""
+    rng = np.random.default_rng(2024)
+    n = 1 << 22
+    p = np.concatenate([rng.integers(-2**31, 2**31, n // 2, dtype=np.int64),
+                        rng.integers(-1024, 1024, n // 4, dtype=np.int64),
+                        (np.sign(rng.standard_normal(n // 4)) *
+                         np.exp(rng.uniform(0, 21.4, n // 4))).astype(np.int64)]).astype(np.int32)
+    p[:8] = [0, 1, -1, 255, -256, 2**31 - 1, -2**31, 256]
+    mx = np.exp(rng.uniform(np.log(1e-5), np.log(1e5), (2, n)))
+    la, lb = 127.0 / mx[0], 127.0 / mx[1]
+    la[8:16] = [1.0, 0.5, 2.0, 127.0, 63.5, 1e-3, 1e3, 31.75]
+    got, flags = _dq_ff(p, la, lb)
+    ref = _dq_ref(p, la, lb)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    small = np.abs(p.astype(np.int64)) < 2**24
+    assert (flags[small] != 0).mean() < 1e-3  # fast path decides nearly all |p| < 2^24
+    assert (flags[~small] >= 2).mean() < 1e-3  # the split form decides nearly all the rest
+
+
+def test_dq_ff_near_midpoints_exact():
+    """Adversarial: scales chosen so p/(la*lb) sits within a few fp64 ulps of a
+    float rounding midpoint, where only the reference's own double rounding
+    decides the result."""
+    rng = np.random.default_rng(7)
+    n = 1 << 20
+    p = rng.integers(1, 2**31, n, dtype=np.int64) * rng.choice([-1, 1], n)
+    lb = 127.0 / np.exp(rng.uniform(np.log(1e-3), np.log(1e3), n))
+    f = (p / (127.0 * lb)).astype(np.float32)
+    f = np.where(f == 0, np.float32(1), f)
+    nxt = np.nextafter(f, np.float32(np.inf) * np.sign(f)).astype(np.float64)
+    mid = (f.astype(np.float64) + nxt) / 2.0
+    la = p / (mid * lb)
+    nudge = rng.integers(-4, 5, n)
+    la = la + nudge * np.spacing(la)
+    got, flags = _dq_ff(p.astype(np.int32), la, lb)
+    ref = _dq_ref(p.astype(np.int32), la, lb)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    assert (flags >= 2).mean() > 0.9  # nearly all must reach the exact fp64 division
