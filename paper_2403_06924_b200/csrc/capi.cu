@@ -391,7 +391,15 @@ void run_pipeline(const float* a, const float* b, const float* c, float alpha, f
     if (dump && dump->d_f)
         ck(cudaMemcpyAsync(dump->d_f, out, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToDevice, s), "dump");
     if (reduce) {
-        xg::launch_stats(out, M, N, cfg->policy, rstat, cstat, rsum, csum, flags, &p.sc->nflag, s);
+        // without a stage dump the exact-mean fallback is deferred to a
+        // membership test (stats.cu): the means themselves are never observable
+        static const int widen = [] {
+            const char* e = getenv("XG_STATS_WIDEN");  // test hook
+            return e ? atoi(e) : 0;
+        }();
+        const xg::StatsDefer def{a, K, b, N, K, cfg->threshold, widen};
+        xg::launch_stats(out, M, N, cfg->policy, rstat, cstat, rsum, csum, flags, &p.sc->nflag, s,
+                         dump ? nullptr : &def);
         check_launch("stats", cfg->policy == XG_AVG_RULE ? 4 : 3);
     }
     select_operands(p, a, b, reduce, rstat, cstat);

@@ -91,9 +91,22 @@ void launch_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, double de
                      int reduce, cudaStream_t s);
 
 // statistics over D_F (pipeline.cpp:215-247)
+// Deferred exact-mean fallback (AvgRule): the operands whose selection the
+// statistics drive (A rows: M x inner, B columns: inner x N) and the threshold
+// multiplier; `widen` (test hook) scales the verified-rounding interval by
+// 2^widen so the deferred path is exercised on every statistic.
+struct StatsDefer {
+    const float* a;
+    int64_t lda;
+    const float* b;
+    int64_t ldb;
+    int inner;
+    double thr_m;
+    int widen;
+};
 void launch_stats(const float* d, int rows, int cols, int policy, float* row_stat,
                   float* col_stat, double* row_sum, double* col_sum, int* flags, int* nflag,
-                  cudaStream_t s);
+                  cudaStream_t s, const StatsDefer* def = nullptr);
 
 void fill_u32(uint32_t* p, uint32_t v, int64_t n, cudaStream_t s);
 

@@ -99,28 +99,33 @@ __global__ void __launch_bounds__(kThreads)
 
 // float(S / n) with a proof that the reference's sequential sum rounds the
 // same; returns false when the interval straddles a float rounding boundary.
-__device__ __forceinline__ bool verified_mean(double S, int nterms, double n, float& out) {
+__device__ __forceinline__ void mean_candidates(double S, int nterms, double n, float& lo, float& hi,
+                                                int widen = 0) {
     const double u = 1.1102230246251565e-16;  // 2^-53
     const double k = (double)(nterms > 1 ? nterms - 1 : 0);
     const double gam = (k * u) / (1.0 - k * u);
-    const double delta = 4.0 * gam * S;
-    const float lo = __double2float_rn(__ddiv_rn(__dsub_rn(S, delta), n));
-    const float hi = __double2float_rn(__ddiv_rn(__dadd_rn(S, delta), n));
-    out = __double2float_rn(__ddiv_rn(S, n));
+    const double delta = ldexp(4.0 * gam * S, widen);
+    lo = __double2float_rn(__ddiv_rn(__dsub_rn(S, delta), n));
+    hi = __double2float_rn(__ddiv_rn(__dadd_rn(S, delta), n));
+}
+__device__ __forceinline__ bool verified_mean(double S, int nterms, double n, float& out, int widen) {
+    float lo, hi;
+    mean_candidates(S, nterms, n, lo, hi, widen);
+    out = lo == hi ? lo : __double2float_rn(__ddiv_rn(S, n));
     return lo == hi;
 }
 
 __global__ void k_finalize_avg(const double* row_sum, const double* col_sum, int rows, int cols,
-                               float* row_stat, float* col_stat, int* flags, int* nflag) {
+                               float* row_stat, float* col_stat, int* flags, int* nflag, int widen) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows + cols) return;
     float v;
     bool ok;
     if (i < rows) {
-        ok = verified_mean(row_sum[i], cols, (double)cols, v);
+        ok = verified_mean(row_sum[i], cols, (double)cols, v, widen);
         row_stat[i] = v;
     } else {
-        ok = verified_mean(col_sum[i - rows], rows, (double)rows, v);
+        ok = verified_mean(col_sum[i - rows], rows, (double)rows, v, widen);
         col_stat[i - rows] = v;
     }
     if (!ok) flags[atomicAdd(nflag, 1)] = i;
@@ -128,16 +133,40 @@ __global__ void k_finalize_avg(const double* row_sum, const double* col_sum, int
 
 // Exact reference order for the flagged statistics: the CTA stages the slice
 // through shared memory, one thread adds sequentially (pipeline.cpp:219-229).
+//
+// Deferred mode (`def.a != nullptr`, the pipeline without a stage dump): a
+// statistic only matters through its threshold t = M * stat (sparse.cpp:49-65),
+// and the reference's float mean is one of the two candidates lo/hi bracketing
+// the verified interval.  The kept set of the operand slice (row i of A for a
+// row statistic, column j of B for a column statistic) is the same under both
+// candidates unless some |x| lies in [float_above(M*lo), float_above(M*hi)).
+// One parallel scan of that slice decides; only then is the sequential sum
+// paid (the mean stays `lo` otherwise: it is never observable).
 constexpr int kChunk = 2048;
 __global__ void __launch_bounds__(kThreads)
     k_fallback_avg(const float* __restrict__ d, int rows, int cols, const int* flags,
-                   const int* nflag, float* row_stat, float* col_stat) {
+                   const int* nflag, float* row_stat, float* col_stat, const double* row_sum,
+                   const double* col_sum, const StatsDefer def) {
     __shared__ float buf[kChunk];
     const int nf = *nflag;
     for (int f = blockIdx.x; f < nf; f += gridDim.x) {
         const int idx = flags[f];
         const bool is_row = idx < rows;
         const int len = is_row ? cols : rows;
+        if (def.a) {
+            const double S = is_row ? row_sum[idx] : col_sum[idx - rows];
+            float lo, hi;
+            mean_candidates(S, len, (double)len, lo, hi, def.widen);
+            const float tlo = float_above(__dmul_rn(def.thr_m, (double)lo));
+            const float thi = float_above(__dmul_rn(def.thr_m, (double)hi));
+            int amb = 0;
+            for (int t = threadIdx.x; t < def.inner; t += kThreads) {
+                const float x = is_row ? def.a[(int64_t)idx * def.lda + t]
+                                       : def.b[(int64_t)t * def.ldb + (idx - rows)];
+                amb |= (fabsf(x) >= tlo && fabsf(x) < thi) ? 1 : 0;
+            }
+            if (!__syncthreads_or(amb)) continue;  // uniform: membership identical under lo and hi
+        }
         double s = 0.0;
         for (int base = 0; base < len; base += kChunk) {
             const int cnt = min(kChunk, len - base);
@@ -171,15 +200,18 @@ __global__ void k_zero(double* a, int na, double* b, int nb, int* n) {
 }  // namespace
 
 void launch_stats(const float* d, int rows, int cols, int policy, float* row_stat, float* col_stat,
-                  double* row_sum, double* col_sum, int* flags, int* nflag, cudaStream_t s) {
+                  double* row_sum, double* col_sum, int* flags, int* nflag, cudaStream_t s,
+                  const StatsDefer* def) {
     dim3 grid((cols + kThreads * 4 - 1) / (kThreads * 4), (rows + kSlabRows - 1) / kSlabRows);
     if (policy == kAvg) {
         const int nz = rows > cols ? rows : cols;
         k_zero<<<(nz + 255) / 256, 256, 0, s>>>(row_sum, rows, col_sum, cols, nflag);
         k_stats_slab<kAvg><<<grid, kThreads, 0, s>>>(d, rows, cols, row_sum, col_sum, nullptr, nullptr);
         k_finalize_avg<<<(rows + cols + 255) / 256, 256, 0, s>>>(row_sum, col_sum, rows, cols,
-                                                                 row_stat, col_stat, flags, nflag);
-        k_fallback_avg<<<64, kThreads, 0, s>>>(d, rows, cols, flags, nflag, row_stat, col_stat);
+                                                                 row_stat, col_stat, flags, nflag,
+                                                                 def ? def->widen : 0);
+        k_fallback_avg<<<64, kThreads, 0, s>>>(d, rows, cols, flags, nflag, row_stat, col_stat, row_sum,
+                                               col_sum, def ? *def : StatsDefer{});
     } else {
         // the float bit patterns of |x| order like uints; FLT_MAX initial value (pipeline.cpp:237-238)
         fill_u32(reinterpret_cast<uint32_t*>(row_stat), 0x7f7fffffu, rows, s);

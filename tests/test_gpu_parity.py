@@ -319,3 +319,20 @@ def test_dq_ff_near_midpoints_exact():
     ref = _dq_ref(p.astype(np.int32), la, lb)
     assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
     assert (flags >= 2).mean() > 0.9  # nearly all must reach the exact fp64 division
+
+
+def test_deferred_mean_fallback_widened():
+    """AvgRule statistics the GPU cannot pin by verified rounding are resolved
+    lazily (stats.cu: membership scan, then the exact sequential sum only if a
+    kept set could differ).  XG_STATS_WIDEN=24 widens the verified interval
+    2^24-fold so every statistic takes that path; outputs must still match the
+    reference bit for bit (re-runs the golden pipeline cases in a subprocess,
+    the hook is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, XG_STATS_WIDEN="24")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-x", "-k", "pipeline_golden",
+                        "-p", "no:cacheprovider"], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.abspath(__file__)))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
