@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -128,11 +130,21 @@ xg::ScaleRef sref(const double* p, int stride) { return xg::ScaleRef{p, stride};
 struct EventTimer {
     bool on;
     cudaStream_t s;
-    cudaEvent_t ev[8];
+    cudaEvent_t* ev;
     int n = 0;
     EventTimer(bool on_, cudaStream_t s_) : on(on_), s(s_) {
-        if (on)
-            for (auto& e : ev) cudaEventCreate(&e);
+        // per-thread, per-device events created once (event creation is a
+        // host-side cost paid before the first launch of every call otherwise)
+        thread_local cudaEvent_t pool[16][8];
+        thread_local bool made[16] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        dev &= 15;
+        ev = pool[dev];
+        if (on && !made[dev]) {
+            for (int i = 0; i < 8; ++i) cudaEventCreate(&ev[i]);
+            made[dev] = true;
+        }
     }
     void mark() {
         if (on && n < 8) cudaEventRecord(ev[n++], s);
@@ -143,10 +155,7 @@ struct EventTimer {
         cudaEventElapsedTime(&ms, ev[a], ev[b]);
         return ms * 1e6;
     }
-    ~EventTimer() {
-        if (on)
-            for (auto& e : ev) cudaEventDestroy(e);
-    }
+
 };
 
 // ------------------------------------------------------------------ pipeline
@@ -348,74 +357,206 @@ void dump_operands(Pipe& p, xg_dump* d) {
     cpd(d->b_red_scale, &p.sc->lamBred, 1);
 }
 
-void run_pipeline(const float* a, const float* b, const float* c, float alpha, float beta, int M,
-                  int K, int N, const xg_config* cfg, int reduce, float* out, xg_report* rep,
-                  xg_dump* dump, cudaStream_t s) {
-    validate_cfg(cfg);
-    req(M >= 1 && K >= 1 && N >= 1, "xigemm: matrix dimensions must be >= 1");
-    req(a && b && out, "xigemm: null matrix");
-    req(K <= xg::gemm_max_inner(cfg->bits), "gemm_int: inner dimension permits 32-bit overflow");
-    Scratch S(s);
-    Pipe p;
-    p.M = M; p.K = K; p.N = N; p.cfg = cfg; p.s = s;
-    p.ldk = pad16(K);
-    p.vw = cfg->scheme == XG_Q_VECTORWISE;
-    p.sc = S.get<xg::DevScalars>(1);
-    p.aq = S.get<int8_t>(M * p.ldk);
-    p.raq = S.get<int8_t>(M * p.ldk);
-    p.ared = S.get<int8_t>(M * p.ldk);
-    p.bqT = S.get<int8_t>(N * p.ldk);
-    p.rbqT = S.get<int8_t>(N * p.ldk);
-    p.bredT = S.get<int8_t>(N * p.ldk);
-    p.la = S.get<double>(M);
-    p.lb = S.get<double>(N);
-    p.colmax = S.get<uint32_t>(N);
-    float* rstat = S.get<float>(M);
-    float* cstat = S.get<float>(N);
-    double* rsum = S.get<double>(M);
-    double* csum = S.get<double>(N);
-    int* flags = S.get<int>((int64_t)M + N);
-    ck(cudaMemsetAsync(p.sc, 0, sizeof(xg::DevScalars), s), "memset");
+// All device buffers of one pipeline call.
+struct PipeWs {
+    xg::DevScalars* sc;
+    int8_t *aq, *raq, *ared, *bqT, *rbqT, *bredT;
+    double *la, *lb;
+    uint32_t* colmax;
+    float *rstat, *cstat;
+    double *rsum, *csum;
+    int* flags;
+};
 
-    EventTimer tm(rep != nullptr, s);
-    tm.mark();  // 0
-    if (c) {
-        xg::finite_max(c, (int64_t)M * N, &p.sc->retB /*scratch, reset below*/, &p.sc->nonfinite, s);
-        check_launch("finite C");
-        ck(cudaMemsetAsync(&p.sc->retB, 0, sizeof(uint32_t), s), "memset");
+template <class Get>
+void alloc_ws(PipeWs& w, int M, int N, int64_t ldk, Get&& get) {
+    w.sc = get((xg::DevScalars*)nullptr, 1);
+    w.aq = get((int8_t*)nullptr, M * ldk);
+    w.raq = get((int8_t*)nullptr, M * ldk);
+    w.ared = get((int8_t*)nullptr, M * ldk);
+    w.bqT = get((int8_t*)nullptr, N * ldk);
+    w.rbqT = get((int8_t*)nullptr, N * ldk);
+    w.bredT = get((int8_t*)nullptr, N * ldk);
+    w.la = get((double*)nullptr, M);
+    w.lb = get((double*)nullptr, N);
+    w.colmax = get((uint32_t*)nullptr, N);
+    w.rstat = get((float*)nullptr, M);
+    w.cstat = get((float*)nullptr, N);
+    w.rsum = get((double*)nullptr, M);
+    w.csum = get((double*)nullptr, N);
+    w.flags = get((int*)nullptr, (int64_t)M + N);
+}
+
+struct PipeCall {
+    const float *a, *b, *c;
+    float alpha, beta;
+    int M, K, N;
+    xg_config cfg;
+    int reduce;
+    float* out;
+};
+
+// One stage group of the device pipeline (no host synchronisation anywhere):
+// 0 quantise, 1 D_F GEMM, 2 statistics + selection + dispatch, 3 compensation.
+// Returns the number of kernels it launched.
+int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* dump, cudaStream_t s) {
+    const int64_t l0 = g_launches.load();
+    Pipe p;
+    p.M = q.M; p.K = q.K; p.N = q.N; p.cfg = &q.cfg; p.s = s;
+    p.ldk = pad16(q.K);
+    p.vw = q.cfg.scheme == XG_Q_VECTORWISE;
+    p.sc = w.sc;
+    p.aq = w.aq; p.raq = w.raq; p.ared = w.ared;
+    p.bqT = w.bqT; p.rbqT = w.rbqT; p.bredT = w.bredT;
+    p.la = w.la; p.lb = w.lb; p.colmax = w.colmax;
+    const int M = q.M, K = q.K, N = q.N;
+    if (stage == 0) {
+        ck(cudaMemsetAsync(p.sc, 0, sizeof(xg::DevScalars), s), "memset");
+        if (q.c) {
+            xg::finite_max(q.c, (int64_t)M * N, &p.sc->retB /*scratch, reset below*/, &p.sc->nonfinite, s);
+            check_launch("finite C");
+            ck(cudaMemsetAsync(&p.sc->retB, 0, sizeof(uint32_t), s), "memset");
+        }
+        quantize_operands(p, q.a, q.b);
+    } else if (stage == 1) {
+        gemm_df(p, q.out);
+        if (dump && dump->d_f)
+            ck(cudaMemcpyAsync(dump->d_f, q.out, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToDevice, s), "dump");
+    } else if (stage == 2) {
+        if (q.reduce) {
+            // without a stage dump the exact-mean fallback is deferred to a
+            // membership test (stats.cu): the means themselves are never observable
+            static const int widen = [] {
+                const char* e = getenv("XG_STATS_WIDEN");  // test hook
+                return e ? atoi(e) : 0;
+            }();
+            const xg::StatsDefer def{q.a, K, q.b, N, K, q.cfg.threshold, widen};
+            xg::launch_stats(q.out, M, N, q.cfg.policy, w.rstat, w.cstat, w.rsum, w.csum, w.flags,
+                             &p.sc->nflag, s, dump ? nullptr : &def);
+            check_launch("stats", q.cfg.policy == XG_AVG_RULE ? 4 : 3);
+        }
+        select_operands(p, q.a, q.b, q.reduce, w.rstat, w.cstat);
+        xg::launch_dispatch(p.sc, q.cfg.bits, (int64_t)M * K, (int64_t)K * N, q.cfg.density_limit, q.reduce, s);
+        check_launch("dispatch");
+        if (dump) {
+            dump_operands(p, dump);
+            if (dump->row_stat && q.reduce) ck(cudaMemcpyAsync(dump->row_stat, w.rstat, 4 * (size_t)M, cudaMemcpyDeviceToDevice, s), "dump");
+            if (dump->col_stat && q.reduce) ck(cudaMemcpyAsync(dump->col_stat, w.cstat, 4 * (size_t)N, cudaMemcpyDeviceToDevice, s), "dump");
+        }
+    } else {
+        gemm_comp(p, q.out, q.c, q.alpha, q.beta);
     }
-    quantize_operands(p, a, b);
-    tm.mark();  // 1 quant
-    gemm_df(p, out);
-    tm.mark();  // 2 xxmm
-    if (dump && dump->d_f)
-        ck(cudaMemcpyAsync(dump->d_f, out, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToDevice, s), "dump");
-    if (reduce) {
-        // without a stage dump the exact-mean fallback is deferred to a
-        // membership test (stats.cu): the means themselves are never observable
-        static const int widen = [] {
-            const char* e = getenv("XG_STATS_WIDEN");  // test hook
-            return e ? atoi(e) : 0;
-        }();
-        const xg::StatsDefer def{a, K, b, N, K, cfg->threshold, widen};
-        xg::launch_stats(out, M, N, cfg->policy, rstat, cstat, rsum, csum, flags, &p.sc->nflag, s,
-                         dump ? nullptr : &def);
-        check_launch("stats", cfg->policy == XG_AVG_RULE ? 4 : 3);
+    return g_launches.load() - l0;
+}
+
+// ---- CUDA-graph cache ------------------------------------------------------
+// A repeated call (same pointers, shapes and configuration) replays the four
+// stage groups as CUDA graphs captured on a private stream, over a workspace
+// owned by the cache entry: no per-call allocation, TMA-map encoding or
+// per-kernel launch overhead on the host, so the GPU is not left idle between
+// kernels.  Entries are captured on their second use; at most kGraphEntries
+// are kept (least recently used evicted).  XG_NO_GRAPH=1 disables the cache.
+constexpr int kGraphEntries = 4;
+
+struct GraphEntry {
+    PipeCall key{};
+    int dev = -1;
+    PipeWs ws{};
+    void* ws_base = nullptr;
+    cudaGraphExec_t exec[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t launches[4] = {0, 0, 0, 0};
+    int hits = 0;
+    bool busy = false;
+    uint64_t last = 0;
+    void release() {
+        for (auto& e : exec)
+            if (e) cudaGraphExecDestroy(e), e = nullptr;
+        if (ws_base) cudaFree(ws_base), ws_base = nullptr;
     }
-    select_operands(p, a, b, reduce, rstat, cstat);
-    xg::launch_dispatch(p.sc, cfg->bits, (int64_t)M * K, (int64_t)K * N, cfg->density_limit, reduce, s);
-    check_launch("dispatch");
-    tm.mark();  // 3 reduce
-    if (dump) {
-        dump_operands(p, dump);
-        if (dump->row_stat && reduce) ck(cudaMemcpyAsync(dump->row_stat, rstat, 4 * (size_t)M, cudaMemcpyDeviceToDevice, s), "dump");
-        if (dump->col_stat && reduce) ck(cudaMemcpyAsync(dump->col_stat, cstat, 4 * (size_t)N, cudaMemcpyDeviceToDevice, s), "dump");
+};
+
+std::mutex g_graph_mu;
+GraphEntry g_graphs[kGraphEntries];
+uint64_t g_graph_clock = 0;
+
+bool same_call(const PipeCall& x, const PipeCall& y) {
+    return x.a == y.a && x.b == y.b && x.c == y.c && x.out == y.out && x.M == y.M && x.K == y.K &&
+           x.N == y.N && x.reduce == y.reduce && std::memcmp(&x.alpha, &y.alpha, sizeof(float)) == 0 &&
+           std::memcmp(&x.beta, &y.beta, sizeof(float)) == 0 &&
+           std::memcmp(&x.cfg, &y.cfg, sizeof(xg_config)) == 0;
+}
+
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("XG_NO_GRAPH");
+        return !(e && *e == '1');
+    }();
+    return on;
+}
+
+// Capture the four stage groups of `e` (its workspace) into graphs.
+void capture_entry(GraphEntry& e) {
+    static thread_local cudaStream_t cs = nullptr;
+    if (!cs) ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
+    for (int st = 0; st < 4; ++st) {
+        cudaGraph_t g = nullptr;
+        ck(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
+        int64_t n = 0;
+        try {
+            n = enqueue_stage(st, e.key, e.ws, nullptr, cs);
+        } catch (...) {
+            cudaStreamEndCapture(cs, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        ck(cudaStreamEndCapture(cs, &g), "end capture");
+        const cudaError_t r = cudaGraphInstantiate(&e.exec[st], g, 0);
+        cudaGraphDestroy(g);
+        ck(r, "graph instantiate");
+        e.launches[st] = n;
+        g_launches -= n;  // counted again at every replay
     }
-    gemm_comp(p, out, c, alpha, beta);
-    tm.mark();  // 4 xxmm + fused package
-    xg::DevScalars h;
-    ck(cudaMemcpyAsync(&h, p.sc, sizeof h, cudaMemcpyDeviceToHost, s), "report");
-    ck(cudaStreamSynchronize(s), "pipeline");
+}
+
+// Returns the entry to replay (marked busy), or nullptr for the eager path.
+GraphEntry* graph_acquire(const PipeCall& q) {
+    if (!graphs_enabled()) return nullptr;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    GraphEntry* hit = nullptr;
+    for (auto& e : g_graphs)
+        if (e.dev == dev && same_call(e.key, q)) hit = &e;
+    if (hit) {
+        if (hit->busy) return nullptr;
+        hit->last = ++g_graph_clock;
+        if (++hit->hits < 2) return nullptr;
+        hit->busy = true;
+        return hit;
+    }
+    GraphEntry* v = nullptr;  // first use: remember the call, run it eagerly
+    for (auto& e : g_graphs)
+        if (!e.busy && (!v || e.last < v->last)) v = &e;
+    if (!v) return nullptr;
+    v->release();
+    v->key = q;
+    v->dev = dev;
+    v->hits = 1;
+    v->last = ++g_graph_clock;
+    return nullptr;
+}
+
+void graph_release(GraphEntry* e, bool failed) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    if (failed) {
+        e->release();
+        e->dev = -1;
+        e->hits = 0;
+    }
+    e->busy = false;
+}
+
+void finish_report(const xg::DevScalars& h, int reduce, EventTimer& tm, xg_report* rep) {
     req(!h.nonfinite, "xigemm: inputs must be finite");
     if (rep) {
         rep->density_a = h.densA;
@@ -431,6 +572,71 @@ void run_pipeline(const float* a, const float* b, const float* c, float alpha, f
         rep->ns_gemm_df = tm.ns(1, 2);
         rep->ns_gemm_comp = tm.ns(3, 4);
     }
+}
+
+void run_pipeline(const float* a, const float* b, const float* c, float alpha, float beta, int M,
+                  int K, int N, const xg_config* cfg, int reduce, float* out, xg_report* rep,
+                  xg_dump* dump, cudaStream_t s) {
+    validate_cfg(cfg);
+    req(M >= 1 && K >= 1 && N >= 1, "xigemm: matrix dimensions must be >= 1");
+    req(a && b && out, "xigemm: null matrix");
+    req(K <= xg::gemm_max_inner(cfg->bits), "gemm_int: inner dimension permits 32-bit overflow");
+    PipeCall q{a, b, c, alpha, beta, M, K, N, *cfg, reduce, out};
+    const int64_t ldk = pad16(K);
+    EventTimer tm(rep != nullptr, s);
+    xg::DevScalars h;
+
+    GraphEntry* e = dump ? nullptr : graph_acquire(q);
+    if (e) {
+        bool failed = true;
+        try {
+            if (!e->exec[0]) {
+                // persistent workspace of this entry, one allocation
+                int64_t total = 0;
+                alloc_ws(e->ws, M, N, ldk, [&](auto* tag, int64_t n) {
+                    using T = std::remove_pointer_t<decltype(tag)>;
+                    const int64_t off = total;
+                    total += ((int64_t)(n > 0 ? n : 1) * (int64_t)sizeof(T) + 255) / 256 * 256;
+                    return reinterpret_cast<T*>(off);
+                });
+                ck(cudaMalloc(&e->ws_base, (size_t)total), "workspace");
+                alloc_ws(e->ws, M, N, ldk, [&, off = (int64_t)0](auto* tag, int64_t n) mutable {
+                    using T = std::remove_pointer_t<decltype(tag)>;
+                    T* p = reinterpret_cast<T*>(static_cast<char*>(e->ws_base) + off);
+                    off += ((int64_t)(n > 0 ? n : 1) * (int64_t)sizeof(T) + 255) / 256 * 256;
+                    return p;
+                });
+                capture_entry(*e);
+            }
+            for (int st = 0; st < 4; ++st) {
+                tm.mark();
+                ck(cudaGraphLaunch(e->exec[st], s), "graph launch");
+                g_launches += e->launches[st];
+            }
+            tm.mark();
+            ck(cudaMemcpyAsync(&h, e->ws.sc, sizeof h, cudaMemcpyDeviceToHost, s), "report");
+            ck(cudaStreamSynchronize(s), "pipeline");
+            failed = false;
+        } catch (...) {
+            graph_release(e, true);
+            throw;
+        }
+        graph_release(e, failed);
+        finish_report(h, reduce, tm, rep);
+        return;
+    }
+
+    Scratch S(s);
+    PipeWs w;
+    alloc_ws(w, M, N, ldk, [&](auto* tag, int64_t n) { return S.get<std::remove_pointer_t<decltype(tag)>>(n); });
+    for (int st = 0; st < 4; ++st) {
+        tm.mark();
+        enqueue_stage(st, q, w, dump, s);
+    }
+    tm.mark();
+    ck(cudaMemcpyAsync(&h, w.sc, sizeof h, cudaMemcpyDeviceToHost, s), "report");
+    ck(cudaStreamSynchronize(s), "pipeline");
+    finish_report(h, reduce, tm, rep);
 }
 
 void run_direct(const float* a, const float* b, int M, int K, int N, const xg_config* cfg,
@@ -541,6 +747,15 @@ xg_status xg_workspace_release(void) {
         cudaMemPool_t pool;
         ck(cudaDeviceGetDefaultMemPool(&pool, dev), "pool");
         ck(cudaDeviceSynchronize(), "sync");
+        {   // cached graphs and their workspaces (entries in use are kept)
+            std::lock_guard<std::mutex> lk(g_graph_mu);
+            for (auto& e : g_graphs)
+                if (!e.busy && e.dev == dev) {
+                    e.release();
+                    e.dev = -1;
+                    e.hits = 0;
+                }
+        }
         ck(cudaMemPoolTrimTo(pool, 0), "trim");
     });
 }
