@@ -1292,6 +1292,181 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// ============================================================ row kernels, r4
+// One 128-thread CTA (4 warps) per row, 8 CTAs per SM.  Compared with the
+// 256-thread ring kernels above: one CTA barrier per row instead of three (the
+// dequant table is double-buffered, so building row i+1's table never waits
+// for row i's readers), plain 16-byte streaming loads issued U at a time per
+// lane for memory-level parallelism, and 7 rows per CTA so the static
+// row-to-CTA assignment leaves no long tail.
+constexpr int kRT = 128;
+constexpr int kRCtasPerSM = 8;
+
+__device__ __forceinline__ float4 ld_stream(const float* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// the 2*qmax+1 entries float(q / lam) (quantize.cpp:156), exact: fast product
+// with a proven-safe rounding check, fp64 division otherwise
+__device__ __forceinline__ void build_row_lut(float* lut, double lam, int qmax) {
+    const double inv = __ddiv_rn(1.0, lam);
+    for (int e = threadIdx.x; e <= 2 * qmax; e += kRT) lut[e] = dequant_fast(e - qmax, inv, lam);
+}
+
+template <int U>
+__global__ void __launch_bounds__(kRT, kRCtasPerSM) k_select_rows_r4(const SelectArgs a) {
+    __shared__ float lut[2][256];
+    __shared__ float redf[kRT / 32];
+    __shared__ unsigned long long redu[kRT / 32];
+    const int qmax = quant_max(a.bits);
+    const float qmaxf = (float)qmax;
+    const double lam_r = compute_scale((double)__uint_as_float(*a.rmax), a.bits);
+    const float lam_r32 = __double2float_rn(lam_r);
+    const double lam_t = a.vec ? 0.0 : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
+    const double so = a.do_select && a.policy == kMin ? compute_scale((double)__uint_as_float(*a.other_max), a.bits)
+                                                     : 1.0;
+    unsigned cnt = 0;
+    float ret = 0.0f;
+    int it = 0;
+    for (int r = blockIdx.x; r < a.rows; r += gridDim.x, ++it) {
+        const double lam = a.vec ? a.lam[r] : lam_t;
+        const float tf = a.do_select ? float_above(threshold_of(a.policy, a.thr_m, a.stat[r], so, a.cols))
+                                     : __int_as_float(0x7f800000);
+        float* tb = lut[it & 1];
+        build_row_lut(tb, lam, qmax);
+        __syncthreads();  // table of this row complete (and the previous row's readers are past it)
+        const float lam32 = __double2float_rn(lam);
+        const bool exact = !(lam32 <= FLT_MAX) || !(lam_r32 <= FLT_MAX);
+        const uint32_t adj = smem_u32(tb) + 4u * (uint32_t)qmax - 4u * 0x4B400000u;
+        const float* row = a.x + (int64_t)r * a.ld;
+        int8_t* rq_row = a.rq + (int64_t)r * a.ldq;
+        int8_t* rd_row = a.red + (int64_t)r * a.ldq;
+        float lmax = 0.0f;
+        for (int c0 = threadIdx.x * 4; c0 < a.cols; c0 += kRT * 4 * U) {
+            float4 f[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int c = c0 + u * kRT * 4;
+                f[u] = c < a.cols ? ld_stream(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int c = c0 + u * kRT * 4;
+                if (c < a.cols) {
+                    const float x[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
+                    uint32_t pq, pr;
+                    select_quad_n<2>(x, adj, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, pq, pr, cnt, lmax);
+                    *reinterpret_cast<uint32_t*>(rq_row + c) = pq;
+                    if (a.do_select) *reinterpret_cast<uint32_t*>(rd_row + c) = pr;
+                }
+            }
+        }
+        ret = fmaxf(ret, lmax >= tf ? lmax : 0.0f);
+    }
+    if (a.do_select) {
+        unsigned long long c64 = warp_sum((unsigned long long)cnt);
+        float rr = warp_maxf(ret);
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        if (l == 0) { redu[w] = c64; redf[w] = rr; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int i = 1; i < kRT / 32; ++i) { c64 += redu[i]; rr = fmaxf(rr, redf[i]); }
+            if (c64) atomicAdd(a.nnz, c64);
+            atomicMax(a.retmax, fbits(rr));
+        }
+    }
+}
+
+// K1, A side: the row lives in registers (VPT float4 per thread), absmax ->
+// lambda -> table -> quantise -> residual max; two CTA barriers per row.
+template <int VPT>
+__global__ void __launch_bounds__(kRT, 4) k_quant_rows_r4(const QuantRowsArgs a) {
+    __shared__ float lut[2][256];
+    __shared__ float red[2][kRT / 32];
+    const int qmax = quant_max(a.bits);
+    const float qmaxf = (float)qmax;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    float rmax_acc = 0.0f, gmax_acc = 0.0f;
+    int bad = 0;
+    int it = 0;
+    for (int r = blockIdx.x; r < a.rows; r += gridDim.x, ++it) {
+        const float* row = a.x + (int64_t)r * a.ld;
+        float4 f[VPT];
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            const int c = (v * kRT + (int)threadIdx.x) * 4;
+            f[v] = c < a.cols ? ld_stream(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float m = 0.0f, sum = 0.0f;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(f[v].x), fabsf(f[v].y)), fmaxf(fabsf(f[v].z), fabsf(f[v].w))));
+            sum = __fadd_rn(sum, __fadd_rn(__fadd_rn(f[v].x, f[v].y), __fadd_rn(f[v].z, f[v].w)));
+        }
+        const bool odd = !(fabsf(sum) <= FLT_MAX);  // NaN / inf somewhere (or a finite overflow)
+        if (odd) {
+#pragma unroll
+            for (int v = 0; v < VPT; ++v)
+                bad |= (fabsf(f[v].x) <= FLT_MAX && fabsf(f[v].y) <= FLT_MAX && fabsf(f[v].z) <= FLT_MAX &&
+                        fabsf(f[v].w) <= FLT_MAX) ? 0 : 2;
+        }
+        m = warp_maxf(m);
+        float* rb = red[it & 1];
+        if (l == 0) rb[w] = m;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kRT / 32; ++i) m = fmaxf(m, rb[i]);
+        bad |= m > FLT_MAX ? 1 : 0;
+        gmax_acc = fmaxf(gmax_acc, m);
+        double lam;
+        if (a.per_row) {
+            lam = compute_scale((double)m, a.bits);
+            if (threadIdx.x == 0 && a.lam_out) a.lam_out[r] = lam;
+        } else {
+            lam = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
+        }
+        float* tb = lut[it & 1];
+        build_row_lut(tb, lam, qmax);
+        __syncthreads();
+        const float lam32 = __double2float_rn(lam);
+        const bool exact = odd || !(lam32 <= FLT_MAX);
+        const uint32_t adj = smem_u32(tb) + 4u * (uint32_t)qmax - 4u * 0x4B400000u;
+        float rm = 0.0f;
+        int8_t* qrow = a.q + (int64_t)r * a.ldq;
+#pragma unroll
+        for (int v = 0; v < VPT; ++v) {
+            const int c = (v * kRT + (int)threadIdx.x) * 4;
+            const float x[4] = {f[v].x, f[v].y, f[v].z, f[v].w};
+            uint32_t u[4];
+            float dmax = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) u[e] = qn(x[e], lam32, dmax);
+            if (exact || !(dmax < 0.4999f)) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(x[e], lam, qmaxf, kNearest));
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[e], lds_f32((u[e] << 2) + adj))));
+            if (c < a.cols) *reinterpret_cast<uint32_t*>(qrow + c) = pack4u(u[0], u[1], u[2], u[3]);
+        }
+        rmax_acc = fmaxf(rmax_acc, rm);
+    }
+    rmax_acc = warp_maxf(rmax_acc);
+    __syncthreads();
+    if (l == 0) red[0][w] = rmax_acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < kRT / 32; ++i) rmax_acc = fmaxf(rmax_acc, red[0][i]);
+        if (a.rmax) atomicMax(a.rmax, fbits(rmax_acc));
+        if (a.gmax) atomicMax(a.gmax, fbits(gmax_acc));
+    }
+    if (bad && a.nonfinite) atomicOr(a.nonfinite, bad);
+}
+
 // ------------------------------------------------------------- scalars --
 __global__ void k_lambdas(DevScalars* sc, int bits) {
     sc->lamA = compute_scale((double)__uint_as_float(sc->maxA), bits);
@@ -1344,6 +1519,14 @@ bool async_enabled() {
     return on;
 }
 
+bool r4_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("XG_NO_R4");
+        return !(e && *e == '1');
+    }();
+    return on;
+}
+
 // persistent grid: as many CTAs as fit (by shared memory) on every SM
 int async_grid(int rows, int smem_bytes) {
     const int per_sm = smem_bytes <= 70 * 1024 ? 3 : smem_bytes <= 105 * 1024 ? 2 : 1;
@@ -1380,6 +1563,15 @@ void quant_rows_rnd(const QuantRowsArgs& a, cudaStream_t s) {
 void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
     const bool aligned = (a.ld % 4 == 0) && (a.ldq % 4 == 0) && (a.cols % 4 == 0) &&
                          ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+    if (a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 8192 && r4_enabled()) {
+        const int vpt = (a.cols + kRT * 4 - 1) / (kRT * 4);
+        const int g = a.rows < kNumSMs * 4 ? a.rows : kNumSMs * 4;
+        if (vpt <= 2) k_quant_rows_r4<2><<<g, kRT, 0, s>>>(a);
+        else if (vpt <= 4) k_quant_rows_r4<4><<<g, kRT, 0, s>>>(a);
+        else if (vpt <= 8) k_quant_rows_r4<8><<<g, kRT, 0, s>>>(a);
+        else k_quant_rows_r4<16><<<g, kRT, 0, s>>>(a);
+        return;
+    }
     if (a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 16384 && async_enabled()) {
         const int bytes = kRowSlots * a.cols * 4;
         set_dyn_smem(k_quant_rows_async, bytes);
@@ -1429,6 +1621,11 @@ void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {
 void launch_select_rows(const SelectArgs& a, cudaStream_t s) {
     const bool aligned = (a.ld % 4 == 0) && (a.ldq % 4 == 0) && (a.cols % 4 == 0) &&
                          ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+    if (!a.fix_mode && a.rounding == kNearest && aligned && a.cols >= 512 && r4_enabled()) {
+        const int g = a.rows < kNumSMs * kRCtasPerSM ? a.rows : kNumSMs * kRCtasPerSM;
+        k_select_rows_r4<4><<<g, kRT, 0, s>>>(a);
+        return;
+    }
     if (!a.fix_mode && a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 16384 &&
         async_enabled()) {
         const int bytes = kRowSlots * a.cols * 4;
