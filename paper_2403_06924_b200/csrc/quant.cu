@@ -1467,6 +1467,172 @@ __global__ void __launch_bounds__(kRT, 4) k_quant_rows_r4(const QuantRowsArgs a)
     if (bad && a.nonfinite) atomicOr(a.nonfinite, bad);
 }
 
+// ============================================================ column kernels, w4
+// B side (K x N row-major in, N x K K-major int8 out).  One 4-warp CTA works on
+// an item = 32-column strip x 1024 rows; each warp streams its own 256 rows as
+// 32 x 32 fp32 sub-tiles through a private 4-deep TMA ring (own mbarriers, no
+// CTA barrier inside the item).  Lane l owns column l: it reads its column of
+// the tile conflict-free, quantises 4 consecutive rows into one word, and
+// writes its 32 output bytes of row n of B^T itself (two 16-byte stores), so
+// no shared-memory transpose is needed.  The per-strip dequant tables
+// lut[q][lane] are built once per item (2 CTA barriers per item).
+constexpr int kWC = 32, kWR = 32, kWItemRows = 1024, kWSlots = 2, kWW = 8;
+constexpr int kWCtas = 2;
+constexpr int kWSub = kWItemRows / (kWW * kWR);  // sub-tiles per warp per item
+constexpr int kColWSmem = kWW * kWSlots * kWC * kWR * 4 + 256 * kWC * 4 + 1024;
+
+template <bool SELECT>
+__global__ void __launch_bounds__(kWW * 32, kWCtas)
+    k_cols_w4(const __grid_constant__ CUtensorMap tmap, const QuantColsArgs qa, const SelectArgs sa) {
+    extern __shared__ float4 dyn_smem[];
+    float* ring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
+    float(*lut)[kWC] = reinterpret_cast<float(*)[kWC]>(ring + kWW * kWSlots * kWC * kWR);
+    __shared__ uint64_t full[kWW][kWSlots];
+    __shared__ float redf[kWW];
+    __shared__ unsigned long long redu[kWW];
+    const int rows = SELECT ? sa.rows : qa.rows, cols = SELECT ? sa.cols : qa.cols;
+    const int bits = SELECT ? sa.bits : qa.bits;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qmax = quant_max(bits);
+    const float qmaxf = (float)qmax;
+    const int nstrips = (cols + kWC - 1) / kWC;
+    const int nchunks = (rows + kWItemRows - 1) / kWItemRows;
+    const int nitems = nstrips * nchunks;
+    const int my_items = nitems > (int)blockIdx.x ? (nitems - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    const int nsub = my_items * kWSub;  // sub-tiles this warp will consume
+    double lam_r = 0.0, lam_t = 0.0, so = 1.0;
+    if (SELECT) {
+        lam_r = compute_scale((double)__uint_as_float(*sa.rmax), bits);
+        lam_t = sa.vec ? 0.0 : compute_scale((double)__uint_as_float(*sa.tensor_max), bits);
+        if (sa.do_select && sa.policy == kMin) so = compute_scale((double)__uint_as_float(*sa.other_max), bits);
+    } else if (!qa.per_col) {
+        lam_t = compute_scale((double)__uint_as_float(*qa.tensor_max), bits);
+    }
+    const float lam_r32 = __double2float_rn(lam_r);
+    float* wring = ring + w * kWSlots * kWC * kWR;
+    auto issue = [&](int g) {  // sub-tile g of this warp's sequence into slot g % kWSlots
+        const int item = (int)blockIdx.x + (g / kWSub) * (int)gridDim.x;
+        const int strip = item % nstrips, chunk = item / nstrips;
+        const int slot = g % kWSlots;
+        mbar_expect_tx(&full[w][slot], kWC * kWR * 4);
+        tma_load_2d(wring + slot * kWC * kWR, &tmap, &full[w][slot], strip * kWC,
+                    chunk * kWItemRows + (w * kWSub + g % kWSub) * kWR);
+    };
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tmap);
+        for (int i = 0; i < kWW; ++i)
+            for (int j = 0; j < kWSlots; ++j) mbar_init(&full[i][j], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (lane == 0)
+        for (int g = 0; g < kWSlots && g < nsub; ++g) issue(g);
+    const uint32_t adj_base = smem_u32(&lut[0][0]) + 4u * lane + 128u * (uint32_t)qmax - 128u * 0x4B400000u;
+    float rm = 0.0f, ret = 0.0f;
+    unsigned cnt = 0;
+    int g = 0;
+    for (int i = 0; i < my_items; ++i) {
+        const int item = (int)blockIdx.x + i * (int)gridDim.x;
+        const int strip = item % nstrips, chunk = item / nstrips;
+        const int n = strip * kWC + lane;
+        const int nc = min(n, cols - 1);
+        double lam;
+        if (SELECT) lam = sa.vec ? sa.lam[nc] : lam_t;
+        else lam = qa.per_col ? compute_scale((double)__uint_as_float(qa.colmax[nc]), bits) : lam_t;
+        if (!SELECT && qa.per_col && qa.lam_out && chunk == 0 && w == 0 && n < cols) qa.lam_out[n] = lam;
+        const float lam32 = __double2float_rn(lam);
+        const bool exact = !(lam32 <= FLT_MAX) || (SELECT && !(lam_r32 <= FLT_MAX));
+        float tf = __int_as_float(0x7f800000);
+        if (SELECT && sa.do_select && n < cols) tf = float_above(threshold_of(sa.policy, sa.thr_m, sa.stat[nc], so, rows));
+        __syncthreads();  // previous item's table readers are done
+        {
+            const double inv = __ddiv_rn(1.0, lam);
+            for (int e = w * (256 / kWW); e < (w + 1) * (256 / kWW); ++e)
+                if (e <= 2 * qmax) lut[e][lane] = dequant_fast(e - qmax, inv, lam);
+        }
+        __syncthreads();
+        float lmax = 0.0f;
+        for (int j = 0; j < kWSub; ++j, ++g) {
+            const int slot = g % kWSlots;
+            const int k0 = chunk * kWItemRows + (w * kWSub + j) * kWR;
+            mbar_wait(&full[w][slot], (g / kWSlots) & 1);
+            const float* tile = wring + slot * kWC * kWR;
+            float x[kWR];
+#pragma unroll
+            for (int r = 0; r < kWR; ++r) x[r] = tile[r * kWC + lane];
+            __syncwarp();
+            if (lane == 0 && g + kWSlots < nsub) {
+                fence_proxy_async();
+                issue(g + kWSlots);
+            }
+            uint32_t w0[kWR / 4], w1[kWR / 4];
+#pragma unroll
+            for (int q = 0; q < kWR / 4; ++q) {
+                const float xq[4] = {x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]};
+                if (SELECT) {
+                    select_quad_n<7>(xq, adj_base, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, w0[q], w1[q],
+                                     cnt, lmax);
+                } else {
+                    uint32_t u[4];
+                    float dmax = 0.0f;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) u[e] = qn(xq[e], lam32, dmax);
+                    if (exact || !(dmax < 0.4999f)) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(xq[e], lam, qmaxf, kNearest));
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(xq[e], lds_f32((u[e] << 7) + adj_base))));
+                    w0[q] = pack4u(u[0], u[1], u[2], u[3]);
+                }
+            }
+            if (n < cols && k0 < rows) {
+                int8_t* d0 = (SELECT ? sa.rq : qa.qT) + (int64_t)n * (SELECT ? sa.ldq : qa.ldq) + k0;
+                int8_t* d1 = SELECT && sa.do_select ? sa.red + (int64_t)n * sa.ldq + k0 : nullptr;
+                if (k0 + kWR <= rows) {
+#pragma unroll
+                    for (int v = 0; v < kWR / 16; ++v) {
+                        reinterpret_cast<uint4*>(d0)[v] = make_uint4(w0[4 * v], w0[4 * v + 1], w0[4 * v + 2], w0[4 * v + 3]);
+                        if (d1) reinterpret_cast<uint4*>(d1)[v] = make_uint4(w1[4 * v], w1[4 * v + 1], w1[4 * v + 2], w1[4 * v + 3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < kWR / 4; ++q)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (4 * q + e < rows - k0) {
+                                d0[4 * q + e] = (int8_t)(w0[q] >> (8 * e));
+                                if (d1) d1[4 * q + e] = (int8_t)(w1[q] >> (8 * e));
+                            }
+                }
+            }
+        }
+        if (SELECT) ret = fmaxf(ret, lmax >= tf ? lmax : 0.0f);
+    }
+    // block reductions (all warps reach here)
+    if (SELECT) {
+        if (sa.do_select) {
+            unsigned long long c64 = warp_sum((unsigned long long)cnt);
+            float rr = warp_maxf(ret);
+            if (lane == 0) { redu[w] = c64; redf[w] = rr; }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int i = 1; i < kWW; ++i) { c64 += redu[i]; rr = fmaxf(rr, redf[i]); }
+                if (c64) atomicAdd(sa.nnz, c64);
+                atomicMax(sa.retmax, fbits(rr));
+            }
+        }
+    } else {
+        float r = warp_maxf(rm);
+        if (lane == 0) redf[w] = r;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int i = 1; i < kWW; ++i) r = fmaxf(r, redf[i]);
+            if (qa.rmax) atomicMax(qa.rmax, fbits(r));
+        }
+    }
+}
+
 // ------------------------------------------------------------- scalars --
 __global__ void k_lambdas(DevScalars* sc, int bits) {
     sc->lamA = compute_scale((double)__uint_as_float(sc->maxA), bits);
@@ -1599,7 +1765,21 @@ int col_async_grid(int rows, int cols) {
     return items < g ? items : g;
 }
 
+int col_w4_grid(int rows, int cols) {
+    const int items = ((cols + kWC - 1) / kWC) * ((rows + kWItemRows - 1) / kWItemRows);
+    const int g = kNumSMs * kWCtas;
+    return items < g ? items : g;
+}
+
 void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {
+    if (a.rounding == kNearest && r4_enabled() && a.rows >= 256 && (a.ldq % 16) == 0) {
+        alignas(64) CUtensorMap tm;
+        if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) {
+            set_dyn_smem(k_cols_w4<false>, kColWSmem);
+            k_cols_w4<false><<<col_w4_grid(a.rows, a.cols), kWW * 32, kColWSmem, s>>>(tm, a, SelectArgs{});
+            return;
+        }
+    }
     if (a.rounding == kNearest && async_enabled() && a.rows >= 512) {
         alignas(64) CUtensorMap tm;
         if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kCT, kCR)) {
@@ -1645,6 +1825,14 @@ void launch_select_cols_T(const SelectArgs& a, cudaStream_t s) {
     if (a.fix_mode) {
         k_fix_cols_T<<<grid_rows(a.cols), kThreads, 0, s>>>(a);
         return;
+    }
+    if (a.rounding == kNearest && r4_enabled() && a.rows >= 256 && (a.ldq % 16) == 0) {
+        alignas(64) CUtensorMap tm;
+        if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) {
+            set_dyn_smem(k_cols_w4<true>, kColWSmem);
+            k_cols_w4<true><<<col_w4_grid(a.rows, a.cols), kWW * 32, kColWSmem, s>>>(tm, QuantColsArgs{}, a);
+            return;
+        }
     }
     if (a.rounding == kNearest && async_enabled() && a.rows >= 512) {
         alignas(64) CUtensorMap tm;
