@@ -171,15 +171,60 @@ struct Pipe {
     uint32_t* colmax;
 };
 
+// Second stream for the independent A-side / B-side memory-bound kernels of
+// K1 and K3 (thread-local per device so concurrent callers and graph capture
+// never share it).  fork(): aux waits for work queued on s so far; join(): s
+// waits for everything queued on aux.
+struct Aux {
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+Aux& aux_stream() {
+    thread_local Aux a[16];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Aux& x = a[dev & 15];
+    if (!x.s2) {
+        ck(cudaStreamCreateWithFlags(&x.s2, cudaStreamNonBlocking), "aux stream");
+        for (auto& e : x.ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "aux event");
+    }
+    return x;
+}
+// Opt-in (XG_COSCHED=1): measured slower on B200 at C3 (quant 220->281 us,
+// reduce 309->454 us) -- the persistent grids split the SMs but the two sides
+// do not finish together, so each runs part of the time at half width.
+bool coschedule_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("XG_COSCHED");
+        return e && *e == '1';
+    }();
+    return on;
+}
+cudaStream_t fork(cudaStream_t s) {
+    Aux& x = aux_stream();
+    ck(cudaEventRecord(x.ev[0], s), "fork");
+    ck(cudaStreamWaitEvent(x.s2, x.ev[0], 0), "fork");
+    return x.s2;
+}
+void join(cudaStream_t s) {
+    Aux& x = aux_stream();
+    ck(cudaEventRecord(x.ev[1], x.s2), "join");
+    ck(cudaStreamWaitEvent(s, x.ev[1], 0), "join");
+}
+
 void quantize_operands(Pipe& p, const float* a, const float* b) {
     using namespace xg;
     const int bits = p.cfg->bits, rnd = p.cfg->rounding;
+    // A side on p.s, B side on the aux stream, sharing the SMs
+    const bool co = coschedule_enabled();
+    cudaStream_t sb = co ? fork(p.s) : p.s;
     // --- A: per row (VectorWise) or per tensor
     QuantRowsArgs qa{};
     qa.x = a; qa.rows = p.M; qa.cols = p.K; qa.ld = p.K;
     qa.bits = bits; qa.rounding = rnd;
     qa.q = p.aq; qa.ldq = p.ldk;
     qa.rmax = &p.sc->maxRA; qa.nonfinite = &p.sc->nonfinite;
+    qa.co_share = co ? 2 : 0;
     if (p.vw) {
         qa.per_row = 1; qa.lam_out = p.la; qa.gmax = &p.sc->maxA;
     } else {
@@ -194,18 +239,20 @@ void quantize_operands(Pipe& p, const float* a, const float* b) {
     qb.x = b; qb.rows = p.K; qb.cols = p.N; qb.ld = p.N;
     qb.bits = bits; qb.rounding = rnd;
     qb.qT = p.bqT; qb.ldq = p.ldk; qb.rmax = &p.sc->maxRB;
+    qb.co_share = co ? 1 : 0;
     if (p.vw) {
-        ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, p.s), "memset");
-        launch_absmax_cols(b, p.K, p.N, p.N, p.colmax, &p.sc->maxB, &p.sc->nonfinite, p.s);
+        ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, sb), "memset");
+        launch_absmax_cols(b, p.K, p.N, p.N, p.colmax, &p.sc->maxB, &p.sc->nonfinite, sb);
         check_launch("absmax B cols");
         qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb;
     } else {
-        launch_absmax_global(b, (int64_t)p.K * p.N, &p.sc->maxB, &p.sc->nonfinite, p.s);
+        launch_absmax_global(b, (int64_t)p.K * p.N, &p.sc->maxB, &p.sc->nonfinite, sb);
         check_launch("absmax B");
         qb.per_col = 0; qb.tensor_max = &p.sc->maxB;
     }
-    launch_quant_cols_T(qb, p.s);
+    launch_quant_cols_T(qb, sb);
     check_launch("quantize B");
+    if (co) join(p.s);
     launch_lambdas(p.sc, bits, p.s);
     check_launch("lambdas");
 }
@@ -237,16 +284,21 @@ void select_operands(Pipe& p, const float* a, const float* b, int reduce, const 
     sa.other_max = &p.sc->maxB;
     sa.rq = p.raq; sa.red = p.ared; sa.ldq = p.ldk;
     sa.nnz = &p.sc->nnzA; sa.retmax = &p.sc->retA;
+    const bool co = coschedule_enabled();
+    cudaStream_t s2 = co ? fork(p.s) : p.s;
+    sa.co_share = co ? 4 : 0;
     launch_select_rows(sa, p.s);
     check_launch("select A");
     SelectArgs sb = sa;
+    sb.co_share = co ? 1 : 0;
     sb.x = b; sb.rows = p.K; sb.cols = p.N; sb.ld = p.N;
     sb.lam = p.lb; sb.tensor_max = &p.sc->maxB; sb.rmax = &p.sc->maxRB;
     sb.stat = cstat; sb.other_max = &p.sc->maxA;
     sb.rq = p.rbqT; sb.red = p.bredT;
     sb.nnz = &p.sc->nnzB; sb.retmax = &p.sc->retB;
-    launch_select_cols_T(sb, p.s);
+    launch_select_cols_T(sb, s2);
     check_launch("select B");
+    if (co) join(p.s);
     if (reduce && !p.vw) {
         // per-tensor reduced operands: lambda' over retained values may differ
         // from the operand's scale (sparse.cpp:198-203); device-side check.

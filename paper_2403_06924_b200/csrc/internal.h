@@ -38,6 +38,7 @@ struct QuantRowsArgs {
     uint32_t* gmax;         // atomicMax of max|x| (float bits), may be null
     uint32_t* rmax;         // atomicMax of max|x - deq| (float bits), may be null
     int* nonfinite;
+    int co_share;           // host-only: CTAs per SM when co-scheduled with the B side (0: all)
 };
 
 struct QuantColsArgs {
@@ -52,6 +53,7 @@ struct QuantColsArgs {
     int8_t* qT;              // [cols x ldq] transposed (K-major)
     int64_t ldq;
     uint32_t* rmax;
+    int co_share;            // host-only: CTAs per SM when co-scheduled with the A side (0: all)
 };
 
 // K3: residual quantisation + threshold selection of the original operand.
@@ -76,6 +78,7 @@ struct SelectArgs {
     uint32_t* retmax;
     // fix-up mode: rewrite `red` with the retained-max scale when it differs
     int fix_mode;
+    int co_share;            // host-only: CTAs per SM when co-scheduled (0: all)
 };
 
 void launch_absmax_global(const float* x, int64_t n, uint32_t* gmax, int* nonfinite,

@@ -1731,7 +1731,8 @@ void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
                          ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
     if (a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 8192 && r4_enabled()) {
         const int vpt = (a.cols + kRT * 4 - 1) / (kRT * 4);
-        const int g = a.rows < kNumSMs * 4 ? a.rows : kNumSMs * 4;
+        const int cap = kNumSMs * (a.co_share > 0 ? a.co_share : 4);
+        const int g = a.rows < cap ? a.rows : cap;
         if (vpt <= 2) k_quant_rows_r4<2><<<g, kRT, 0, s>>>(a);
         else if (vpt <= 4) k_quant_rows_r4<4><<<g, kRT, 0, s>>>(a);
         else if (vpt <= 8) k_quant_rows_r4<8><<<g, kRT, 0, s>>>(a);
@@ -1765,9 +1766,9 @@ int col_async_grid(int rows, int cols) {
     return items < g ? items : g;
 }
 
-int col_w4_grid(int rows, int cols) {
+int col_w4_grid(int rows, int cols, int co_share) {
     const int items = ((cols + kWC - 1) / kWC) * ((rows + kWItemRows - 1) / kWItemRows);
-    const int g = kNumSMs * kWCtas;
+    const int g = kNumSMs * (co_share > 0 ? co_share : kWCtas);
     return items < g ? items : g;
 }
 
@@ -1776,7 +1777,7 @@ void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {
         alignas(64) CUtensorMap tm;
         if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) {
             set_dyn_smem(k_cols_w4<false>, kColWSmem);
-            k_cols_w4<false><<<col_w4_grid(a.rows, a.cols), kWW * 32, kColWSmem, s>>>(tm, a, SelectArgs{});
+            k_cols_w4<false><<<col_w4_grid(a.rows, a.cols, a.co_share), kWW * 32, kColWSmem, s>>>(tm, a, SelectArgs{});
             return;
         }
     }
@@ -1802,7 +1803,8 @@ void launch_select_rows(const SelectArgs& a, cudaStream_t s) {
     const bool aligned = (a.ld % 4 == 0) && (a.ldq % 4 == 0) && (a.cols % 4 == 0) &&
                          ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
     if (!a.fix_mode && a.rounding == kNearest && aligned && a.cols >= 512 && r4_enabled()) {
-        const int g = a.rows < kNumSMs * kRCtasPerSM ? a.rows : kNumSMs * kRCtasPerSM;
+        const int cap = kNumSMs * (a.co_share > 0 ? a.co_share : kRCtasPerSM);
+        const int g = a.rows < cap ? a.rows : cap;
         k_select_rows_r4<4><<<g, kRT, 0, s>>>(a);
         return;
     }
@@ -1830,7 +1832,7 @@ void launch_select_cols_T(const SelectArgs& a, cudaStream_t s) {
         alignas(64) CUtensorMap tm;
         if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) {
             set_dyn_smem(k_cols_w4<true>, kColWSmem);
-            k_cols_w4<true><<<col_w4_grid(a.rows, a.cols), kWW * 32, kColWSmem, s>>>(tm, QuantColsArgs{}, a);
+            k_cols_w4<true><<<col_w4_grid(a.rows, a.cols, a.co_share), kWW * 32, kColWSmem, s>>>(tm, QuantColsArgs{}, a);
             return;
         }
     }
