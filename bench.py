@@ -306,6 +306,17 @@ def run_b200(args, world, rank, local):
     else:
         name, kops, tk = "D_F GEMM (2MNK tensor ops)", 2.0 * m * n * k, t_df
     achieved = kops / tk / 1e12
+    traffic = None
+    try:  # DRAM bytes per launch of that kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r1c_gemm_traffic.json")) as f:
+            tr = json.load(f)
+        key = "void k_gemm_i8_tc2<1, 4, 1>" if t_cp >= t_df else "void k_gemm_i8_tc2<1, 1, 1>"
+        traffic = {"dram_bytes_per_launch": tr[key]["bytes_per_launch"],
+                   # int8 operands in, fp32 D_F / partial C in (compensation only), fp32 out
+                   "algorithmic_bytes_per_launch": m * k + k * n + (8 if t_cp >= t_df else 4) * m * n,
+                   "source": "profiles/r1c_gemm_traffic.json (ncu --set full, this kernel, C3)"}
+    except (OSError, KeyError, ValueError):
+        pass
     cpu = None
     if not args.no_cpu_baseline:
         v, dt, kind = cpu_baseline_sample(a.cpu().numpy(), b.cpu().numpy(), thr, args.ref_rows, 1)
@@ -323,7 +334,7 @@ def run_b200(args, world, rank, local):
                 "h2d_bytes_per_step": 4 * (m * k + k * n), "d2h_bytes_per_step": 4 * m * n},
         "roofline": {"bound": "tensor", "kernel": name, "achieved": achieved,
                      "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
-                     "traffic": None,
+                     "traffic": traffic,
                      "peak_source": f"2 x bf16_tflops ({bf16}) of MEASURED_PEAKS.json ({src}); INT8 dense = 2x bf16 on B200",
                      "gemm_df_ms": t_df * 1e3, "gemm_comp_ms": t_cp * 1e3},
         "clocks": clk.summary(),

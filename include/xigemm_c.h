@@ -182,6 +182,29 @@ xg_status xg_gemm_direct_q(const int8_t *aq, int scheme_a, const double *sa, con
                            int scheme_b, const double *sb, int m, int k, int n, int bits_a,
                            int bits_b, float *out, xg_stream s);
 
+/* ---- row-sharded xigemm (multi-GPU) ----------------
+ * The reference has no distributed path; this splits its xigemm()
+ * (pipeline.cpp:182-213) by rows of A and C across ranks with B replicated.
+ * Each rank creates a handle over its rows, then for p = 0..5 runs
+ * xg_shard_step(h, p) followed by the collectives xg_shard_exchange(h, p, i)
+ * describes (i = 0, 1, ... until *count == 0), executed by the caller on the
+ * same stream order (NCCL over NVLink, or any exact reduction):
+ *   dtype 0 uint32, 1 uint64, 2 float64, 3 float32;
+ *   op 0 MAX, 1 SUM, 2 MIN (in place on send), 3 ALLGATHER (send -> recv,
+ *   nranks * count elements in rank order).
+ * After step 5, xg_shard_finish synchronises and fills the (global) report;
+ * out_rows holds this rank's rows of the result, bit-identical to the
+ * single-GPU xg_xigemm on the full problem. */
+typedef struct xg_shard xg_shard;
+xg_status xg_shard_create(const float *a_rows, const float *b, const float *c_rows, float alpha,
+                          float beta, int rank, int nranks, const int *rank_rows, int k, int n,
+                          const xg_config *cfg, int reduce, float *out_rows, xg_shard **h);
+xg_status xg_shard_step(xg_shard *h, int step, xg_stream s);
+xg_status xg_shard_exchange(xg_shard *h, int point, int idx, void **send, void **recv,
+                            int64_t *count, int *dtype, int *op);
+xg_status xg_shard_finish(xg_shard *h, xg_report *rep, xg_stream s);
+void xg_shard_destroy(xg_shard *h);
+
 /* ---- host-buffer entry points (what the C++ drop-in binds) --------------- */
 xg_status xg_xigemm_host(const float *a, const float *b, const float *c, float alpha, float beta,
                          int m, int k, int n, const xg_config *cfg, int reduce, float *out,

@@ -82,6 +82,11 @@ _SIGS = {
     "xg_avg_vectors": (_I, [_V, _I, _I, _V, _V, _V]),
     "xg_abs_min_vectors": (_I, [_V, _I, _I, _V, _V, _V]),
     "xg_xigemm": (_I, [_V, _V, _V, _F, _F, _I, _I, _I, _V, _I, _V, _V, _V, _V]),
+    "xg_shard_create": (_I, [_V, _V, _V, _F, _F, _I, _I, _V, _I, _I, _V, _I, _V, _V]),
+    "xg_shard_step": (_I, [_V, _I, _V]),
+    "xg_shard_exchange": (_I, [_V, _I, _I, _V, _V, _V, _V, _V]),
+    "xg_shard_finish": (_I, [_V, _V, _V]),
+    "xg_shard_destroy": (None, [_V]),
     "xg_gemm_direct": (_I, [_V, _V, _I, _I, _I, _V, _V, _V]),
     "xg_gemm_direct_q": (_I, [_V, _I, _V, _V, _I, _V, _I, _I, _I, _I, _I, _V, _V]),
     "xg_xigemm_host": (_I, [_V, _V, _V, _F, _F, _I, _I, _I, _V, _I, _V, _V]),

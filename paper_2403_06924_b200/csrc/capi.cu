@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <memory>
 #include <mutex>
 #include <type_traits>
 #include <cmath>
@@ -212,9 +213,24 @@ void join(cudaStream_t s) {
     ck(cudaStreamWaitEvent(s, x.ev[1], 0), "join");
 }
 
-void quantize_operands(Pipe& p, const float* a, const float* b) {
+// phases: bit 0 = PerTensor absmax of A, bit 1 = quantise A and B, bit 2 =
+// per-tensor lambdas.  The single-GPU pipeline runs all three back to back;
+// the row-sharded one reduces max|A| across ranks between bits 0 and 1 and
+// max|A|, max|RA| between bits 1 and 2.
+void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) {
     using namespace xg;
     const int bits = p.cfg->bits, rnd = p.cfg->rounding;
+    if ((phases & 1) && !p.vw) {
+        launch_absmax_global(a, (int64_t)p.M * p.K, &p.sc->maxA, &p.sc->nonfinite, p.s);
+        check_launch("absmax A");
+    }
+    if (!(phases & 2)) {
+        if (phases & 4) {
+            launch_lambdas(p.sc, bits, p.s);
+            check_launch("lambdas");
+        }
+        return;
+    }
     // A side on p.s, B side on the aux stream, sharing the SMs
     const bool co = coschedule_enabled();
     cudaStream_t sb = co ? fork(p.s) : p.s;
@@ -228,8 +244,6 @@ void quantize_operands(Pipe& p, const float* a, const float* b) {
     if (p.vw) {
         qa.per_row = 1; qa.lam_out = p.la; qa.gmax = &p.sc->maxA;
     } else {
-        launch_absmax_global(a, (int64_t)p.M * p.K, &p.sc->maxA, &p.sc->nonfinite, p.s);
-        check_launch("absmax A");
         qa.per_row = 0; qa.tensor_max = &p.sc->maxA;
     }
     launch_quant_rows(qa, p.s);
@@ -253,8 +267,10 @@ void quantize_operands(Pipe& p, const float* a, const float* b) {
     launch_quant_cols_T(qb, sb);
     check_launch("quantize B");
     if (co) join(p.s);
-    launch_lambdas(p.sc, bits, p.s);
-    check_launch("lambdas");
+    if (phases & 4) {
+        launch_lambdas(p.sc, bits, p.s);
+        check_launch("lambdas");
+    }
 }
 
 void gemm_df(Pipe& p, float* out) {
@@ -273,7 +289,7 @@ void gemm_df(Pipe& p, float* out) {
 }
 
 void select_operands(Pipe& p, const float* a, const float* b, int reduce, const float* rstat,
-                     const float* cstat) {
+                     const float* cstat, int phases = 3) {  // bit 0 select, bit 1 PerTensor fix-ups
     using namespace xg;
     const int bits = p.cfg->bits, rnd = p.cfg->rounding;
     SelectArgs sa{};
@@ -284,22 +300,26 @@ void select_operands(Pipe& p, const float* a, const float* b, int reduce, const 
     sa.other_max = &p.sc->maxB;
     sa.rq = p.raq; sa.red = p.ared; sa.ldq = p.ldk;
     sa.nnz = &p.sc->nnzA; sa.retmax = &p.sc->retA;
-    const bool co = coschedule_enabled();
-    cudaStream_t s2 = co ? fork(p.s) : p.s;
-    sa.co_share = co ? 4 : 0;
-    launch_select_rows(sa, p.s);
-    check_launch("select A");
     SelectArgs sb = sa;
-    sb.co_share = co ? 1 : 0;
     sb.x = b; sb.rows = p.K; sb.cols = p.N; sb.ld = p.N;
     sb.lam = p.lb; sb.tensor_max = &p.sc->maxB; sb.rmax = &p.sc->maxRB;
     sb.stat = cstat; sb.other_max = &p.sc->maxA;
     sb.rq = p.rbqT; sb.red = p.bredT;
     sb.nnz = &p.sc->nnzB; sb.retmax = &p.sc->retB;
+    if (!(phases & 1)) goto fixups;
+    {
+    const bool co = coschedule_enabled();
+    cudaStream_t s2 = co ? fork(p.s) : p.s;
+    sa.co_share = co ? 4 : 0;
+    launch_select_rows(sa, p.s);
+    check_launch("select A");
+    sb.co_share = co ? 1 : 0;
     launch_select_cols_T(sb, s2);
     check_launch("select B");
     if (co) join(p.s);
-    if (reduce && !p.vw) {
+    }
+fixups:
+    if ((phases & 2) && reduce && !p.vw) {
         // per-tensor reduced operands: lambda' over retained values may differ
         // from the operand's scale (sparse.cpp:198-203); device-side check.
         SelectArgs fa = sa;
@@ -1197,6 +1217,266 @@ xg_status xg_abs_min_vectors(const float* d, int rows, int cols, float* row, flo
         check_launch("min", 3);
     });
 }
+
+}  // extern "C"
+
+namespace {
+
+// ===================================================== row-sharded pipeline
+// A and C are split by rows across ranks, B is replicated
+// (every rank redoes the B-side stages).  The pipeline is not reduction-free:
+// the exact couplings are
+//   point 0  max|A| (PerTensor scale)                          uint32 MAX
+//   point 1  max|A|, max|RA| (lambda_RA, MinRule scale), NaN    uint32 MAX
+//   point 2  column statistics of D_F: fp64 sums (AvgRule)     fp64 SUM
+//            or float-bit minima (MinRule)                     uint32 MIN
+//   point 3  D_F columns whose AvgRule mean needs the exact sequential sum
+//            (rare; fixed-size buffer)                         ALLGATHER
+//   point 4  nnz(A') (density / dispatch), retained max|A'|    uint64 SUM, uint32 MAX
+// The caller runs xg_shard_step(h, p) on every rank, then the collectives
+// xg_shard_exchange describes for point p (NCCL / torch.distributed on a
+// multi-GPU box, an in-process reduction in the single-GPU simulation), then
+// step p + 1.  Every reduction is exact (max, min, integer sums) except the
+// fp64 column sums, whose rounding the verified-mean test covers for any
+// summation order; results equal the single-GPU pipeline bit for bit.
+constexpr int kRemoteCap = 8;
+
+struct ShardState {
+    PipeCall q;  // q.a / q.c / q.out: this rank's rows; q.M: this rank's row count
+    int m_total = 0, g = 1, rank = 0, mpad = 0;
+    std::vector<int> rank_rows;
+    PipeWs w{};
+    void* base = nullptr;
+    uint32_t* x1 = nullptr;             // [4] maxA, maxRA, nonfinite, -
+    unsigned long long* x4n = nullptr;  // [1] nnz(A')
+    uint32_t* x4r = nullptr;            // [1] retained max|A'|
+    int* remote = nullptr;              // [kRemoteCap] column indices
+    int* n_remote = nullptr;
+    float* pack = nullptr;              // [kRemoteCap][mpad]
+    float* gath = nullptr;              // [g][kRemoteCap][mpad]
+    int* rank_rows_d = nullptr;
+    ~ShardState() {
+        if (base) cudaFree(base);
+    }
+};
+
+__global__ void k_shard_xfer(xg::DevScalars* sc, uint32_t* x1, unsigned long long* x4n, uint32_t* x4r,
+                             int* n_remote, int what) {
+    switch (what) {
+        case 0: x1[0] = sc->maxA; x1[1] = sc->maxRA; x1[2] = (uint32_t)sc->nonfinite; x1[3] = 0; break;
+        case 1: sc->maxA = x1[0]; sc->maxRA = x1[1]; sc->nonfinite = (int)x1[2]; break;
+        case 2: *x4n = sc->nnzA; *x4r = sc->retA; break;
+        case 3: sc->nnzA = *x4n; sc->retA = *x4r; break;
+        case 4: *n_remote = 0; break;
+    }
+}
+
+void shard_xfer(ShardState& h, int what, cudaStream_t s) {
+    k_shard_xfer<<<1, 1, 0, s>>>(h.w.sc, h.x1, h.x4n, h.x4r, h.n_remote, what);
+    check_launch("shard xfer");
+}
+
+Pipe shard_pipe(ShardState& h, cudaStream_t s) {
+    Pipe p;
+    p.M = h.q.M; p.K = h.q.K; p.N = h.q.N; p.cfg = &h.q.cfg; p.s = s;
+    p.ldk = pad16(h.q.K);
+    p.vw = h.q.cfg.scheme == XG_Q_VECTORWISE;
+    p.sc = h.w.sc;
+    p.aq = h.w.aq; p.raq = h.w.raq; p.ared = h.w.ared;
+    p.bqT = h.w.bqT; p.rbqT = h.w.rbqT; p.bredT = h.w.bredT;
+    p.la = h.w.la; p.lb = h.w.lb; p.colmax = h.w.colmax;
+    return p;
+}
+
+void shard_step(ShardState& h, int step, cudaStream_t s) {
+    Pipe p = shard_pipe(h, s);
+    const PipeCall& q = h.q;
+    const int M = q.M, K = q.K, N = q.N;
+    switch (step) {
+        case 0:
+            ck(cudaMemsetAsync(p.sc, 0, sizeof(xg::DevScalars), s), "memset");
+            shard_xfer(h, 4, s);
+            if (q.c) {
+                xg::finite_max(q.c, (int64_t)M * N, &p.sc->retB, &p.sc->nonfinite, s);
+                check_launch("finite C");
+                ck(cudaMemsetAsync(&p.sc->retB, 0, sizeof(uint32_t), s), "memset");
+            }
+            quantize_operands(p, q.a, q.b, 1);
+            shard_xfer(h, 0, s);
+            break;
+        case 1:
+            shard_xfer(h, 1, s);  // global max|A| (PerTensor), NaN flag
+            quantize_operands(p, q.a, q.b, 2);
+            shard_xfer(h, 0, s);
+            break;
+        case 2:
+            shard_xfer(h, 1, s);  // global max|A|, max|RA|
+            quantize_operands(p, q.a, q.b, 4);
+            gemm_df(p, q.out);
+            if (q.reduce)
+                xg::launch_stats_partial(q.out, M, N, q.cfg.policy, h.w.rstat, h.w.cstat, h.w.rsum, h.w.csum,
+                                         &p.sc->nflag, s);
+            check_launch("stats partial", 2);
+            break;
+        case 3:
+            if (q.reduce) {
+                xg::StatsDefer def{q.a, K, q.b, N, K, q.cfg.threshold, 0, h.remote, h.n_remote, kRemoteCap};
+                xg::launch_stats_final(q.out, M, N, h.m_total, q.cfg.policy, h.w.rstat, h.w.cstat, h.w.rsum,
+                                       h.w.csum, h.w.flags, &p.sc->nflag, s, &def);
+                check_launch("stats final", q.cfg.policy == XG_AVG_RULE ? 2 : 0);
+                xg::launch_pack_remote_cols(q.out, M, N, h.remote, h.n_remote, kRemoteCap, h.mpad, h.pack, s);
+                check_launch("pack columns");
+            }
+            break;
+        case 4:
+            if (q.reduce && q.cfg.policy == XG_AVG_RULE) {
+                xg::launch_remote_col_means(h.gath, h.g, h.rank_rows_d, h.mpad, kRemoteCap, h.remote, h.n_remote,
+                                            h.m_total, h.w.cstat, s);
+                check_launch("remote column means");
+            }
+            select_operands(p, q.a, q.b, q.reduce, h.w.rstat, h.w.cstat, 1);
+            shard_xfer(h, 2, s);
+            break;
+        case 5:
+            shard_xfer(h, 3, s);  // global nnz(A'), retained max
+            select_operands(p, q.a, q.b, q.reduce, h.w.rstat, h.w.cstat, 2);
+            xg::launch_dispatch(p.sc, q.cfg.bits, (int64_t)h.m_total * K, (int64_t)K * N, q.cfg.density_limit,
+                                q.reduce, s);
+            check_launch("dispatch");
+            gemm_comp(p, q.out, q.c, q.alpha, q.beta);
+            break;
+        default:
+            throw InvalidArg("xg_shard_step: step must be in [0, 5]");
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+struct xg_shard {
+    ShardState st;
+};
+
+xg_status xg_shard_create(const float* a_rows, const float* b, const float* c_rows, float alpha, float beta,
+                          int rank, int nranks, const int* rank_rows, int k, int n, const xg_config* cfg,
+                          int reduce, float* out_rows, xg_shard** h) {
+    return guarded([&] {
+        validate_cfg(cfg);
+        req(h != nullptr, "xg_shard_create: null handle");
+        req(nranks >= 1 && rank >= 0 && rank < nranks && rank_rows, "xg_shard_create: bad rank layout");
+        int64_t mt = 0;
+        int mmax = 0;
+        for (int r = 0; r < nranks; ++r) {
+            req(rank_rows[r] >= 1, "xigemm: matrix dimensions must be >= 1");
+            mt += rank_rows[r];
+            mmax = rank_rows[r] > mmax ? rank_rows[r] : mmax;
+        }
+        req(mt <= 0x7fffffff, "xg_shard_create: total rows exceed int");
+        req(k >= 1 && n >= 1, "xigemm: matrix dimensions must be >= 1");
+        req(a_rows && b && out_rows, "xigemm: null matrix");
+        req(k <= xg::gemm_max_inner(cfg->bits), "gemm_int: inner dimension permits 32-bit overflow");
+        auto x = std::make_unique<xg_shard>();
+        ShardState& S = x->st;
+        const int M = rank_rows[rank];
+        S.q = PipeCall{a_rows, b, c_rows, alpha, beta, M, k, n, *cfg, reduce, out_rows};
+        S.m_total = (int)mt;
+        S.g = nranks;
+        S.rank = rank;
+        S.rank_rows.assign(rank_rows, rank_rows + nranks);
+        S.mpad = (mmax + 63) / 64 * 64;
+        const int64_t ldk = pad16(k);
+        auto layout = [&](auto&& get) {
+            alloc_ws(S.w, M, n, ldk, get);
+            S.x1 = get((uint32_t*)nullptr, 4);
+            S.x4n = get((unsigned long long*)nullptr, 1);
+            S.x4r = get((uint32_t*)nullptr, 1);
+            S.remote = get((int*)nullptr, kRemoteCap);
+            S.n_remote = get((int*)nullptr, 1);
+            S.pack = get((float*)nullptr, (int64_t)kRemoteCap * S.mpad);
+            S.gath = get((float*)nullptr, (int64_t)nranks * kRemoteCap * S.mpad);
+            S.rank_rows_d = get((int*)nullptr, nranks);
+        };
+        int64_t total = 0;
+        layout([&](auto* tag, int64_t cnt) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            const int64_t off = total;
+            total += ((cnt > 0 ? cnt : 1) * (int64_t)sizeof(T) + 255) / 256 * 256;
+            return reinterpret_cast<T*>(off);
+        });
+        ck(cudaMalloc(&S.base, (size_t)total), "shard workspace");
+        int64_t off = 0;
+        layout([&](auto* tag, int64_t cnt) {
+            using T = std::remove_pointer_t<decltype(tag)>;
+            T* p = reinterpret_cast<T*>(static_cast<char*>(S.base) + off);
+            off += ((cnt > 0 ? cnt : 1) * (int64_t)sizeof(T) + 255) / 256 * 256;
+            return p;
+        });
+        ck(cudaMemcpy(S.rank_rows_d, rank_rows, sizeof(int) * nranks, cudaMemcpyHostToDevice), "rank rows");
+        ck(cudaMemset(S.gath, 0, sizeof(float) * (size_t)nranks * kRemoteCap * S.mpad), "memset");
+        *h = x.release();
+    });
+}
+
+xg_status xg_shard_step(xg_shard* h, int step, xg_stream s) {
+    return guarded([&] {
+        req(h != nullptr, "xg_shard_step: null handle");
+        shard_step(h->st, step, st(s));
+    });
+}
+
+// Collective `idx` (0, 1, ...) required after step `point`; *count = 0 when
+// there is none.  dtype: 0 uint32, 1 uint64, 2 float64, 3 float32.
+// op: 0 MAX, 1 SUM, 2 MIN, 3 ALLGATHER (send -> recv = nranks * count).
+xg_status xg_shard_exchange(xg_shard* h, int point, int idx, void** send, void** recv, int64_t* count,
+                            int* dtype, int* op) {
+    return guarded([&] {
+        req(h && send && recv && count && dtype && op, "xg_shard_exchange: null argument");
+        const ShardState& S = h->st;
+        const bool vw = S.q.cfg.scheme == XG_Q_VECTORWISE;
+        *send = *recv = nullptr;
+        *count = 0;
+        *dtype = 0;
+        *op = 0;
+        auto set = [&](void* p, void* r, int64_t c, int dt, int o) {
+            *send = p; *recv = r; *count = c; *dtype = dt; *op = o;
+        };
+        if (point == 0 && idx == 0 && !vw) set(S.x1, S.x1, 4, 0, 0);
+        else if (point == 1 && idx == 0) set(S.x1, S.x1, 4, 0, 0);
+        else if (point == 2 && idx == 0 && S.q.reduce) {
+            if (S.q.cfg.policy == XG_AVG_RULE) set(S.w.csum, S.w.csum, S.q.N, 2, 1);
+            else set(S.w.cstat, S.w.cstat, S.q.N, 0, 2);
+        } else if (point == 3 && idx == 0 && S.q.reduce && S.q.cfg.policy == XG_AVG_RULE) {
+            set(S.pack, S.gath, (int64_t)kRemoteCap * S.mpad, 3, 3);
+        } else if (point == 4 && idx == 0) set(S.x4n, S.x4n, 1, 1, 1);
+        else if (point == 4 && idx == 1) set(S.x4r, S.x4r, 1, 0, 0);
+    });
+}
+
+xg_status xg_shard_finish(xg_shard* h, xg_report* rep, xg_stream s) {
+    return guarded([&] {
+        req(h != nullptr, "xg_shard_finish: null handle");
+        ShardState& S = h->st;
+        xg::DevScalars d;
+        int nrem = 0;
+        ck(cudaMemcpyAsync(&d, S.w.sc, sizeof d, cudaMemcpyDeviceToHost, st(s)), "report");
+        ck(cudaMemcpyAsync(&nrem, S.n_remote, sizeof nrem, cudaMemcpyDeviceToHost, st(s)), "report");
+        ck(cudaStreamSynchronize(st(s)), "pipeline");
+        if (nrem > kRemoteCap) throw std::runtime_error("xg_shard: too many ambiguous column statistics");
+        req(!d.nonfinite, "xigemm: inputs must be finite");
+        if (rep) {
+            std::memset(rep, 0, sizeof *rep);
+            rep->density_a = d.densA;
+            rep->density_b = d.densB;
+            rep->path = d.path;
+            rep->nnz_a = S.q.reduce ? (int64_t)d.nnzA : 0;
+            rep->nnz_b = S.q.reduce ? (int64_t)d.nnzB : 0;
+            rep->stats_fallbacks = d.nflag;
+        }
+    });
+}
+
+void xg_shard_destroy(xg_shard* h) { delete h; }
 
 xg_status xg_xigemm(const float* a, const float* b, const float* c, float alpha, float beta,
                     int m, int k, int n, const xg_config* cfg, int reduce, float* out,

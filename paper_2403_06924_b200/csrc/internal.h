@@ -106,10 +106,25 @@ struct StatsDefer {
     int inner;
     double thr_m;
     int widen;
+    // row-sharded pipeline: column statistics that need the exact sequential
+    // sum are listed here (they span other ranks) instead of computed locally
+    int* remote_cols;
+    int* n_remote;
+    int remote_cap;
 };
 void launch_stats(const float* d, int rows, int cols, int policy, float* row_stat,
                   float* col_stat, double* row_sum, double* col_sum, int* flags, int* nflag,
                   cudaStream_t s, const StatsDefer* def = nullptr);
+// the two halves of launch_stats, split around the row-sharded column reduction
+void launch_stats_partial(const float* d, int rows, int cols, int policy, float* row_stat,
+                          float* col_stat, double* row_sum, double* col_sum, int* nflag, cudaStream_t s);
+void launch_stats_final(const float* d, int rows, int cols, int col_n, int policy, float* row_stat,
+                        float* col_stat, double* row_sum, double* col_sum, int* flags, int* nflag,
+                        cudaStream_t s, const StatsDefer* def);
+void launch_pack_remote_cols(const float* d, int rows, int cols, const int* list, const int* n, int cap,
+                             int mpad, float* buf, cudaStream_t s);
+void launch_remote_col_means(const float* gath, int g, const int* rank_rows, int mpad, int cap,
+                             const int* list, const int* n, int col_n, float* col_stat, cudaStream_t s);
 
 void fill_u32(uint32_t* p, uint32_t v, int64_t n, cudaStream_t s);
 

@@ -116,7 +116,8 @@ __device__ __forceinline__ bool verified_mean(double S, int nterms, double n, fl
 }
 
 __global__ void k_finalize_avg(const double* row_sum, const double* col_sum, int rows, int cols,
-                               float* row_stat, float* col_stat, int* flags, int* nflag, int widen) {
+                               int col_n, float* row_stat, float* col_stat, int* flags, int* nflag,
+                               int widen) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows + cols) return;
     float v;
@@ -125,7 +126,7 @@ __global__ void k_finalize_avg(const double* row_sum, const double* col_sum, int
         ok = verified_mean(row_sum[i], cols, (double)cols, v, widen);
         row_stat[i] = v;
     } else {
-        ok = verified_mean(col_sum[i - rows], rows, (double)rows, v, widen);
+        ok = verified_mean(col_sum[i - rows], col_n, (double)col_n, v, widen);
         col_stat[i - rows] = v;
     }
     if (!ok) flags[atomicAdd(nflag, 1)] = i;
@@ -144,7 +145,7 @@ __global__ void k_finalize_avg(const double* row_sum, const double* col_sum, int
 // paid (the mean stays `lo` otherwise: it is never observable).
 constexpr int kChunk = 2048;
 __global__ void __launch_bounds__(kThreads)
-    k_fallback_avg(const float* __restrict__ d, int rows, int cols, const int* flags,
+    k_fallback_avg(const float* __restrict__ d, int rows, int cols, int col_n, const int* flags,
                    const int* nflag, float* row_stat, float* col_stat, const double* row_sum,
                    const double* col_sum, const StatsDefer def) {
     __shared__ float buf[kChunk];
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int f = blockIdx.x; f < nf; f += gridDim.x) {
         const int idx = flags[f];
         const bool is_row = idx < rows;
-        const int len = is_row ? cols : rows;
+        const int len = is_row ? cols : col_n;
         if (def.a) {
             const double S = is_row ? row_sum[idx] : col_sum[idx - rows];
             float lo, hi;
@@ -166,6 +167,13 @@ __global__ void __launch_bounds__(kThreads)
                 amb |= (fabsf(x) >= tlo && fabsf(x) < thi) ? 1 : 0;
             }
             if (!__syncthreads_or(amb)) continue;  // uniform: membership identical under lo and hi
+            if (!is_row && def.remote_cols) {      // row-sharded: the column spans other ranks
+                if (threadIdx.x == 0) {
+                    const int slot = atomicAdd(def.n_remote, 1);
+                    if (slot < def.remote_cap) def.remote_cols[slot] = idx - rows;
+                }
+                continue;
+            }
         }
         double s = 0.0;
         for (int base = 0; base < len; base += kChunk) {
@@ -199,19 +207,13 @@ __global__ void k_zero(double* a, int na, double* b, int nb, int* n) {
 
 }  // namespace
 
-void launch_stats(const float* d, int rows, int cols, int policy, float* row_stat, float* col_stat,
-                  double* row_sum, double* col_sum, int* flags, int* nflag, cudaStream_t s,
-                  const StatsDefer* def) {
+void launch_stats_partial(const float* d, int rows, int cols, int policy, float* row_stat,
+                          float* col_stat, double* row_sum, double* col_sum, int* nflag, cudaStream_t s) {
     dim3 grid((cols + kThreads * 4 - 1) / (kThreads * 4), (rows + kSlabRows - 1) / kSlabRows);
     if (policy == kAvg) {
         const int nz = rows > cols ? rows : cols;
         k_zero<<<(nz + 255) / 256, 256, 0, s>>>(row_sum, rows, col_sum, cols, nflag);
         k_stats_slab<kAvg><<<grid, kThreads, 0, s>>>(d, rows, cols, row_sum, col_sum, nullptr, nullptr);
-        k_finalize_avg<<<(rows + cols + 255) / 256, 256, 0, s>>>(row_sum, col_sum, rows, cols,
-                                                                 row_stat, col_stat, flags, nflag,
-                                                                 def ? def->widen : 0);
-        k_fallback_avg<<<64, kThreads, 0, s>>>(d, rows, cols, flags, nflag, row_stat, col_stat, row_sum,
-                                               col_sum, def ? *def : StatsDefer{});
     } else {
         // the float bit patterns of |x| order like uints; FLT_MAX initial value (pipeline.cpp:237-238)
         fill_u32(reinterpret_cast<uint32_t*>(row_stat), 0x7f7fffffu, rows, s);
@@ -220,6 +222,75 @@ void launch_stats(const float* d, int rows, int cols, int policy, float* row_sta
                                                       reinterpret_cast<uint32_t*>(row_stat),
                                                       reinterpret_cast<uint32_t*>(col_stat));
     }
+}
+
+void launch_stats_final(const float* d, int rows, int cols, int col_n, int policy, float* row_stat,
+                        float* col_stat, double* row_sum, double* col_sum, int* flags, int* nflag,
+                        cudaStream_t s, const StatsDefer* def) {
+    if (policy != kAvg) return;  // MinRule statistics are final after the partial pass (and min-reduce)
+    k_finalize_avg<<<(rows + cols + 255) / 256, 256, 0, s>>>(row_sum, col_sum, rows, cols, col_n, row_stat,
+                                                             col_stat, flags, nflag, def ? def->widen : 0);
+    k_fallback_avg<<<64, kThreads, 0, s>>>(d, rows, cols, col_n, flags, nflag, row_stat, col_stat, row_sum,
+                                           col_sum, def ? *def : StatsDefer{});
+}
+
+void launch_stats(const float* d, int rows, int cols, int policy, float* row_stat, float* col_stat,
+                  double* row_sum, double* col_sum, int* flags, int* nflag, cudaStream_t s,
+                  const StatsDefer* def) {
+    launch_stats_partial(d, rows, cols, policy, row_stat, col_stat, row_sum, col_sum, nflag, s);
+    launch_stats_final(d, rows, cols, rows, policy, row_stat, col_stat, row_sum, col_sum, flags, nflag, s, def);
+}
+
+// Row-sharded rare path: exact sequential column sums (pipeline.cpp:219-229,
+// i outer in global row order) of the listed columns from the gathered
+// per-rank slices gath[rank][slot][row] (rank r holds rank_rows[r] rows).
+__global__ void k_remote_col_means(const float* gath, int g, const int* rank_rows, int mpad, int cap,
+                                   const int* cols_list, const int* n_list, int col_n, float* col_stat) {
+    const int n = min(*n_list, cap);
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < g; ++r) {
+            const float* src = gath + ((int64_t)r * cap + f) * mpad;
+            for (int i = 0; i < rank_rows[r]; ++i) s = __dadd_rn(s, fabs((double)src[i]));
+        }
+        col_stat[cols_list[f]] = __double2float_rn(__ddiv_rn(s, (double)col_n));
+    }
+}
+
+// Packs D_F[:, j] of the listed columns into buf[slot][row] (rows padded to mpad).
+__global__ void k_pack_cols(const float* d, int rows, int cols, const int* cols_list, const int* n_list,
+                            int cap, int mpad, float* buf) {
+    const int n = min(*n_list, cap);
+    for (int f = blockIdx.y; f < n; f += gridDim.y)
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mpad; i += gridDim.x * blockDim.x)
+            buf[(int64_t)f * mpad + i] = i < rows ? d[(int64_t)i * cols + cols_list[f]] : 0.0f;
+}
+
+// Every rank finds the same set of columns, but atomics fill the list in any
+// order: sort it so the gathered slices line up across ranks.
+__global__ void k_sort_list(int* list, const int* n_list, int cap) {
+    const int n = min(*n_list, cap);
+    for (int i = 1; i < n; ++i) {
+        const int v = list[i];
+        int j = i - 1;
+        while (j >= 0 && list[j] > v) {
+            list[j + 1] = list[j];
+            --j;
+        }
+        list[j + 1] = v;
+    }
+}
+
+void launch_pack_remote_cols(const float* d, int rows, int cols, const int* list, const int* n, int cap,
+                             int mpad, float* buf, cudaStream_t s) {
+    k_sort_list<<<1, 1, 0, s>>>(const_cast<int*>(list), n, cap);
+    dim3 grid((mpad + 255) / 256 < 64 ? (mpad + 255) / 256 : 64, cap);
+    k_pack_cols<<<grid, 256, 0, s>>>(d, rows, cols, list, n, cap, mpad, buf);
+}
+
+void launch_remote_col_means(const float* gath, int g, const int* rank_rows, int mpad, int cap,
+                             const int* list, const int* n, int col_n, float* col_stat, cudaStream_t s) {
+    k_remote_col_means<<<1, 32, 0, s>>>(gath, g, rank_rows, mpad, cap, list, n, col_n, col_stat);
 }
 
 }  // namespace xg

@@ -1,0 +1,232 @@
+"""Row-sharded xigemm across ranks.
+
+A and C are split by rows, B is replicated: ``broadcast_b`` ships it from one
+rank with a single collective (NCCL over NVLink on a multi-GPU box).  Every
+rank runs the staged C-ABI pipeline (``xg_shard_*`` in include/xigemm_c.h) on
+its rows; between the stages the ranks perform the exact couplings the
+reference's algorithm has (pipeline.cpp:50-111):
+
+    point 0  max|A|                     (PerTensor scale)            MAX
+    point 1  max|A|, max|RA|, NaN flag  (lambda_RA, MinRule scale)   MAX
+    point 2  column statistics of D_F   (AvgRule sums / MinRule min) SUM / MIN
+    point 3  D_F columns of the rare AvgRule means that need the exact
+             sequential sum across ranks                            ALLGATHER
+    point 4  nnz(A'), retained max|A'|  (density, dispatch, scale)   SUM, MAX
+
+All reductions are exact (max/min/integer sums) except the fp64 column sums,
+whose rounding the verified-mean test covers for any order, so every rank's
+rows equal the single-GPU result bit for bit.
+
+Two communicators drive the same code:
+  * ``DistComm``  - torch.distributed, one shard per process (``nccl`` on GPUs;
+    ``gloo`` works for the host-side protocol tests);
+  * ``LocalComm`` - all shards in one process on one GPU (the single-GPU
+    simulation the parity tests use: g shards must reproduce xigemm exactly).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import XgReport, check, lib
+from .api import GemmPath, GemmReport, InvalidArgument, XigemmConfig, _dev, _p, _s
+
+NSTEPS = 6
+OP_MAX, OP_SUM, OP_MIN, OP_ALLGATHER = 0, 1, 2, 3
+# uint32 payloads (non-negative float bit patterns, flags) travel as int32: all
+# values are < 2^31, so signed max/min order them like the unsigned values.
+_TYPESTR = {0: "<i4", 1: "<i8", 2: "<f8", 3: "<f4"}
+
+
+class _DevView:
+    """Zero-copy torch view of a device buffer owned by the C library."""
+
+    def __init__(self, ptr: int, count: int, dtype: int):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": _TYPESTR[dtype],
+                                         "data": (int(ptr), False), "version": 2}
+
+
+def _view(ptr: int, count: int, dtype: int) -> torch.Tensor:
+    return torch.as_tensor(_DevView(ptr, count, dtype), device="cuda")
+
+
+class Exchange:
+    def __init__(self, send: torch.Tensor, recv: torch.Tensor, op: int):
+        self.send, self.recv, self.op = send, recv, op
+
+
+class Shard:
+    """One rank's rows of a row-sharded xigemm (owns the C handle)."""
+
+    def __init__(self, a_rows, b, c_rows, alpha, beta, rank, rank_rows, cfg: XigemmConfig, reduce=True,
+                 out=None):
+        self.a, _ = _dev(a_rows, torch.float32)
+        self.b, _ = _dev(b, torch.float32)
+        self.c = None if c_rows is None else _dev(c_rows, torch.float32)[0]
+        m, k = self.a.shape
+        if self.b.shape[0] != k:
+            raise InvalidArgument("xigemm: inner dimensions do not match")
+        if rank_rows[rank] != m:
+            raise InvalidArgument("xg_shard: row count of this rank does not match rank_rows")
+        n = self.b.shape[1]
+        if self.c is not None and tuple(self.c.shape) != (m, n):
+            raise InvalidArgument("xigemm: C shape does not match the result")
+        self.out = out if out is not None else torch.empty((m, n), dtype=torch.float32, device="cuda")
+        self.nranks = len(rank_rows)
+        rr = (C.c_int * len(rank_rows))(*[int(r) for r in rank_rows])
+        self._cfg = cfg.c()
+        self.h = C.c_void_p()
+        check(lib().xg_shard_create(_p(self.a), _p(self.b), _p(self.c), float(alpha), float(beta), int(rank),
+                                    len(rank_rows), rr, k, n, C.byref(self._cfg), int(reduce), _p(self.out),
+                                    C.byref(self.h)))
+
+    def step(self, p: int) -> None:
+        check(lib().xg_shard_step(self.h, p, _s()))
+
+    def exchanges(self, p: int) -> list[Exchange]:
+        res, i = [], 0
+        while True:
+            send, recv = C.c_void_p(), C.c_void_p()
+            cnt, dt, op = C.c_int64(), C.c_int(), C.c_int()
+            check(lib().xg_shard_exchange(self.h, p, i, C.byref(send), C.byref(recv), C.byref(cnt),
+                                          C.byref(dt), C.byref(op)))
+            if cnt.value == 0:
+                return res
+            sv = _view(send.value, cnt.value, dt.value)
+            rv = _view(recv.value, cnt.value * self.nranks, dt.value) if op.value == OP_ALLGATHER else sv
+            res.append(Exchange(sv, rv, op.value))
+            i += 1
+
+    def finish(self) -> XgReport:
+        rep = XgReport()
+        try:
+            check(lib().xg_shard_finish(self.h, C.byref(rep), _s()))
+        finally:
+            self.close()
+        return rep
+
+    def close(self):
+        if self.h:
+            lib().xg_shard_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class LocalComm:
+    """All shards in this process (one GPU): collectives are local reductions."""
+
+    def allreduce(self, ts: list[torch.Tensor], op: int) -> None:
+        st = torch.stack(ts)
+        r = st.amax(0) if op == OP_MAX else st.amin(0) if op == OP_MIN else st.sum(0)
+        for t in ts:
+            t.copy_(r)
+
+    def allgather(self, sends: list[torch.Tensor], recvs: list[torch.Tensor]) -> None:
+        cat = torch.cat(sends)
+        for r in recvs:
+            r.copy_(cat)
+
+
+class DistComm:
+    """torch.distributed, one shard per process (nccl on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+
+    def allreduce(self, ts: list[torch.Tensor], op: int) -> None:
+        d = self.dist
+        o = {OP_MAX: d.ReduceOp.MAX, OP_MIN: d.ReduceOp.MIN, OP_SUM: d.ReduceOp.SUM}[op]
+        d.all_reduce(ts[0], op=o, group=self.group)
+
+    def allgather(self, sends: list[torch.Tensor], recvs: list[torch.Tensor]) -> None:
+        self.dist.all_gather_into_tensor(recvs[0], sends[0], group=self.group)
+
+
+def run_protocol(shards: list, comm, nranks: int) -> None:
+    """Steps 0..5 with the point-p collectives after step p, in lockstep over
+    the shards this process holds (one per process with DistComm).  Works for
+    any object with step(p) / exchanges(p) (the CPU protocol tests use mocks)."""
+    for p in range(NSTEPS):
+        for sh in shards:
+            sh.step(p)
+        per = [sh.exchanges(p) for sh in shards]
+        for i in range(len(per[0])):
+            ex = [x[i] for x in per]
+            if ex[0].op == OP_ALLGATHER:
+                comm.allgather([e.send for e in ex], [e.recv for e in ex])
+            else:
+                comm.allreduce([e.send for e in ex], ex[0].op)
+
+
+def _report(rep: XgReport, result) -> GemmReport:
+    return GemmReport(result, rep.density_a, rep.density_b, GemmPath(rep.path), {}, rep.nnz_a, rep.nnz_b,
+                      rep.stats_fallbacks)
+
+
+def split_rows(m: int, nranks: int) -> list[int]:
+    """Balanced contiguous row blocks (the first m % nranks ranks get one more)."""
+    if m < nranks:
+        raise InvalidArgument("xg_shard: fewer rows than ranks")
+    q, r = divmod(m, nranks)
+    return [q + (1 if i < r else 0) for i in range(nranks)]
+
+
+def xigemm_sharded_local(a, b, c=None, alpha: float = 1.0, beta: float = 0.0,
+                         cfg: XigemmConfig | None = None, nranks: int = 2, reduce: bool = True) -> GemmReport:
+    """Single-process simulation of the nranks-way row-sharded pipeline on the
+    current GPU (LocalComm).  Must equal xigemm(a, b, c, ...) bit for bit."""
+    cfg = cfg or XigemmConfig()
+    x, _ = _dev(a, torch.float32)
+    y, _ = _dev(b, torch.float32)
+    cc = None if c is None else _dev(c, torch.float32)[0]
+    rows = split_rows(x.shape[0], nranks)
+    out = torch.empty((x.shape[0], y.shape[1]), dtype=torch.float32, device="cuda")
+    shards, r0 = [], 0
+    for r, m in enumerate(rows):
+        shards.append(Shard(x[r0:r0 + m], y, None if cc is None else cc[r0:r0 + m], alpha, beta, r, rows, cfg,
+                            reduce, out[r0:r0 + m]))
+        r0 += m
+    try:
+        run_protocol(shards, LocalComm(), nranks)
+        reps = [sh.finish() for sh in shards]
+    finally:
+        for sh in shards:
+            sh.close()
+    return _report(reps[0], out)
+
+
+def broadcast_b(b: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
+    """Replicates B from rank `src` with one collective (ncclBroadcast)."""
+    import torch.distributed as dist
+    dist.broadcast(b, src=src, group=group)
+    return b
+
+
+def xigemm_sharded(a_rows, b, c_rows=None, alpha: float = 1.0, beta: float = 0.0,
+                   cfg: XigemmConfig | None = None, *, group=None, reduce: bool = True, out=None) -> GemmReport:
+    """This rank's rows of the row-sharded xigemm (torch.distributed must be
+    initialised; B must already be identical on every rank, see broadcast_b).
+    Returns the global report with this rank's result rows."""
+    import torch.distributed as dist
+    cfg = cfg or XigemmConfig()
+    x, _ = _dev(a_rows, torch.float32)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mine = torch.tensor([x.shape[0]], dtype=torch.int64, device="cuda")
+    allm = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(allm, mine, group=group)
+    rows = [int(t.item()) for t in allm]
+    sh = Shard(x, b, c_rows, alpha, beta, rank, rows, cfg, reduce, out)
+    try:
+        run_protocol([sh], DistComm(group), world)
+        rep = sh.finish()
+    finally:
+        sh.close()
+    return _report(rep, sh.out)

@@ -1,4 +1,8 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum CSV launch list."""
+"""Summarise an ncu --metrics gpu__time_duration.sum CSV launch list.
+
+Steps are counted as the launch count of the once-per-step dispatch kernel
+(k_dispatch), so kernels launched twice per step (the two compensation GEMMs)
+contribute both launches to the per-step total."""
 import collections
 import csv
 import sys
@@ -9,11 +13,13 @@ data = [dict(zip(hdr, r)) for r in rows[rows.index(hdr) + 1:] if len(r) == len(h
 agg = collections.OrderedDict()
 for d in data:
     agg.setdefault(d["Kernel Name"].split("(")[0][-48:], []).append(float(d["Metric Value"]))
+steps = next((len(v) for n, v in agg.items() if "k_dispatch" in n), None) or min(len(v) for v in agg.values())
 tot = 0.0
 for n, v in agg.items():
     if "generate" in n:
         continue
     per = sum(v) / len(v)
-    tot += per
-    print(f"{len(v):4d} x {per / 1e3:9.1f} us  {n}")
-print(f"sum of per-step kernel means: {tot / 1e3:.1f} us")
+    step = sum(v) / steps
+    tot += step
+    print(f"{len(v):4d} x {per / 1e3:9.1f} us  ({step / 1e3:7.1f} us/step)  {n}")
+print(f"steps: {steps}; sum of kernel time per step: {tot / 1e3:.1f} us")
