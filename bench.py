@@ -12,9 +12,10 @@ density (s = 0.3 so the sparse path is taken).  Inputs (256 MiB each) exceed the
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Multi-GPU (torchrun): each rank runs the full C3 problem on its own GPU
-("replicas", weak scaling) — see DESIGN.md §Multi-GPU; the row-sharded
-pipeline is not benchmarked yet.
+Multi-GPU (torchrun, --gpus N > 1): the row-sharded pipeline (weak scaling:
+M rows of A and C per GPU, B broadcast from rank 0 by NCCL every step, exact
+all-reduce couplings between the stages; paper_2403_06924_b200/sharded.py).
+--replicas runs N independent full problems instead.
 """
 from __future__ import annotations
 
@@ -37,9 +38,12 @@ def _dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or "MASTER_ADDR" in os.environ:
+        import torch
         import torch.distributed as dist
         backend = "nccl" if os.environ.get("XG_BENCH_BACKEND", "nccl") == "nccl" else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
         dist.init_process_group(backend)
     return world, rank, local
 
@@ -346,6 +350,109 @@ def run_b200(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def run_b200_sharded(args, world, rank, local):
+    """--gpus N > 1: the row-sharded pipeline.  Weak
+    scaling: every rank owns an M-row block of a tall A (M*N_gpus x K) and of C;
+    B (K x N) lives on rank 0 and is replicated by one NCCL broadcast inside
+    every timed step; the exact couplings (max|A|, max|RA|, column statistics,
+    nnz(A')) are NCCL all-reduces between the pipeline stages."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2403_06924_b200 as xg
+    from paper_2403_06924_b200 import sharded
+
+    torch.cuda.set_device(local)
+    m, n, k = args.m, args.n, args.k
+    a = xg.generate("student_t3", m, k, 1 + 7919 * rank, 0.0, 1.0)
+    b = xg.generate("student_t3", k, n, 2, 0.0, 1.0) if rank == 0 else \
+        torch.empty((k, n), dtype=torch.float32, device="cuda")
+    sharded.broadcast_b(b)
+    scheme, policy = xg.QuantScheme.VectorWise, xg.ReductionPolicy.AvgRule
+    t = torch.tensor([args.threshold or 0.0], dtype=torch.float64, device="cuda")
+    if args.threshold is None and rank == 0:
+        t[0] = find_threshold(xg, a, b, scheme, policy)[0]
+    dist.broadcast(t, src=0)
+    thr = float(t.item())
+    cfg = xg.XigemmConfig(threshold=thr, scheme=scheme, policy=policy)
+    out = torch.empty((m, n), dtype=torch.float32, device="cuda")
+
+    def step():
+        sharded.broadcast_b(b)
+        return sharded.xigemm_sharded(a, b, cfg=cfg, out=out, rank_rows=[m] * world)
+
+    rep = step()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    L = xg.lib()
+    L.xg_launch_count(1)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = int(L.xg_launch_count(1))
+    tt = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    ops = 2.0 * m * world * n * k
+    value = ops / (ms * 1e-3) / 1e12
+
+    # e2e: host A rows on every rank, host B on rank 0, C rows back to the host
+    ah = torch.empty((m, k), dtype=torch.float32, pin_memory=True)
+    ah.copy_(a)
+    bh = torch.empty((k, n), dtype=torch.float32, pin_memory=True)
+    if rank == 0:
+        bh.copy_(b)
+    oh = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
+    ad = torch.empty_like(a)
+    bd = torch.empty_like(b)
+
+    def e2e_step():
+        ad.copy_(ah, non_blocking=True)
+        if rank == 0:
+            bd.copy_(bh, non_blocking=True)
+        sharded.broadcast_b(bd)
+        sharded.xigemm_sharded(ad, bd, cfg=cfg, out=out, rank_rows=[m] * world)
+        oh.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+
+    e2e_step()
+    dist.barrier()
+    n_e2e = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(n_e2e):
+        e2e_step()
+    te = torch.tensor([(time.perf_counter() - t0) / n_e2e], device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = ops / float(te.item()) / 1e12
+    if rank != 0:
+        return
+    line = {
+        "metric": "effective TFLOP/s (2MNK/t) of compensated GEMM",
+        "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int8 (fp64/fp32 exact epilogues)",
+        "data": "synthetic Student-t(3) (device SplitMix64 generator), A rows seeded per rank, B seed 2",
+        "config": dict(_config(args, thr, (rep.density_a, rep.density_b)),
+                       workload=f"row-sharded xigemm: A {m * world}x{k} ({m} rows per GPU), B {k}x{n} "
+                                f"broadcast from rank 0 every step, Student-t(3), INT8 vector-wise AvgRule",
+                       parallelism=f"rows{world} (B replicated by NCCL broadcast; exact all-reduce couplings)"),
+        "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": 4 * (m * k * world + k * n),
+                "d2h_bytes_per_step": 4 * m * n * world},
+        "roofline": None,
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -359,14 +466,20 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=16)
     ap.add_argument("--ref-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent full problems per GPU instead of the row-sharded pipeline")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-sharded pipeline even at N=1 (needs torchrun / a process group)")
     args = ap.parse_args()
     world, rank, local = _dist_init()
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif (world > 1 and not args.replicas) or args.sharded:
+        run_b200_sharded(args, world, rank, local)
     else:
         run_b200(args, world, rank, local)
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
         dist.destroy_process_group()
 
 

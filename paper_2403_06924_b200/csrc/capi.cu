@@ -253,6 +253,7 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
     qb.x = b; qb.rows = p.K; qb.cols = p.N; qb.ld = p.N;
     qb.bits = bits; qb.rounding = rnd;
     qb.qT = p.bqT; qb.ldq = p.ldk; qb.rmax = &p.sc->maxRB;
+    qb.nonfinite = &p.sc->nonfinite;
     qb.co_share = co ? 1 : 0;
     if (p.vw) {
         ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, sb), "memset");
@@ -300,6 +301,7 @@ void select_operands(Pipe& p, const float* a, const float* b, int reduce, const 
     sa.other_max = &p.sc->maxB;
     sa.rq = p.raq; sa.red = p.ared; sa.ldq = p.ldk;
     sa.nnz = &p.sc->nnzA; sa.retmax = &p.sc->retA;
+    sa.nonfinite = &p.sc->nonfinite;
     SelectArgs sb = sa;
     sb.x = b; sb.rows = p.K; sb.cols = p.N; sb.ld = p.N;
     sb.lam = p.lb; sb.tensor_max = &p.sc->maxB; sb.rmax = &p.sc->maxRB;
@@ -1320,7 +1322,11 @@ void shard_step(ShardState& h, int step, cudaStream_t s) {
             break;
         case 3:
             if (q.reduce) {
-                xg::StatsDefer def{q.a, K, q.b, N, K, q.cfg.threshold, 0, h.remote, h.n_remote, kRemoteCap};
+                static const int widen = [] {
+                    const char* e = getenv("XG_STATS_WIDEN");  // test hook (see enqueue_stage)
+                    return e ? atoi(e) : 0;
+                }();
+                xg::StatsDefer def{q.a, K, q.b, N, K, q.cfg.threshold, widen, h.remote, h.n_remote, kRemoteCap};
                 xg::launch_stats_final(q.out, M, N, h.m_total, q.cfg.policy, h.w.rstat, h.w.cstat, h.w.rsum,
                                        h.w.csum, h.w.flags, &p.sc->nflag, s, &def);
                 check_launch("stats final", q.cfg.policy == XG_AVG_RULE ? 2 : 0);

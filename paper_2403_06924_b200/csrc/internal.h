@@ -54,6 +54,7 @@ struct QuantColsArgs {
     int64_t ldq;
     uint32_t* rmax;
     int co_share;            // host-only: CTAs per SM when co-scheduled with the A side (0: all)
+    const int* nonfinite;    // see SelectArgs::nonfinite (set by the column absmax pass)
 };
 
 // K3: residual quantisation + threshold selection of the original operand.
@@ -79,6 +80,10 @@ struct SelectArgs {
     // fix-up mode: rewrite `red` with the retained-max scale when it differs
     int fix_mode;
     int co_share;            // host-only: CTAs per SM when co-scheduled (0: all)
+    // set by the K1 kernels when an input is not finite: the call will fail
+    // (pipeline.cpp:50-52), so the table-driven kernels exit instead of
+    // indexing their dequant tables with NaN bit patterns
+    const int* nonfinite;
 };
 
 void launch_absmax_global(const float* x, int64_t n, uint32_t* gmax, int* nonfinite,

@@ -32,6 +32,11 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// Early exit of the table-driven kernels once a non-finite input was seen
+// (block-uniform: every thread reads the same flag).
+#define XG_EXIT_IF_NONFINITE(flagp) \
+    if ((flagp) && *(volatile const int*)(flagp)) return
+
 template <int NT = kThreads>
 __device__ __forceinline__ float block_max(float v, float* red) {
     v = warp_maxf(v);
@@ -358,6 +363,7 @@ __device__ __forceinline__ void build_col_luts(float (*lut)[kTN], const double* 
 
 template <int RND>
 __global__ void __launch_bounds__(kThreads) k_quant_cols_T(const QuantColsArgs a) {
+    XG_EXIT_IF_NONFINITE(a.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
     __shared__ uint32_t tq[kTN][kTW];
@@ -459,6 +465,7 @@ __device__ __forceinline__ void select_quad(const float (&x)[4], const float* lu
 
 template <int RND>
 __global__ void __launch_bounds__(kThreads) k_select_rows(const SelectArgs a) {
+    XG_EXIT_IF_NONFINITE(a.nonfinite);
     __shared__ float lut[256];
     __shared__ float red[kThreads / 32];
     __shared__ unsigned long long redu[kThreads / 32];
@@ -523,6 +530,7 @@ __global__ void __launch_bounds__(kThreads) k_select_rows(const SelectArgs a) {
 // scale (sparse.cpp:198-203): rewrite the kept ints with lambda'.  Exits at
 // once in the usual case lambda' == lambda.  Exact scalar path (rare).
 __global__ void __launch_bounds__(kThreads) k_fix_rows(const SelectArgs a) {
+    XG_EXIT_IF_NONFINITE(a.nonfinite);
     const double lam_t = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
     const double lam_fix = compute_scale((double)__uint_as_float(*a.retmax), a.bits);
     if (lam_fix == lam_t) return;
@@ -540,6 +548,7 @@ __global__ void __launch_bounds__(kThreads) k_fix_rows(const SelectArgs a) {
 
 // B side: column j of the reduced operand is row j of B'q^T.
 __global__ void __launch_bounds__(kThreads) k_fix_cols_T(const SelectArgs a) {
+    XG_EXIT_IF_NONFINITE(a.nonfinite);
     const double lam_t = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
     const double lam_fix = compute_scale((double)__uint_as_float(*a.retmax), a.bits);
     if (lam_fix == lam_t) return;
@@ -559,6 +568,7 @@ __global__ void __launch_bounds__(kThreads) k_fix_cols_T(const SelectArgs a) {
 // B side: RBq^T and B'q^T (both N x K, K-major), column thresholds t_j.
 template <int RND>
 __global__ void __launch_bounds__(kThreads) k_select_cols_T(const SelectArgs a) {
+    XG_EXIT_IF_NONFINITE(a.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
     __shared__ uint32_t trq[kTN][kTW];
@@ -645,10 +655,17 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
     return v;
 }
+// NaN-propagating max (PTX max.NaN): a NaN input makes dmax NaN, which sends
+// the quad to the exact path (quantize.cpp:13-24 maps NaN to -qmax).
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
 __device__ __forceinline__ uint32_t qn(float x, float lam32, float& dmax) {
     const float t = __fmul_rn(x, lam32);
     const float u = __fadd_rn(t, kMagic);
-    dmax = fmaxf(dmax, fabsf(__fsub_rn(t, __fsub_rn(u, kMagic))));
+    dmax = fmax_nan(dmax, fabsf(__fsub_rn(t, __fsub_rn(u, kMagic))));
     return __float_as_uint(u);
 }
 __device__ __forceinline__ uint32_t ubits(int q) { return (uint32_t)(q + 0x4B400000); }
@@ -761,6 +778,7 @@ __device__ __forceinline__ void select_quad_n(const float (&x)[4], uint32_t lut_
 }
 
 __global__ void __launch_bounds__(kThreads) k_select_rows_fast(const SelectArgs a) {
+    XG_EXIT_IF_NONFINITE(a.nonfinite);
     __shared__ float lut[256];
     __shared__ float red[kThreads / 32];
     __shared__ unsigned long long redu[kThreads / 32];
@@ -812,6 +830,7 @@ __global__ void __launch_bounds__(kThreads) k_select_rows_fast(const SelectArgs 
 }
 
 __global__ void __launch_bounds__(kThreads) k_quant_cols_T_fast(const QuantColsArgs a) {
+    XG_EXIT_IF_NONFINITE(a.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
     __shared__ uint32_t tq[kTN][kTW];
@@ -876,6 +895,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_cols_T_fast(const QuantColsA
 }
 
 __global__ void __launch_bounds__(kThreads) k_select_cols_T_fast(const SelectArgs a) {
+    XG_EXIT_IF_NONFINITE(a.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
     __shared__ uint32_t trq[kTN][kTW];
@@ -1054,6 +1074,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows_async(const QuantRowsAr
 // K3, A side (Nearest): RAq and A'q from a streamed row ring; the per-row
 // dequant table for row i+1 is built while row i is processed.
 __global__ void __launch_bounds__(kThreads) k_select_rows_async(const SelectArgs a) {
+    XG_EXIT_IF_NONFINITE(a.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float* ring = reinterpret_cast<float*>(dyn_smem);
     __shared__ uint64_t full[kRowSlots];
@@ -1167,6 +1188,7 @@ __device__ __forceinline__ void store_T32(const uint32_t (*t)[kCW], int8_t* dst,
 template <bool SELECT>
 __global__ void __launch_bounds__(kThreads)
     k_cols_T_async(const __grid_constant__ CUtensorMap tmap, const QuantColsArgs qa, const SelectArgs sa) {
+    XG_EXIT_IF_NONFINITE(SELECT ? sa.nonfinite : qa.nonfinite);
     extern __shared__ float4 dyn_smem[];
     // TMA destinations need 128-byte alignment
     float* ring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
@@ -1319,6 +1341,7 @@ __device__ __forceinline__ void build_row_lut(float* lut, double lam, int qmax) 
 
 template <int U>
 __global__ void __launch_bounds__(kRT, kRCtasPerSM) k_select_rows_r4(const SelectArgs a) {
+    XG_EXIT_IF_NONFINITE(a.nonfinite);
     __shared__ float lut[2][256];
     __shared__ float redf[kRT / 32];
     __shared__ unsigned long long redu[kRT / 32];
@@ -1484,6 +1507,7 @@ constexpr int kColWSmem = kWW * kWSlots * kWC * kWR * 4 + 256 * kWC * 4 + 1024;
 template <bool SELECT>
 __global__ void __launch_bounds__(kWW * 32, kWCtas)
     k_cols_w4(const __grid_constant__ CUtensorMap tmap, const QuantColsArgs qa, const SelectArgs sa) {
+    XG_EXIT_IF_NONFINITE(SELECT ? sa.nonfinite : qa.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float* ring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
     float(*lut)[kWC] = reinterpret_cast<float(*)[kWC]>(ring + kWW * kWSlots * kWC * kWR);

@@ -74,6 +74,7 @@ class Shard:
             raise InvalidArgument("xigemm: C shape does not match the result")
         self.out = out if out is not None else torch.empty((m, n), dtype=torch.float32, device="cuda")
         self.nranks = len(rank_rows)
+        self._ex = {}
         rr = (C.c_int * len(rank_rows))(*[int(r) for r in rank_rows])
         self._cfg = cfg.c()
         self.h = C.c_void_p()
@@ -85,6 +86,12 @@ class Shard:
         check(lib().xg_shard_step(self.h, p, _s()))
 
     def exchanges(self, p: int) -> list[Exchange]:
+        """Collectives after step p (buffers are fixed for the handle's life: cached)."""
+        if p not in self._ex:
+            self._ex[p] = self._query(p)
+        return self._ex[p]
+
+    def _query(self, p: int) -> list[Exchange]:
         res, i = [], 0
         while True:
             send, recv = C.c_void_p(), C.c_void_p()
@@ -99,11 +106,10 @@ class Shard:
             i += 1
 
     def finish(self) -> XgReport:
+        """Synchronises and returns the global report; the handle (and its
+        workspace) stays valid for the next run of the same problem."""
         rep = XgReport()
-        try:
-            check(lib().xg_shard_finish(self.h, C.byref(rep), _s()))
-        finally:
-            self.close()
+        check(lib().xg_shard_finish(self.h, C.byref(rep), _s()))
         return rep
 
     def close(self):
@@ -209,24 +215,47 @@ def broadcast_b(b: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
     return b
 
 
+_SHARD_CACHE: dict = {}
+_SHARD_CACHE_MAX = 2
+
+
+def _cached_shard(key, make):
+    """Reuses the handle (persistent workspace, no per-call allocation) of a
+    repeated call; at most _SHARD_CACHE_MAX problems are kept."""
+    sh = _SHARD_CACHE.pop(key, None)
+    if sh is None:
+        while len(_SHARD_CACHE) >= _SHARD_CACHE_MAX:
+            _SHARD_CACHE.pop(next(iter(_SHARD_CACHE))).close()
+        sh = make()
+    _SHARD_CACHE[key] = sh
+    return sh
+
+
 def xigemm_sharded(a_rows, b, c_rows=None, alpha: float = 1.0, beta: float = 0.0,
-                   cfg: XigemmConfig | None = None, *, group=None, reduce: bool = True, out=None) -> GemmReport:
+                   cfg: XigemmConfig | None = None, *, group=None, reduce: bool = True, out=None,
+                   rank_rows: list[int] | None = None) -> GemmReport:
     """This rank's rows of the row-sharded xigemm (torch.distributed must be
     initialised; B must already be identical on every rank, see broadcast_b).
+    rank_rows (every rank's row count) is all-gathered when not given.
     Returns the global report with this rank's result rows."""
     import torch.distributed as dist
     cfg = cfg or XigemmConfig()
     x, _ = _dev(a_rows, torch.float32)
+    y, _ = _dev(b, torch.float32)
+    cc = None if c_rows is None else _dev(c_rows, torch.float32)[0]
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    mine = torch.tensor([x.shape[0]], dtype=torch.int64, device="cuda")
-    allm = [torch.zeros_like(mine) for _ in range(world)]
-    dist.all_gather(allm, mine, group=group)
-    rows = [int(t.item()) for t in allm]
-    sh = Shard(x, b, c_rows, alpha, beta, rank, rows, cfg, reduce, out)
-    try:
-        run_protocol([sh], DistComm(group), world)
-        rep = sh.finish()
-    finally:
-        sh.close()
-    return _report(rep, sh.out)
+    if rank_rows is None:
+        mine = torch.tensor([x.shape[0]], dtype=torch.int64, device="cuda")
+        allm = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allm, mine, group=group)
+        rank_rows = [int(t) for t in torch.cat(allm).tolist()]
+    if out is None:
+        out = torch.empty((x.shape[0], y.shape[1]), dtype=torch.float32, device="cuda")
+    c = cfg.c()
+    key = (x.data_ptr(), tuple(x.shape), y.data_ptr(), tuple(y.shape), 0 if cc is None else cc.data_ptr(),
+           out.data_ptr(), float(alpha), float(beta), bool(reduce), rank, tuple(rank_rows),
+           (c.bits, c.threshold, c.density_limit, c.scheme, c.policy, c.rounding), id(group))
+    sh = _cached_shard(key, lambda: Shard(x, y, cc, alpha, beta, rank, rank_rows, cfg, reduce, out))
+    run_protocol([sh], DistComm(group), world)
+    return _report(sh.finish(), sh.out)

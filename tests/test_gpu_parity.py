@@ -354,3 +354,32 @@ def test_pipeline_vs_oracle_wide(oracle, shape):
         rep = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), cfg=cfg_from(c))
         assert beq(rep.result, ref), (shape, scheme, pol, bits)
         assert (rep.density_a, rep.density_b, int(rep.path)) == (orep.density_a, orep.density_b, orep.path)
+
+
+@pytest.mark.parametrize("shape", [(9, 7), (300, 1030), (600, 2048)])
+def test_quantize_nan_maps_to_minus_qmax(oracle, shape):
+    """quantize.cpp:13-24: a NaN element quantises to -qmax (x86 llround of NaN),
+    the slice maximum skips it; every scheme, both the row and column kernels."""
+    a = ol.random_dense(*shape, seed=sum(shape), lo=-3, hi=3)
+    a[1, 2] = np.nan
+    a[shape[0] - 1, shape[1] - 1] = np.nan
+    for scheme in (0, 1, 2):
+        rc, q_ref, s_ref = oracle.quantize(a, 8, scheme, 1)
+        q = xg.quantize(torch.from_numpy(a).cuda(), 8, scheme, 1)
+        assert beq(q.data, q_ref) and beq(q.scales.values, s_ref), scheme
+
+
+def test_pipeline_nan_input_rejected():
+    """A NaN anywhere rejects the call (pipeline.cpp:50-52) without faulting."""
+    for shape in ((3, 8, 4), (300, 1024, 260)):
+        m, k, n = shape
+        a = torch.zeros((m, k), device="cuda")
+        b = torch.ones((k, n), device="cuda")
+        a[1, 2] = float("nan")
+        with pytest.raises(xg.InvalidArgument):
+            xg.xigemm(a, b)
+        b[k - 1, n - 1] = float("nan")
+        a[1, 2] = 0.0
+        with pytest.raises(xg.InvalidArgument):
+            xg.xigemm(a, b)
+    torch.cuda.synchronize()
