@@ -537,14 +537,15 @@ struct GraphEntry {
     int dev = -1;
     PipeWs ws{};
     void* ws_base = nullptr;
-    cudaGraphExec_t exec[4] = {nullptr, nullptr, nullptr, nullptr};
-    int64_t launches[4] = {0, 0, 0, 0};
+    cudaGraphExec_t exec = nullptr;  // the whole pipeline, one graph
+    int64_t launches = 0;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // stage boundaries (event nodes)
+    xg::DevScalars* host_sc = nullptr;  // pinned; the graph's last node copies the scalars here
     int hits = 0;
     bool busy = false;
     uint64_t last = 0;
     void release() {
-        for (auto& e : exec)
-            if (e) cudaGraphExecDestroy(e), e = nullptr;
+        if (exec) cudaGraphExecDestroy(exec), exec = nullptr;
         if (ws_base) cudaFree(ws_base), ws_base = nullptr;
     }
 };
@@ -568,28 +569,37 @@ bool graphs_enabled() {
     return on;
 }
 
-// Capture the four stage groups of `e` (its workspace) into graphs.
+// Capture the whole pipeline of `e` (its workspace) into one graph: event
+// record nodes at the stage boundaries (timings) and a final copy of the
+// device scalars into pinned host memory, so a replay is one graph launch and
+// one stream synchronisation.
 void capture_entry(GraphEntry& e) {
     static thread_local cudaStream_t cs = nullptr;
     if (!cs) ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
-    for (int st = 0; st < 4; ++st) {
-        cudaGraph_t g = nullptr;
-        ck(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
-        int64_t n = 0;
-        try {
-            n = enqueue_stage(st, e.key, e.ws, nullptr, cs);
-        } catch (...) {
-            cudaStreamEndCapture(cs, &g);
-            if (g) cudaGraphDestroy(g);
-            throw;
+    for (auto& ev : e.ev)
+        if (!ev) ck(cudaEventCreate(&ev), "event");
+    if (!e.host_sc) ck(cudaMallocHost(&e.host_sc, sizeof(xg::DevScalars)), "pinned scalars");
+    cudaGraph_t g = nullptr;
+    ck(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
+    int64_t n = 0;
+    try {
+        for (int st = 0; st < 4; ++st) {
+            ck(cudaEventRecordWithFlags(e.ev[st], cs, cudaEventRecordExternal), "event");
+            n += enqueue_stage(st, e.key, e.ws, nullptr, cs);
         }
-        ck(cudaStreamEndCapture(cs, &g), "end capture");
-        const cudaError_t r = cudaGraphInstantiate(&e.exec[st], g, 0);
-        cudaGraphDestroy(g);
-        ck(r, "graph instantiate");
-        e.launches[st] = n;
-        g_launches -= n;  // counted again at every replay
+        ck(cudaEventRecordWithFlags(e.ev[4], cs, cudaEventRecordExternal), "event");
+        ck(cudaMemcpyAsync(e.host_sc, e.ws.sc, sizeof(xg::DevScalars), cudaMemcpyDeviceToHost, cs), "report");
+    } catch (...) {
+        cudaStreamEndCapture(cs, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
     }
+    ck(cudaStreamEndCapture(cs, &g), "end capture");
+    const cudaError_t r = cudaGraphInstantiate(&e.exec, g, 0);
+    cudaGraphDestroy(g);
+    ck(r, "graph instantiate");
+    e.launches = n;
+    g_launches -= n;  // counted again at every replay
 }
 
 // Returns the entry to replay (marked busy), or nullptr for the eager path.
@@ -664,7 +674,7 @@ void run_pipeline(const float* a, const float* b, const float* c, float alpha, f
     if (e) {
         bool failed = true;
         try {
-            if (!e->exec[0]) {
+            if (!e->exec) {
                 // persistent workspace of this entry, one allocation
                 int64_t total = 0;
                 alloc_ws(e->ws, M, N, ldk, [&](auto* tag, int64_t n) {
@@ -682,14 +692,12 @@ void run_pipeline(const float* a, const float* b, const float* c, float alpha, f
                 });
                 capture_entry(*e);
             }
-            for (int st = 0; st < 4; ++st) {
-                tm.mark();
-                ck(cudaGraphLaunch(e->exec[st], s), "graph launch");
-                g_launches += e->launches[st];
-            }
-            tm.mark();
-            ck(cudaMemcpyAsync(&h, e->ws.sc, sizeof h, cudaMemcpyDeviceToHost, s), "report");
+            ck(cudaGraphLaunch(e->exec, s), "graph launch");
+            g_launches += e->launches;
             ck(cudaStreamSynchronize(s), "pipeline");
+            h = *e->host_sc;
+            tm.ev = e->ev;  // the graph's event nodes bound the stages
+            tm.n = rep ? 5 : 0;
             failed = false;
         } catch (...) {
             graph_release(e, true);
