@@ -20,6 +20,7 @@
 //   reduce_a / reduce_b (+density, quantize_csr values) sparse.cpp:36-95,193-240
 #include <cuda.h>
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -1334,9 +1335,15 @@ __device__ __forceinline__ float4 ld_stream(const float* p) {
 
 // the 2*qmax+1 entries float(q / lam) (quantize.cpp:156), exact: fast product
 // with a proven-safe rounding check, fp64 division otherwise
+// float(-q / lam) == -float(q / lam) (round-to-nearest is symmetric): half the
+// entries are computed, the negative ones mirrored (q = 0 keeps +0).
 __device__ __forceinline__ void build_row_lut(float* lut, double lam, int qmax) {
     const double inv = __ddiv_rn(1.0, lam);
-    for (int e = threadIdx.x; e <= 2 * qmax; e += kRT) lut[e] = dequant_fast(e - qmax, inv, lam);
+    for (int q = threadIdx.x; q <= qmax; q += kRT) {
+        const float v = dequant_fast(q, inv, lam);
+        lut[qmax + q] = v;
+        if (q > 0) lut[qmax - q] = -v;
+    }
 }
 
 template <int U>
@@ -1499,14 +1506,14 @@ __global__ void __launch_bounds__(kRT, 4) k_quant_rows_r4(const QuantRowsArgs a)
 // writes its 32 output bytes of row n of B^T itself (two 16-byte stores), so
 // no shared-memory transpose is needed.  The per-strip dequant tables
 // lut[q][lane] are built once per item (2 CTA barriers per item).
-constexpr int kWC = 32, kWR = 32, kWItemRows = 1024, kWSlots = 2, kWW = 8;
-constexpr int kWCtas = 2;
-constexpr int kWSub = kWItemRows / (kWW * kWR);  // sub-tiles per warp per item
-constexpr int kColWSmem = kWW * kWSlots * kWC * kWR * 4 + 256 * kWC * 4 + 1024;
+constexpr int kWC = 32, kWR = 32, kWSub = 4;  // strip width, sub-tile rows, sub-tiles per warp per item
+template <int WW, int SLOTS>
+constexpr int col_w_smem() { return WW * SLOTS * kWC * kWR * 4 + 256 * kWC * 4 + 1024; }
 
-template <bool SELECT>
+template <bool SELECT, int kWW, int kWSlots, int kWCtas>
 __global__ void __launch_bounds__(kWW * 32, kWCtas)
     k_cols_w4(const __grid_constant__ CUtensorMap tmap, const QuantColsArgs qa, const SelectArgs sa) {
+    constexpr int kWItemRows = kWW * kWR * kWSub;
     XG_EXIT_IF_NONFINITE(SELECT ? sa.nonfinite : qa.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float* ring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
@@ -1571,8 +1578,13 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
         __syncthreads();  // previous item's table readers are done
         {
             const double inv = __ddiv_rn(1.0, lam);
-            for (int e = w * (256 / kWW); e < (w + 1) * (256 / kWW); ++e)
-                if (e <= 2 * qmax) lut[e][lane] = dequant_fast(e - qmax, inv, lam);
+            constexpr int per = (128 + kWW - 1) / kWW;  // q in [0, qmax], mirrored (see build_row_lut)
+            for (int q = w * per; q < (w + 1) * per; ++q)
+                if (q <= qmax) {
+                    const float v = dequant_fast(q, inv, lam);
+                    lut[qmax + q][lane] = v;
+                    if (q > 0) lut[qmax - q][lane] = -v;
+                }
         }
         __syncthreads();
         float lmax = 0.0f;
@@ -1790,18 +1802,48 @@ int col_async_grid(int rows, int cols) {
     return items < g ? items : g;
 }
 
-int col_w4_grid(int rows, int cols, int co_share) {
-    const int items = ((cols + kWC - 1) / kWC) * ((rows + kWItemRows - 1) / kWItemRows);
-    const int g = kNumSMs * (co_share > 0 ? co_share : kWCtas);
-    return items < g ? items : g;
+// Column-kernel shape (warps per CTA, ring slots per warp, CTAs per SM);
+// XG_COLW=WWxSLOTSxCTAS picks a compiled variant (tuning aid).
+struct ColW { int ww, slots, ctas; };
+ColW colw_shape() {
+    static const ColW c = [] {
+        ColW d{16, 2, 1};
+        if (const char* e = getenv("XG_COLW")) {
+            ColW v{};
+            if (sscanf(e, "%dx%dx%d", &v.ww, &v.slots, &v.ctas) == 3) d = v;
+        }
+        return d;
+    }();
+    return c;
+}
+
+template <bool SELECT, int WW, int SLOTS, int CTAS>
+void launch_cols_w(const CUtensorMap& tm, const QuantColsArgs& qa, const SelectArgs& sa, int rows, int cols,
+                   int co_share, cudaStream_t s) {
+    constexpr int smem = col_w_smem<WW, SLOTS>();
+    auto kern = k_cols_w4<SELECT, WW, SLOTS, CTAS>;
+    set_dyn_smem(kern, smem);
+    const int items = ((cols + kWC - 1) / kWC) * ((rows + WW * kWR * kWSub - 1) / (WW * kWR * kWSub));
+    const int cap = kNumSMs * (co_share > 0 ? co_share : CTAS);
+    kern<<<items < cap ? items : cap, WW * 32, smem, s>>>(tm, qa, sa);
+}
+
+template <bool SELECT>
+void launch_cols_any(const CUtensorMap& tm, const QuantColsArgs& qa, const SelectArgs& sa, int rows, int cols,
+                     int co_share, cudaStream_t s) {
+    const ColW c = colw_shape();
+    if (c.ww == 12 && c.slots == 1 && c.ctas == 2) launch_cols_w<SELECT, 12, 1, 2>(tm, qa, sa, rows, cols, co_share, s);
+    else if (c.ww == 24 && c.slots == 1 && c.ctas == 1) launch_cols_w<SELECT, 24, 1, 1>(tm, qa, sa, rows, cols, co_share, s);
+    else if (c.ww == 16 && c.slots == 2 && c.ctas == 1) launch_cols_w<SELECT, 16, 2, 1>(tm, qa, sa, rows, cols, co_share, s);
+    else if (c.ww == 4 && c.slots == 4 && c.ctas == 2) launch_cols_w<SELECT, 4, 4, 2>(tm, qa, sa, rows, cols, co_share, s);
+    else launch_cols_w<SELECT, 8, 2, 2>(tm, qa, sa, rows, cols, co_share, s);
 }
 
 void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {
     if (a.rounding == kNearest && r4_enabled() && a.rows >= 256 && (a.ldq % 16) == 0) {
         alignas(64) CUtensorMap tm;
         if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) {
-            set_dyn_smem(k_cols_w4<false>, kColWSmem);
-            k_cols_w4<false><<<col_w4_grid(a.rows, a.cols, a.co_share), kWW * 32, kColWSmem, s>>>(tm, a, SelectArgs{});
+            launch_cols_any<false>(tm, a, SelectArgs{}, a.rows, a.cols, a.co_share, s);
             return;
         }
     }
@@ -1855,8 +1897,7 @@ void launch_select_cols_T(const SelectArgs& a, cudaStream_t s) {
     if (a.rounding == kNearest && r4_enabled() && a.rows >= 256 && (a.ldq % 16) == 0) {
         alignas(64) CUtensorMap tm;
         if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) {
-            set_dyn_smem(k_cols_w4<true>, kColWSmem);
-            k_cols_w4<true><<<col_w4_grid(a.rows, a.cols, a.co_share), kWW * 32, kColWSmem, s>>>(tm, QuantColsArgs{}, a);
+            launch_cols_any<true>(tm, QuantColsArgs{}, a, a.rows, a.cols, a.co_share, s);
             return;
         }
     }
