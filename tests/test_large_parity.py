@@ -1,0 +1,149 @@
+"""Full-size parity at BASELINE.json's configurations (SURVEY.md section 8(c),
+"large-shape parity method"): the GPU pipeline runs the whole problem and
+dumps every intermediate; each stage is then checked against the CPU oracle's
+stage function fed the already-verified inputs of that stage:
+
+  K1  Aq, lambda_a, Bq, lambda_b, RAq, RBq, lambda_R      full matrices
+  K2  D_F                                                  sampled rows (fp64 BLAS products are exact)
+  -   AvgRule row / column means of |D_F|                  full (reference order, oracle C)
+  K3  kept sets of A and B, A'q, B'q, densities, path      full
+  K4+5 final C = fl(fl(D_F + dr1) + dr2)                   sampled rows
+
+C5 (65536 x 16384^2, row-sharded) is checked as 8 in-process shards against the
+single-GPU pipeline, bit for bit.  All comparisons are bit-exact."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle_lib as ol  # noqa: E402
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2403_06924_b200 as xg  # noqa: E402
+from paper_2403_06924_b200 import sharded  # noqa: E402
+
+
+def beq(x, y):
+    x = x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+    y = y.cpu().numpy() if hasattr(y, "cpu") else np.asarray(y)
+    if x.shape != y.shape:
+        return False
+    if x.dtype.kind == "f":
+        w = np.uint32 if x.dtype.itemsize == 4 else np.uint64
+        return np.array_equal(x.view(w), y.astype(x.dtype).view(w))
+    return np.array_equal(x, y)
+
+
+def vw_cfg(thr, s=0.3):
+    return xg.XigemmConfig(threshold=thr, density_limit=s, scheme=xg.QuantScheme.VectorWise,
+                           policy=xg.ReductionPolicy.AvgRule)
+
+
+def bisect_threshold(a, b, target, s=0.3):
+    lo, hi = 1e-4, 10.0
+    for _ in range(40):
+        mid = (lo * hi) ** 0.5
+        r = xg.xigemm(a, b, cfg=vw_cfg(mid, s))
+        d = max(r.density_a, r.density_b)
+        if abs(d - target) <= 0.1 * target:
+            return mid
+        lo, hi = (mid, hi) if d > target else (lo, mid)
+    return mid
+
+
+def stagewise(a, b, thr, s=0.3, nrows=48, seed=0):
+    o = ol.oracle()
+    cfg = vw_cfg(thr, s)
+    rep, d = xg.xigemm_dump(a, b, cfg)
+    res = rep.result.cpu().numpy()
+    an, bn = a.cpu().numpy(), b.cpu().numpy()
+    m, k = an.shape
+    n = bn.shape[1]
+    # K1
+    rc, aq, la = o.quantize(an, 8, 1, 1)
+    assert rc == 0 and beq(d["aq"], aq) and beq(d["aq_scales"], la)
+    rc, bq, lb = o.quantize(bn, 8, 2, 1)
+    assert rc == 0 and beq(d["bq"], bq) and beq(d["bq_scales"], lb)
+    rc, ra = o.residual(an, aq, la, 1)
+    rc, raq, lra = o.quantize(ra, 8, 0, 1)  # pipeline.cpp:86-93: always per tensor
+    assert beq(d["raq"], raq) and beq(d["raq_scale"], lra)
+    rc, rb = o.residual(bn, bq, lb, 2)
+    rc, rbq, lrb = o.quantize(rb, 8, 0, 1)
+    assert beq(d["rbq"], rbq) and beq(d["rbq_scale"], lrb)
+    del ra, rb
+    # K2 on sampled rows (int8 products summed exactly in fp64: |sum| < 2^31)
+    rows = np.sort(np.random.default_rng(seed).choice(m, size=min(nrows, m), replace=False))
+    dint = (aq[rows].astype(np.float64) @ bq.astype(np.float64)).astype(np.int32)
+    rc, df_rows = o.dequant_product(dint, la[rows], lb, 1, 2)
+    df = d["d_f"].cpu().numpy()
+    assert beq(df[rows], df_rows)
+    # statistics in the reference's order, full
+    rc, rs, cs = o.avg_vectors(df)
+    assert beq(d["row_stat"], rs) and beq(d["col_stat"], cs)
+    del df
+    # K3 kept sets
+    rc, rp, ci, _ = o.reduce(an, rs, thr, 0, per_row=True)
+    mask_a = np.zeros((m, k), bool)
+    mask_a[np.repeat(np.arange(m), np.diff(rp)), ci] = True
+    rc, rp, ci, _ = o.reduce(bn, cs, thr, 0, per_row=False)
+    mask_b = np.zeros((k, n), bool)
+    mask_b[np.repeat(np.arange(k), np.diff(rp)), ci] = True
+    a_red = np.where(mask_a, aq, 0).astype(np.int8)
+    b_red = np.where(mask_b, bq, 0).astype(np.int8)
+    assert beq(d["a_red"], a_red) and beq(d["b_red"], b_red)
+    dens_a = float(mask_a.sum()) / (float(m) * k)
+    dens_b = float(mask_b.sum()) / (float(k) * n)
+    assert (rep.density_a, rep.density_b) == (dens_a, dens_b)
+    sparse_path = max(dens_a, dens_b) < s
+    assert int(rep.path) == (0 if sparse_path else 1)
+    # K4 + K5 on the sampled rows (pipeline.cpp:113-145)
+    x1, y2 = (a_red, b_red) if sparse_path else (aq, bq)
+    dr1 = (x1[rows].astype(np.float64) @ rbq.astype(np.float64)).astype(np.int32)
+    dr2 = (raq[rows].astype(np.float64) @ y2.astype(np.float64)).astype(np.int32)
+    rc, t1 = o.dequant_product(dr1, la[rows], lrb, 1, 0)
+    rc, t2 = o.dequant_product(dr2, lra, lb, 0, 2)
+    want = (df_rows + t1) + t2  # float32 adds, round to nearest (pipeline.cpp:141-145)
+    assert beq(res[rows], want)
+    return rep
+
+
+def test_c2_4096_normal_density_sweep():
+    """C2: 4096^3, normal(0,1), thresholds giving 1% / 5% / 10% residual density."""
+    a = xg.generate("normal", 4096, 4096, 1, 0.0, 1.0)
+    b = xg.generate("normal", 4096, 4096, 2, 0.0, 1.0)
+    for target in (0.01, 0.05, 0.10):
+        thr = bisect_threshold(a, b, target)
+        rep = stagewise(a, b, thr, seed=int(target * 100))
+        assert abs(max(rep.density_a, rep.density_b) - target) <= 0.1 * target
+
+
+def test_c3_8192_student_t_5pct():
+    """C3 (the bench workload): 8192^3, Student-t(3), 5% density."""
+    a = xg.generate("student_t3", 8192, 8192, 1, 0.0, 1.0)
+    b = xg.generate("student_t3", 8192, 8192, 2, 0.0, 1.0)
+    rep = stagewise(a, b, 0.01539926526059492, nrows=32)
+    assert int(rep.path) == 0 and 0.045 <= max(rep.density_a, rep.density_b) <= 0.055
+
+
+def test_c4_llm_linear_shape():
+    """C4: M=16384, N=11008, K=4096 (LLM linear), A Student-t(3), B normal."""
+    a = xg.generate("student_t3", 16384, 4096, 1, 0.0, 1.0)
+    b = xg.generate("normal", 4096, 11008, 2, 0.0, 1.0)
+    thr = bisect_threshold(a, b, 0.05)
+    rep = stagewise(a, b, thr, nrows=32)
+    assert int(rep.path) == 0
+
+
+def test_c5_row_sharded_equals_single():
+    """C5: M=65536, N=K=16384 normal(0,1), 8 row shards (one process, one GPU)
+    against the single-GPU pipeline, bit for bit, with the global report."""
+    a = xg.generate("normal", 65536, 16384, 1, 0.0, 1.0)
+    b = xg.generate("normal", 16384, 16384, 2, 0.0, 1.0)
+    cfg = vw_cfg(0.05)
+    ref = xg.xigemm(a, b, cfg=cfg)
+    got = sharded.xigemm_sharded_local(a, b, cfg=cfg, nranks=8)
+    assert beq(got.result, ref.result)
+    assert (got.density_a, got.density_b, int(got.path)) == (ref.density_a, ref.density_b, int(ref.path))
