@@ -569,6 +569,41 @@ bool graphs_enabled() {
     return on;
 }
 
+// Opt-in (XG_PDL=1): measured no gain at C3 (1.645 vs 1.648 ms per call).
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("XG_PDL");
+        return e && *e == '1';
+    }();
+    return on;
+}
+
+// Programmatic dependent launch inside the graph: every kernel->kernel edge
+// becomes a programmatic edge, so a kernel's CTAs are launched (prologue:
+// barriers, TMEM allocation, tensor-map prefetch) while its predecessor's last
+// CTAs finish; each kernel waits (griddepcontrol.wait, XG_PDL_WAIT) before it
+// reads anything the predecessor wrote.
+void make_programmatic(cudaGraph_t g) {
+    size_t ne = 0;
+    ck(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne), "graph edges");
+    if (!ne) return;
+    std::vector<cudaGraphNode_t> from(ne), to(ne);
+    std::vector<cudaGraphEdgeData> data(ne);
+    ck(cudaGraphGetEdges_v2(g, from.data(), to.data(), data.data(), &ne), "graph edges");
+    for (size_t i = 0; i < ne; ++i) {
+        cudaGraphNodeType tf, tt;
+        ck(cudaGraphNodeGetType(from[i], &tf), "node type");
+        ck(cudaGraphNodeGetType(to[i], &tt), "node type");
+        if (tf != cudaGraphNodeTypeKernel || tt != cudaGraphNodeTypeKernel) continue;
+        if (data[i].type != cudaGraphDependencyTypeDefault) continue;
+        cudaGraphEdgeData pe = data[i];
+        pe.from_port = cudaGraphKernelNodePortProgrammatic;
+        pe.type = cudaGraphDependencyTypeProgrammatic;
+        ck(cudaGraphRemoveDependencies_v2(g, &from[i], &to[i], &data[i], 1), "remove edge");
+        ck(cudaGraphAddDependencies_v2(g, &from[i], &to[i], &pe, 1), "programmatic edge");
+    }
+}
+
 // Capture the whole pipeline of `e` (its workspace) into one graph: event
 // record nodes at the stage boundaries (timings) and a final copy of the
 // device scalars into pinned host memory, so a replay is one graph launch and
@@ -595,6 +630,7 @@ void capture_entry(GraphEntry& e) {
         throw;
     }
     ck(cudaStreamEndCapture(cs, &g), "end capture");
+    if (pdl_enabled()) make_programmatic(g);
     const cudaError_t r = cudaGraphInstantiate(&e.exec, g, 0);
     cudaGraphDestroy(g);
     ck(r, "graph instantiate");
@@ -1017,6 +1053,7 @@ extern "C" double xg_debug_gemm_df(int m, int n, int k, int flags, int iters) {
 namespace {
 __global__ void k_debug_dq_ff(const int32_t* p, const double* la, const double* lb, int64_t n,
                               float* out, int* flags) {
+    XG_PDL_WAIT();
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
          x += (int64_t)gridDim.x * blockDim.x) {
         // exactly the epilogue sequence: dq_ff24, then dq_slow for flagged elements
@@ -1272,6 +1309,7 @@ struct ShardState {
 
 __global__ void k_shard_xfer(xg::DevScalars* sc, uint32_t* x1, unsigned long long* x4n, uint32_t* x4r,
                              int* n_remote, int what) {
+    XG_PDL_WAIT();
     switch (what) {
         case 0: x1[0] = sc->maxA; x1[1] = sc->maxRA; x1[2] = (uint32_t)sc->nonfinite; x1[3] = 0; break;
         case 1: sc->maxA = x1[0]; sc->maxRA = x1[1]; sc->nonfinite = (int)x1[2]; break;

@@ -289,6 +289,11 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
+// Programmatic dependent launch: a kernel that may be started before its
+// predecessor in the graph has finished (programmatic edge) waits here before
+// touching any memory the predecessor writes.  A no-op without such an edge.
+#define XG_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
 // --------------------------------------------------------------- PTX: misc --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -225,7 +225,6 @@ __global__ void __launch_bounds__(256, 1)
     const int num_n = (args.N + BN - 1) / BN;
     const int num_tiles = num_m * num_n;
     const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
-    const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -246,6 +245,8 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    XG_PDL_WAIT();
+    const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -435,7 +436,6 @@ __global__ void __launch_bounds__(384, 1)
     const int num_n = (args.N + Cfg::BN - 1) / Cfg::BN;
     const int num_tiles = num_m * num_n;
     const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
-    const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
     const int gm = args.group_m > 0 ? args.group_m : Cfg::GROUP_M;
 
     if (threadIdx.x == 0) {
@@ -460,6 +460,9 @@ __global__ void __launch_bounds__(384, 1)
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // everything above overlaps the predecessor's tail under a programmatic edge
+    XG_PDL_WAIT();
+    const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================

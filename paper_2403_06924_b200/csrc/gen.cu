@@ -34,6 +34,7 @@ __device__ __forceinline__ double normal_at(uint64_t seed, uint64_t pos) {
 // kind 2: Student-t(3) scaled by p2: z / sqrt((z1^2+z2^2+z3^2)/3)  (8 draws)
 // kind 3: exponential(p1)                               (1 draw)
 __global__ void k_generate(int kind, double p1, double p2, uint64_t seed, int64_t n, float* out) {
+    XG_PDL_WAIT();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         float v;

@@ -32,6 +32,7 @@ __device__ __forceinline__ double scale_of(int scheme, const double* s, int i, i
 // src: rows x cols int8 with pitch lds -> dst: cols x rows with pitch ldd
 __global__ void k_transpose_i8(const int8_t* __restrict__ src, int rows, int cols, int64_t lds,
                                int8_t* __restrict__ dst, int64_t ldd) {
+    XG_PDL_WAIT();
     __shared__ int8_t t[32][33];
     const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -48,6 +49,7 @@ __global__ void k_transpose_i8(const int8_t* __restrict__ src, int rows, int col
 __global__ void k_quantize_with_scales(const float* __restrict__ a, int rows, int cols, int bits,
                                        int scheme, const double* __restrict__ s, int rounding,
                                        int8_t* __restrict__ q) {
+    XG_PDL_WAIT();
     const int qmax = quant_max(bits);
     const int64_t n = (int64_t)rows * cols;
     GRID_STRIDE(x, n) {
@@ -59,6 +61,7 @@ __global__ void k_quantize_with_scales(const float* __restrict__ a, int rows, in
 __global__ void k_dequantize(const int8_t* __restrict__ q, int rows, int cols, int scheme,
                              const double* __restrict__ s, const float* __restrict__ a,
                              float* __restrict__ out) {
+    XG_PDL_WAIT();
     const int64_t n = (int64_t)rows * cols;
     GRID_STRIDE(x, n) {
         const int i = (int)(x / cols), j = (int)(x % cols);
@@ -70,6 +73,7 @@ __global__ void k_dequantize(const int8_t* __restrict__ q, int rows, int cols, i
 __global__ void k_dequant_product(const int32_t* __restrict__ p, int rows, int cols, int sa_scheme,
                                   const double* __restrict__ sa, int sb_scheme,
                                   const double* __restrict__ sb, float* __restrict__ out) {
+    XG_PDL_WAIT();
     const int64_t n = (int64_t)rows * cols;
     GRID_STRIDE(x, n) {
         const int i = (int)(x / cols), j = (int)(x % cols);
@@ -82,6 +86,7 @@ __global__ void k_dequant_product(const int32_t* __restrict__ p, int rows, int c
 // matrix.cpp:75-95: fp64 accumulate over ascending k, then float.
 __global__ void k_gemm_f32_exact(const float* __restrict__ a, const float* __restrict__ b, int m,
                                  int k, int n, float* __restrict__ c) {
+    XG_PDL_WAIT();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = blockIdx.y;
     if (j >= n || i >= m) return;
@@ -93,13 +98,16 @@ __global__ void k_gemm_f32_exact(const float* __restrict__ a, const float* __res
 
 __global__ void k_axpby(float* __restrict__ d, float alpha, const float* __restrict__ c, float beta,
                         int64_t n) {
+    XG_PDL_WAIT();
     GRID_STRIDE(x, n) { d[x] = __fadd_rn(__fmul_rn(alpha, d[x]), __fmul_rn(beta, c[x])); }
 }
 __global__ void k_subtract(const float* __restrict__ a, const float* __restrict__ b,
                            float* __restrict__ o, int64_t n) {
+    XG_PDL_WAIT();
     GRID_STRIDE(x, n) { o[x] = __fsub_rn(a[x], b[x]); }
 }
 __global__ void k_add(float* __restrict__ d, const float* __restrict__ x, int64_t n) {
+    XG_PDL_WAIT();
     GRID_STRIDE(i, n) { d[i] = __fadd_rn(d[i], x[i]); }
 }
 
@@ -127,6 +135,7 @@ __device__ __forceinline__ bool keep_at(int mode, const float* m, int cols, int 
 __global__ void k_csr_count(int mode, const float* __restrict__ m, int rows, int cols,
                             const float* stat, double thr_m, int policy, double so, int per_row,
                             int32_t* __restrict__ cnt) {
+    XG_PDL_WAIT();
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= rows) return;
@@ -141,6 +150,7 @@ __global__ void k_csr_fill(int mode, const float* __restrict__ m, int rows, int 
                            const float* stat, double thr_m, int policy, double so, int per_row,
                            const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
                            float* __restrict__ values) {
+    XG_PDL_WAIT();
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= rows) return;
@@ -160,12 +170,14 @@ __global__ void k_csr_fill(int mode, const float* __restrict__ m, int rows, int 
 
 // exclusive scan of cnt[0..rows) into row_ptr[0..rows], row_ptr[rows] = total
 __global__ void k_shift_total(int32_t* row_ptr, const int32_t* cnt, int rows) {
+    XG_PDL_WAIT();
     row_ptr[rows] = rows > 0 ? row_ptr[rows - 1] + cnt[rows - 1] : 0;
 }
 
 // quantize_csr scales (sparse.cpp:198-225)
 __global__ void k_csr_rowmax(int rows, const int32_t* __restrict__ rp, const float* __restrict__ v,
                              int bits, double* scales) {
+    XG_PDL_WAIT();
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= rows) return;
@@ -176,6 +188,7 @@ __global__ void k_csr_rowmax(int rows, const int32_t* __restrict__ rp, const flo
 }
 __global__ void k_csr_colmax(int64_t nnz, const int32_t* __restrict__ ci, const float* __restrict__ v,
                              uint32_t* colmax, uint32_t* tmax) {
+    XG_PDL_WAIT();
     GRID_STRIDE(p, nnz) {
         const uint32_t b = fbits(fabsf(v[p]));
         atomicMax(colmax + ci[p], b);
@@ -183,11 +196,13 @@ __global__ void k_csr_colmax(int64_t nnz, const int32_t* __restrict__ ci, const 
     }
 }
 __global__ void k_scales_from_bits(const uint32_t* bits_in, int n, int bits, double* scales) {
+    XG_PDL_WAIT();
     GRID_STRIDE(i, (int64_t)n) { scales[i] = compute_scale((double)__uint_as_float(bits_in[i]), bits); }
 }
 __global__ void k_csr_quant(int rows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             const float* __restrict__ v, int bits, int scheme,
                             const double* __restrict__ s, int rounding, int8_t* __restrict__ q) {
+    XG_PDL_WAIT();
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= rows) return;
@@ -200,18 +215,22 @@ __global__ void k_csr_quant(int rows, const int32_t* __restrict__ rp, const int3
 
 // csr rows of each element (for transposes)
 __global__ void k_csr_rows(int rows, const int32_t* __restrict__ rp, int32_t* __restrict__ r) {
+    XG_PDL_WAIT();
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= rows) return;
     for (int p = rp[w] + lane; p < rp[w + 1]; p += 32) r[p] = w;
 }
-__global__ void k_iota(int32_t* p, int64_t n) { GRID_STRIDE(i, n) p[i] = (int32_t)i; }
+__global__ void k_iota(int32_t* p, int64_t n) {
+    XG_PDL_WAIT(); GRID_STRIDE(i, n) p[i] = (int32_t)i; }
 __global__ void k_col_hist(int64_t nnz, const int32_t* __restrict__ ci, int32_t* cnt) {
+    XG_PDL_WAIT();
     GRID_STRIDE(p, nnz) atomicAdd(cnt + ci[p], 1);
 }
 template <class T>
 __global__ void k_gather_T(int64_t nnz, const int32_t* __restrict__ perm, const int32_t* __restrict__ rows_of,
                            const T* __restrict__ v, int32_t* __restrict__ tci, T* __restrict__ tv) {
+    XG_PDL_WAIT();
     GRID_STRIDE(p, nnz) {
         const int32_t src = perm[p];
         tci[p] = rows_of[src];
@@ -223,6 +242,7 @@ __global__ void k_gather_T(int64_t nnz, const int32_t* __restrict__ perm, const 
 __global__ void k_spmm_i8(int rows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                           const int8_t* __restrict__ v, const int8_t* __restrict__ d, int d_cols,
                           int32_t* __restrict__ out) {
+    XG_PDL_WAIT();
     const int i = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows || j >= d_cols) return;
@@ -235,6 +255,7 @@ __global__ void k_spmm_i8(int rows, const int32_t* __restrict__ rp, const int32_
 __global__ void k_spmm_f32(int rows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                            const float* __restrict__ v, const float* __restrict__ d, int d_cols,
                            float* __restrict__ out) {
+    XG_PDL_WAIT();
     const int i = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows || j >= d_cols) return;
@@ -247,6 +268,7 @@ __global__ void k_spmm_f32(int rows, const int32_t* __restrict__ rp, const int32
 __global__ void k_densify(int rows, int cols, const int32_t* __restrict__ rp,
                           const int32_t* __restrict__ ci, const float* __restrict__ v,
                           float* __restrict__ out) {
+    XG_PDL_WAIT();
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= rows) return;
@@ -256,6 +278,7 @@ __global__ void k_densify(int rows, int cols, const int32_t* __restrict__ rp,
 }
 
 __global__ void k_finite_max(const float* __restrict__ x, int64_t n, uint32_t* mx, int* bad) {
+    XG_PDL_WAIT();
     float m = 0.0f;
     int b = 0;
     GRID_STRIDE(i, n) {
@@ -272,6 +295,7 @@ __global__ void k_finite_max(const float* __restrict__ x, int64_t n, uint32_t* m
 }
 
 __global__ void k_random_i8(int8_t* p, int64_t n, uint64_t seed) {
+    XG_PDL_WAIT();
     GRID_STRIDE(i, n) {
         uint64_t z = seed + (uint64_t)i * 0x9E3779B97F4A7C15ULL;
         z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;

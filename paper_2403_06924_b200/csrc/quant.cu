@@ -134,6 +134,7 @@ __device__ __forceinline__ void store_quad(int8_t* __restrict__ row, int c, int 
 // reference's compute_scale throws), bit 1 = any NaN/inf (all_finite fails).
 template <int VPT, int RND>
 __global__ void __launch_bounds__(kThreads) k_quant_rows(const QuantRowsArgs a) {
+    XG_PDL_WAIT();
     __shared__ float lut[256];
     __shared__ float red[kThreads / 32];
     const int qmax = quant_max(a.bits);
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows(const QuantRowsArgs a) 
 // Generic (any column count) variant: two passes over the row, the second one
 // served from L2.  Exact scalar path throughout.
 __global__ void __launch_bounds__(kThreads) k_quant_rows_generic(const QuantRowsArgs a) {
+    XG_PDL_WAIT();
     __shared__ float lut[256];
     __shared__ float red[kThreads / 32];
     const int qmax = quant_max(a.bits);
@@ -245,6 +247,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows_generic(const QuantRows
 // --------------------------------------------------------------- absmaxes --
 __global__ void __launch_bounds__(kThreads)
     k_absmax_global(const float* __restrict__ x, int64_t n, uint32_t* gmax, int* nonfinite) {
+    XG_PDL_WAIT();
     __shared__ float red[kThreads / 32];
     float m = 0.0f;
     int bad = 0;
@@ -272,6 +275,7 @@ constexpr int kColSlab = 64;
 __global__ void __launch_bounds__(kThreads)
     k_absmax_cols(const float* __restrict__ x, int rows, int cols, int64_t ld, uint32_t* colmax,
                   uint32_t* gmax, int* nonfinite) {
+    XG_PDL_WAIT();
     __shared__ float red[kThreads / 32];
     const int c = (blockIdx.x * kThreads + threadIdx.x) * 4;
     const int r0 = blockIdx.y * kColSlab;
@@ -364,6 +368,7 @@ __device__ __forceinline__ void build_col_luts(float (*lut)[kTN], const double* 
 
 template <int RND>
 __global__ void __launch_bounds__(kThreads) k_quant_cols_T(const QuantColsArgs a) {
+    XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
@@ -466,6 +471,7 @@ __device__ __forceinline__ void select_quad(const float (&x)[4], const float* lu
 
 template <int RND>
 __global__ void __launch_bounds__(kThreads) k_select_rows(const SelectArgs a) {
+    XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
     __shared__ float lut[256];
     __shared__ float red[kThreads / 32];
@@ -531,6 +537,7 @@ __global__ void __launch_bounds__(kThreads) k_select_rows(const SelectArgs a) {
 // scale (sparse.cpp:198-203): rewrite the kept ints with lambda'.  Exits at
 // once in the usual case lambda' == lambda.  Exact scalar path (rare).
 __global__ void __launch_bounds__(kThreads) k_fix_rows(const SelectArgs a) {
+    XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
     const double lam_t = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
     const double lam_fix = compute_scale((double)__uint_as_float(*a.retmax), a.bits);
@@ -549,6 +556,7 @@ __global__ void __launch_bounds__(kThreads) k_fix_rows(const SelectArgs a) {
 
 // B side: column j of the reduced operand is row j of B'q^T.
 __global__ void __launch_bounds__(kThreads) k_fix_cols_T(const SelectArgs a) {
+    XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
     const double lam_t = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
     const double lam_fix = compute_scale((double)__uint_as_float(*a.retmax), a.bits);
@@ -569,6 +577,7 @@ __global__ void __launch_bounds__(kThreads) k_fix_cols_T(const SelectArgs a) {
 // B side: RBq^T and B'q^T (both N x K, K-major), column thresholds t_j.
 template <int RND>
 __global__ void __launch_bounds__(kThreads) k_select_cols_T(const SelectArgs a) {
+    XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
@@ -676,6 +685,7 @@ __device__ __forceinline__ uint32_t pack4u(uint32_t a, uint32_t b, uint32_t c, u
 
 template <int VPT, int NT>
 __global__ void __launch_bounds__(NT) k_quant_rows_fast(const QuantRowsArgs a) {
+    XG_PDL_WAIT();
     __shared__ float lut[256];
     __shared__ float red[NT / 32];
     const int qmax = quant_max(a.bits);
@@ -779,6 +789,7 @@ __device__ __forceinline__ void select_quad_n(const float (&x)[4], uint32_t lut_
 }
 
 __global__ void __launch_bounds__(kThreads) k_select_rows_fast(const SelectArgs a) {
+    XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
     __shared__ float lut[256];
     __shared__ float red[kThreads / 32];
@@ -831,6 +842,7 @@ __global__ void __launch_bounds__(kThreads) k_select_rows_fast(const SelectArgs 
 }
 
 __global__ void __launch_bounds__(kThreads) k_quant_cols_T_fast(const QuantColsArgs a) {
+    XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
@@ -896,6 +908,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_cols_T_fast(const QuantColsA
 }
 
 __global__ void __launch_bounds__(kThreads) k_select_cols_T_fast(const SelectArgs a) {
+    XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
@@ -988,6 +1001,7 @@ __device__ __forceinline__ void issue_row(float* slot, const float* src, uint32_
 
 // K1, A side: per-row absmax -> lambda, quantise, residual max (Nearest).
 __global__ void __launch_bounds__(kThreads) k_quant_rows_async(const QuantRowsArgs a) {
+    XG_PDL_WAIT();
     extern __shared__ float4 dyn_smem[];
     float* ring = reinterpret_cast<float*>(dyn_smem);
     __shared__ uint64_t full[kRowSlots];
@@ -1075,6 +1089,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows_async(const QuantRowsAr
 // K3, A side (Nearest): RAq and A'q from a streamed row ring; the per-row
 // dequant table for row i+1 is built while row i is processed.
 __global__ void __launch_bounds__(kThreads) k_select_rows_async(const SelectArgs a) {
+    XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
     extern __shared__ float4 dyn_smem[];
     float* ring = reinterpret_cast<float*>(dyn_smem);
@@ -1189,6 +1204,7 @@ __device__ __forceinline__ void store_T32(const uint32_t (*t)[kCW], int8_t* dst,
 template <bool SELECT>
 __global__ void __launch_bounds__(kThreads)
     k_cols_T_async(const __grid_constant__ CUtensorMap tmap, const QuantColsArgs qa, const SelectArgs sa) {
+    XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(SELECT ? sa.nonfinite : qa.nonfinite);
     extern __shared__ float4 dyn_smem[];
     // TMA destinations need 128-byte alignment
@@ -1348,6 +1364,7 @@ __device__ __forceinline__ void build_row_lut(float* lut, double lam, int qmax) 
 
 template <int U>
 __global__ void __launch_bounds__(kRT, kRCtasPerSM) k_select_rows_r4(const SelectArgs a) {
+    XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
     __shared__ float lut[2][256];
     __shared__ float redf[kRT / 32];
@@ -1415,6 +1432,7 @@ __global__ void __launch_bounds__(kRT, kRCtasPerSM) k_select_rows_r4(const Selec
 // lambda -> table -> quantise -> residual max; two CTA barriers per row.
 template <int VPT>
 __global__ void __launch_bounds__(kRT, 4) k_quant_rows_r4(const QuantRowsArgs a) {
+    XG_PDL_WAIT();
     __shared__ float lut[2][256];
     __shared__ float red[2][kRT / 32];
     const int qmax = quant_max(a.bits);
@@ -1513,6 +1531,7 @@ constexpr int col_w_smem() { return WW * SLOTS * kWC * kWR * 4 + 256 * kWC * 4 +
 template <bool SELECT, int kWW, int kWSlots, int kWCtas>
 __global__ void __launch_bounds__(kWW * 32, kWCtas)
     k_cols_w4(const __grid_constant__ CUtensorMap tmap, const QuantColsArgs qa, const SelectArgs sa) {
+    XG_PDL_WAIT();
     constexpr int kWItemRows = kWW * kWR * kWSub;
     XG_EXIT_IF_NONFINITE(SELECT ? sa.nonfinite : qa.nonfinite);
     extern __shared__ float4 dyn_smem[];
@@ -1671,6 +1690,7 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
 
 // ------------------------------------------------------------- scalars --
 __global__ void k_lambdas(DevScalars* sc, int bits) {
+    XG_PDL_WAIT();
     sc->lamA = compute_scale((double)__uint_as_float(sc->maxA), bits);
     sc->lamB = compute_scale((double)__uint_as_float(sc->maxB), bits);
 }
@@ -1678,6 +1698,7 @@ __global__ void k_lambdas(DevScalars* sc, int bits) {
 // Density, dispatch (pipeline.cpp:106-111) and the per-tensor scales the
 // compensation epilogue reads.
 __global__ void k_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, double s, int reduce) {
+    XG_PDL_WAIT();
     sc->lamRA = compute_scale((double)__uint_as_float(sc->maxRA), bits);
     sc->lamRB = compute_scale((double)__uint_as_float(sc->maxRB), bits);
     sc->lamAred = compute_scale((double)__uint_as_float(sc->retA), bits);
@@ -1698,6 +1719,7 @@ __global__ void k_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, dou
 }
 
 __global__ void k_fill_u32(uint32_t* p, uint32_t v, int64_t n) {
+    XG_PDL_WAIT();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         p[i] = v;

@@ -25,6 +25,7 @@ template <int POLICY>
 __global__ void __launch_bounds__(kThreads)
     k_stats_slab(const float* __restrict__ d, int rows, int cols, double* row_sum,
                  double* col_sum, uint32_t* row_min, uint32_t* col_min) {
+    XG_PDL_WAIT();
     const int c = (blockIdx.x * kThreads + threadIdx.x) * 4;
     const int r0 = blockIdx.y * kSlabRows;
     const int lane = threadIdx.x & 31;
@@ -118,6 +119,7 @@ __device__ __forceinline__ bool verified_mean(double S, int nterms, double n, fl
 __global__ void k_finalize_avg(const double* row_sum, const double* col_sum, int rows, int cols,
                                int col_n, float* row_stat, float* col_stat, int* flags, int* nflag,
                                int widen) {
+    XG_PDL_WAIT();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows + cols) return;
     float v;
@@ -148,6 +150,7 @@ __global__ void __launch_bounds__(kThreads)
     k_fallback_avg(const float* __restrict__ d, int rows, int cols, int col_n, const int* flags,
                    const int* nflag, float* row_stat, float* col_stat, const double* row_sum,
                    const double* col_sum, const StatsDefer def) {
+    XG_PDL_WAIT();
     __shared__ float buf[kChunk];
     const int nf = *nflag;
     for (int f = blockIdx.x; f < nf; f += gridDim.x) {
@@ -199,6 +202,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 __global__ void k_zero(double* a, int na, double* b, int nb, int* n) {
+    XG_PDL_WAIT();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < na) a[i] = 0.0;
     if (i < nb) b[i] = 0.0;
@@ -246,6 +250,7 @@ void launch_stats(const float* d, int rows, int cols, int policy, float* row_sta
 // per-rank slices gath[rank][slot][row] (rank r holds rank_rows[r] rows).
 __global__ void k_remote_col_means(const float* gath, int g, const int* rank_rows, int mpad, int cap,
                                    const int* cols_list, const int* n_list, int col_n, float* col_stat) {
+    XG_PDL_WAIT();
     const int n = min(*n_list, cap);
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x) {
         double s = 0.0;
@@ -260,6 +265,7 @@ __global__ void k_remote_col_means(const float* gath, int g, const int* rank_row
 // Packs D_F[:, j] of the listed columns into buf[slot][row] (rows padded to mpad).
 __global__ void k_pack_cols(const float* d, int rows, int cols, const int* cols_list, const int* n_list,
                             int cap, int mpad, float* buf) {
+    XG_PDL_WAIT();
     const int n = min(*n_list, cap);
     for (int f = blockIdx.y; f < n; f += gridDim.y)
         for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < mpad; i += gridDim.x * blockDim.x)
@@ -269,6 +275,7 @@ __global__ void k_pack_cols(const float* d, int rows, int cols, const int* cols_
 // Every rank finds the same set of columns, but atomics fill the list in any
 // order: sort it so the gathered slices line up across ranks.
 __global__ void k_sort_list(int* list, const int* n_list, int cap) {
+    XG_PDL_WAIT();
     const int n = min(*n_list, cap);
     for (int i = 1; i < n; ++i) {
         const int v = list[i];
