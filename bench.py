@@ -306,7 +306,8 @@ def run_b200(args, world, rank, local):
     t_cp = float(np.mean(gemm_ns["gemm_comp"])) * 1e-9
     # dominant kernel: the larger of the two tensor-core launches
     if t_cp >= t_df:
-        name, kops, tk = "compensation GEMM (masked-dense dr1+dr2, 4MNK tensor ops)", 4.0 * m * n * k, t_cp
+        name, kops, tk = ("compensation GEMM (one launch, masked-dense dr1 and dr2 per tile: 4MNK tensor ops)",
+                          4.0 * m * n * k, t_cp)
     else:
         name, kops, tk = "D_F GEMM (2MNK tensor ops)", 2.0 * m * n * k, t_df
     achieved = kops / tk / 1e12
@@ -316,8 +317,9 @@ def run_b200(args, world, rank, local):
             tr = json.load(f)
         key = "void k_gemm_i8_tc2<1, 4, 1>" if t_cp >= t_df else "void k_gemm_i8_tc2<1, 1, 1>"
         traffic = {"dram_bytes_per_launch": tr[key]["bytes_per_launch"],
-                   # int8 operands in, fp32 D_F / partial C in (compensation only), fp32 out
-                   "algorithmic_bytes_per_launch": m * k + k * n + (8 if t_cp >= t_df else 4) * m * n,
+                   # int8 operands in (A'q, RBq, RAq, B'q | Aq, Bq), fp32 D_F in (compensation), fp32 out
+                   "algorithmic_bytes_per_launch": (2 * (m * k + k * n) + 8 * m * n) if t_cp >= t_df
+                   else (m * k + k * n + 4 * m * n),
                    "source": "profiles/r1c_gemm_traffic.json (ncu --set full, this kernel, C3)"}
     except (OSError, KeyError, ValueError):
         pass

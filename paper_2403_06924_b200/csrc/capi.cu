@@ -365,6 +365,20 @@ void gemm_comp(Pipe& p, float* out, const float* c, float alpha, float beta) {
         g.bmap[0][0] = 2; g.bmap[0][1] = 2;
         g.rs[0][0] = r1d; g.rs[0][1] = r1s;
         g.cs[0][0] = c1; g.cs[0][1] = c1;
+        g.amap[1][0] = 3; g.amap[1][1] = 3;
+        g.bmap[1][0] = 4; g.bmap[1][1] = 5;
+        g.rs[1][0] = r2; g.rs[1][1] = r2;
+        g.cs[1][0] = c2d; g.cs[1][1] = c2s;
+        static const bool split = [] {
+            const char* e = getenv("XG_COMP_SPLIT");
+            return e && *e == '1';
+        }();
+        if (!split) {  // one launch, both terms per tile (TMEM buffers alternate by term)
+            g.dual = 1;
+            gemm_i8(EPI_ACC, ops, isb, 6, g, p.s);
+            check_launch("gemm compensate");
+            return;
+        }
         g.finalize = 0;
         gemm_i8(EPI_ACC, ops, isb, 6, g, p.s);
         check_launch("gemm compensate dr1");

@@ -65,6 +65,8 @@ struct GemmArgs {
     ScaleRef cs[3][2];
     int debug;  // probes: bit 0 skip TMA loads (MMA on stale smem), bit 1 skip epilogue work
     int finalize;  // EPI_ACC: apply the alpha/beta tail (pipeline.cpp:195-202)
+    int dual;      // pair EPI_ACC: both compensation terms per tile (term 0: amap/bmap/rs/cs[0],
+                   // out = fl(din + deq); term 1: [1], finalize), TMEM buffers alternate by term
     int group_m;   // pair kernel: tile-raster group height in 256-row units (0: default)
     int pf_dist;   // pair kernel: L2 prefetch distance in k-blocks (0: off)
 };
@@ -463,6 +465,7 @@ __global__ void __launch_bounds__(384, 1)
     // everything above overlaps the predecessor's tail under a programmatic edge
     XG_PDL_WAIT();
     const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
+    const int nterms = (EPI == EPI_ACC && args.dual) ? 2 : 1;
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================
@@ -471,13 +474,14 @@ __global__ void __launch_bounds__(384, 1)
             uint32_t phase = 0;
             const int pf = args.pf_dist;
             int it = 0;  // tiles already issued by this cluster
-            for (int t = cluster_id; t < num_tiles; t += nclusters, ++it) {
+            for (int t = cluster_id; t < num_tiles; t += nclusters, ++it)
+            for (int term = 0; term < nterms; ++term) {
                 int mb, nb;
                 tile_coords(t, num_m, num_n, gm, mb, nb);
                 const int arow = (mb * PAIRS + (int)pair) * 2 * Cfg::BM + (int)prank * Cfg::BM;
                 const int brow = nb * Cfg::BN + (int)prank * Cfg::BNH + (int)pair * (Cfg::BNH / PAIRS);
                 for (int kb = 0; kb < nkb; ++kb) {
-                    if (pf > 0 && !(args.debug & 1)) {  // L2 prefetch of the block `pf` ahead in this CTA's stream
+                    if (pf > 0 && nterms == 1 && !(args.debug & 1)) {  // L2 prefetch of the block `pf` ahead in this CTA's stream
                         const int f = it * nkb + kb + pf;
                         const int t2 = cluster_id + (f / nkb) * nclusters, kb2 = f % nkb;
                         if (t2 < num_tiles) {
@@ -492,6 +496,7 @@ __global__ void __launch_bounds__(384, 1)
                         }
                     }
                     for (int a = 0; a < NACC; ++a) {
+                        const int ai = a + term;  // operand-map index (term selects it in dual mode)
                         mbar_wait(&empty[stage], phase ^ 1);
                         uint8_t* sA = smem + stage * Cfg::STAGE_BYTES;
                         uint8_t* sB = sA + Cfg::A_BYTES;
@@ -499,11 +504,11 @@ __global__ void __launch_bounds__(384, 1)
                             if (leader) mbar_arrive(&full[stage]);
                         } else {
                             if (leader) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
-                            tma_load_2d_pair(sA, &maps.m[args.amap[a][sel]], &full[stage], kb * Cfg::BK, arow);
+                            tma_load_2d_pair(sA, &maps.m[args.amap[ai][sel]], &full[stage], kb * Cfg::BK, arow);
                             if (PAIRS == 1) {
-                                tma_load_2d_pair(sB, &maps.m[args.bmap[a][sel]], &full[stage], kb * Cfg::BK, brow);
+                                tma_load_2d_pair(sB, &maps.m[args.bmap[ai][sel]], &full[stage], kb * Cfg::BK, brow);
                             } else {
-                                tma_load_2d_pair_mc(sB + pair * (Cfg::B_BYTES / PAIRS), &maps.m[args.bmap[a][sel]],
+                                tma_load_2d_pair_mc(sB + pair * (Cfg::B_BYTES / PAIRS), &maps.m[args.bmap[ai][sel]],
                                                     &full[stage], kb * Cfg::BK, brow,
                                                     (uint16_t)((1u << rank) | (1u << (rank ^ 2u))));
                             }
@@ -524,7 +529,8 @@ __global__ void __launch_bounds__(384, 1)
             uint32_t phase = 0;
             int buf = 0;
             uint32_t bphase = 0;
-            for (int t = cluster_id; t < num_tiles; t += nclusters) {
+            for (int t = cluster_id; t < num_tiles; t += nclusters)
+            for (int term = 0; term < nterms; ++term) {
                 mbar_wait(&tempty[buf], bphase ^ 1);
                 tc_fence_after();
                 const uint32_t dbase = tmem_base + buf * Cfg::ACC_COLS;
@@ -570,7 +576,10 @@ __global__ void __launch_bounds__(384, 1)
         const int sw = lane & 7;  // 128B swizzle: chunk k of row `lane` sits at k ^ (lane & 7)
         int buf = 0;
         uint32_t bphase = 0;
-        for (int t = cluster_id; t < num_tiles; t += nclusters) {
+        for (int t = cluster_id; t < num_tiles; t += nclusters)
+        for (int term = 0; term < nterms; ++term) {
+            const int ts = term;  // scale / operand index of this accumulator (0 unless dual)
+            const int fin = nterms == 2 ? term : args.finalize;
             int mb, nb;
             tile_coords(t, num_m, num_n, gm, mb, nb);
             const int rowbase = (mb * PAIRS + (int)pair) * 2 * Cfg::BM + (int)prank * Cfg::BM + q * 32;
@@ -579,7 +588,9 @@ __global__ void __launch_bounds__(384, 1)
             const int colbase = nb * Cfg::BN + half * (Cfg::BN / 2);
             const int nchunk = (args.debug & 2) ? 0 : min(Cfg::BN / 2 / 32, (args.N - colbase + 31) / 32);
             if (Cfg::LOADS_DIN && lane == 0 && nchunk > 0) {  // D_F chunk 0 while the MMA still runs
-                bulk_wait_read<0>();
+                // dual term 1 reads back what term 0 stored: wait for the stores themselves
+                if (term) bulk_wait<0>(), fence_proxy_async();
+                else bulk_wait_read<0>();
                 mbar_expect_tx(&mybar[0], Cfg::STG_BYTES);
                 tma_load_2d(stg[0], &emaps.din, &mybar[0], colbase, rowbase);
             }
@@ -587,7 +598,7 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_after();
             double r0 = 1.0, r1 = 1.0;
             if (row_ok) {
-                r0 = args.rs[0][sel].at(row);
+                r0 = args.rs[ts][sel].at(row);
                 if (NACC > 1) r1 = args.rs[1][sel].at(row);
             }
             const float2 i0 = ff_recip(r0), i1 = ff_recip(r1);
@@ -605,7 +616,7 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 // column reciprocals of this chunk, broadcast through shared memory
                 const int mycol = min(col0 + lane, args.N - 1);
-                scw[lane] = ff_recip(args.cs[0][sel].at(mycol));
+                scw[lane] = ff_recip(args.cs[ts][sel].at(mycol));
                 if (NACC > 1) scw[32 + lane] = ff_recip(args.cs[1][sel].at(mycol));
                 uint32_t acc[NACC][32];
 #pragma unroll
@@ -661,7 +672,7 @@ __global__ void __launch_bounds__(384, 1)
                     for (int j = 0; j < 32; ++j)
                         res[j] = __fadd_rn(res[j], dq_ff24((int32_t)acc[0][j], i0, scw[j], sm, 1u << j));
                     if (sm) {  // rare: exact redo of the flagged elements
-                        const ScaleRef c0 = args.cs[0][sel];
+                        const ScaleRef c0 = args.cs[ts][sel];
                         const float* rowf = tile + lane * 32;
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
@@ -670,7 +681,7 @@ __global__ void __launch_bounds__(384, 1)
                                                    dq_slow((int32_t)acc[0][j], i0, scw[j], r0,
                                                            c0.at(min(col0 + j, args.N - 1))));
                     }
-                    if (args.finalize) {  // pipeline.cpp:195-202 (non-fused)
+                    if (fin) {  // pipeline.cpp:195-202 (non-fused)
                         const float* cin = args.c_in + (int64_t)row * args.N + col0;
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
