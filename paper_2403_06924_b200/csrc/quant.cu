@@ -1086,251 +1086,6 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows_async(const QuantRowsAr
     if (bad && a.nonfinite) atomicOr(a.nonfinite, bad);
 }
 
-// K3, A side (Nearest): RAq and A'q from a streamed row ring; the per-row
-// dequant table for row i+1 is built while row i is processed.
-__global__ void __launch_bounds__(kThreads) k_select_rows_async(const SelectArgs a) {
-    XG_PDL_WAIT();
-    XG_EXIT_IF_NONFINITE(a.nonfinite);
-    extern __shared__ float4 dyn_smem[];
-    float* ring = reinterpret_cast<float*>(dyn_smem);
-    __shared__ uint64_t full[kRowSlots];
-    __shared__ float lut[2][256];
-    __shared__ float red[kThreads / 32];
-    __shared__ unsigned long long redu[kThreads / 32];
-    const int qmax = quant_max(a.bits);
-    const float qmaxf = (float)qmax;
-    const uint32_t adj0 = smem_u32(&lut[0][0]) + 4u * (uint32_t)qmax - 4u * 0x4B400000u;
-    const double lam_r = compute_scale((double)__uint_as_float(*a.rmax), a.bits);
-    const float lam_r32 = __double2float_rn(lam_r);
-    const double lam_t = a.vec ? 0.0 : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
-    const double scale_other =
-        a.do_select && a.policy == kMin ? compute_scale((double)__uint_as_float(*a.other_max), a.bits)
-                                        : 1.0;
-    const uint32_t bytes = (uint32_t)a.cols * 4u;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kRowSlots; ++i) mbar_init(&full[i], 1);
-        fence_mbar_init();
-        for (int i = 0; i < kRowSlots; ++i) {
-            const int r = blockIdx.x + i * gridDim.x;
-            if (r < a.rows) issue_row(ring + (size_t)i * a.cols, a.x + (int64_t)r * a.ld, bytes, &full[i]);
-        }
-    }
-    if ((int)blockIdx.x < a.rows && threadIdx.x <= 2 * qmax)
-        lut[0][threadIdx.x] = dequant_value((int)threadIdx.x - qmax, a.vec ? a.lam[blockIdx.x] : lam_t);
-    __syncthreads();
-    unsigned cnt = 0;
-    float ret = 0.0f;
-    for (int it = 0;; ++it) {
-        const int r = blockIdx.x + it * gridDim.x;
-        if (r >= a.rows) break;
-        const int rn1 = r + gridDim.x;
-        if (rn1 < a.rows && threadIdx.x <= 2 * qmax)
-            lut[(it + 1) & 1][threadIdx.x] = dequant_value((int)threadIdx.x - qmax, a.vec ? a.lam[rn1] : lam_t);
-        const int slot = it % kRowSlots;
-        const float* row = ring + (size_t)slot * a.cols;
-        const double lam = a.vec ? a.lam[r] : lam_t;
-        const float lam32 = __double2float_rn(lam);
-        const bool exact = !(lam32 <= FLT_MAX) || !(lam_r32 <= FLT_MAX);
-        const float tf = a.do_select
-                             ? float_above(threshold_of(a.policy, a.thr_m, a.stat[r], scale_other, a.cols))
-                             : __int_as_float(0x7f800000);
-        const uint32_t adj = adj0 + (uint32_t)(it & 1) * 1024u;
-        int8_t* rq_row = a.rq + (int64_t)r * a.ldq;
-        int8_t* rd_row = a.red + (int64_t)r * a.ldq;
-        mbar_wait(&full[slot], (it / kRowSlots) & 1);
-        float lmax = 0.0f;
-#pragma unroll 2
-        for (int c = threadIdx.x * 4; c < a.cols; c += kThreads * 4) {
-            const float4 f = *reinterpret_cast<const float4*>(row + c);
-            const float x[4] = {f.x, f.y, f.z, f.w};
-            uint32_t pq, pr;
-            select_quad_n<2>(x, adj, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, pq, pr, cnt, lmax);
-            *reinterpret_cast<uint32_t*>(rq_row + c) = pq;
-            if (a.do_select) *reinterpret_cast<uint32_t*>(rd_row + c) = pr;
-        }
-        ret = fmaxf(ret, lmax >= tf ? lmax : 0.0f);
-        __syncthreads();  // slot + lut[it&1] free, lut[(it+1)&1] complete
-        if (threadIdx.x == 0) {
-            const int rn = blockIdx.x + (it + kRowSlots) * gridDim.x;
-            if (rn < a.rows) {
-                fence_proxy_async();
-                issue_row(ring + (size_t)slot * a.cols, a.x + (int64_t)rn * a.ld, bytes, &full[slot]);
-            }
-        }
-    }
-    if (a.do_select) {
-        const unsigned long long c64 = block_sum_u64(cnt, redu);
-        ret = block_max(ret, red);
-        if (threadIdx.x == 0) {
-            if (c64) atomicAdd(a.nnz, c64);
-            atomicMax(a.retmax, fbits(ret));
-        }
-    }
-}
-
-
-// B side with TMA 2-D tiles: 32 columns x 128 rows of fp32 per stage, a 4-deep
-// ring, persistent CTAs walking (column strip, K chunk) work items.  Lane l owns
-// column l; warp w rows [16w, 16w+16) of each tile, read conflict-free from the
-// TMA's dense [128][32] layout.  Per-strip dequant tables lut[q][col]
-// (column-interleaved: lane l always hits bank l) are rebuilt per item.
-constexpr int kCT = 32, kCR = 128, kCSlots = 4, kCW = kCR / 4 + 1;
-constexpr int kCChunk = 16;  // sub-tiles (of 128 rows) per work item
-constexpr int kColAsyncSmem = kCSlots * kCT * kCR * 4 + 256 * kCT * 4 + 1024;  // + alignment slack
-
-struct ColItem {
-    int n0, k0;
-};
-__device__ __forceinline__ ColItem col_item(int item, int nstrips) {
-    return {(item % nstrips) * kCT, (item / nstrips) * kCR * kCChunk};
-}
-
-__device__ __forceinline__ void store_T32(const uint32_t (*t)[kCW], int8_t* dst, int64_t ldq, int n0, int k0,
-                                          int cols, int rows) {
-    const int r = threadIdx.x >> 3;   // 0..31
-    const int seg = threadIdx.x & 7;  // 16-byte segment
-    if (n0 + r >= cols) return;
-    const uint32_t w0 = t[r][seg * 4], w1 = t[r][seg * 4 + 1], w2 = t[r][seg * 4 + 2], w3 = t[r][seg * 4 + 3];
-    int8_t* d = dst + (int64_t)(n0 + r) * ldq + k0 + seg * 16;
-    const int kval = rows - (k0 + seg * 16);
-    if (kval >= 16) {
-        *reinterpret_cast<uint4*>(d) = make_uint4(w0, w1, w2, w3);
-    } else if (kval > 0) {
-        const uint32_t w[4] = {w0, w1, w2, w3};
-        for (int j = 0; j < kval; ++j) d[j] = (int8_t)(w[j >> 2] >> (8 * (j & 3)));
-    }
-}
-
-template <bool SELECT>
-__global__ void __launch_bounds__(kThreads)
-    k_cols_T_async(const __grid_constant__ CUtensorMap tmap, const QuantColsArgs qa, const SelectArgs sa) {
-    XG_PDL_WAIT();
-    XG_EXIT_IF_NONFINITE(SELECT ? sa.nonfinite : qa.nonfinite);
-    extern __shared__ float4 dyn_smem[];
-    // TMA destinations need 128-byte alignment
-    float* ring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
-    float(*lut)[kCT] = reinterpret_cast<float(*)[kCT]>(ring + kCSlots * kCT * kCR);
-    __shared__ uint64_t full[kCSlots];
-    __shared__ uint32_t t0[kCT][kCW];
-    __shared__ uint32_t t1[kCT][kCW];
-    __shared__ float red[kThreads / 32];
-    __shared__ unsigned long long redu[kThreads / 32];
-    const int rows = SELECT ? sa.rows : qa.rows, cols = SELECT ? sa.cols : qa.cols;
-    const int bits = SELECT ? sa.bits : qa.bits;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qmax = quant_max(bits);
-    const float qmaxf = (float)qmax;
-    const int nstrips = (cols + kCT - 1) / kCT;
-    const int nchunks = (rows + kCR * kCChunk - 1) / (kCR * kCChunk);
-    const int nitems = nstrips * nchunks;
-    const int ntiles = ((nitems - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * kCChunk;
-    // per-tensor scalars
-    double lam_r = 0.0, lam_t = 0.0, so = 1.0;
-    if (SELECT) {
-        lam_r = compute_scale((double)__uint_as_float(*sa.rmax), bits);
-        lam_t = sa.vec ? 0.0 : compute_scale((double)__uint_as_float(*sa.tensor_max), bits);
-        if (sa.do_select && sa.policy == kMin) so = compute_scale((double)__uint_as_float(*sa.other_max), bits);
-    } else if (!qa.per_col) {
-        lam_t = compute_scale((double)__uint_as_float(*qa.tensor_max), bits);
-    }
-    const float lam_r32 = __double2float_rn(lam_r);
-    auto issue = [&](int g, int slot) {
-        const ColItem ci = col_item((int)blockIdx.x + (g / kCChunk) * (int)gridDim.x, nstrips);
-        mbar_expect_tx(&full[slot], kCT * kCR * 4);
-        tma_load_2d(ring + slot * kCT * kCR, &tmap, &full[slot], ci.n0, ci.k0 + (g % kCChunk) * kCR);
-    };
-    if (threadIdx.x == 0) {
-        tma_prefetch(&tmap);
-        for (int i = 0; i < kCSlots; ++i) mbar_init(&full[i], 1);
-        fence_mbar_init();
-        for (int g = 0; g < kCSlots && g < ntiles; ++g) issue(g, g);
-    }
-    __syncthreads();
-    const uint32_t adj_base = smem_u32(&lut[0][0]) + 4u * lane + 128u * (uint32_t)qmax - 128u * 0x4B400000u;
-    float rm = 0.0f, ret = 0.0f;
-    unsigned cnt = 0;
-    int g = 0;
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-        const ColItem ci = col_item(item, nstrips);
-        const int n = ci.n0 + lane;
-        const int nc = min(n, cols - 1);
-        double lam;
-        if (SELECT) lam = sa.vec ? sa.lam[nc] : lam_t;
-        else lam = qa.per_col ? compute_scale((double)__uint_as_float(qa.colmax[nc]), bits) : lam_t;
-        if (!SELECT && qa.per_col && qa.lam_out && ci.k0 == 0 && n < cols) qa.lam_out[n] = lam;
-        const float lam32 = __double2float_rn(lam);
-        const bool exact = !(lam32 <= FLT_MAX) || (SELECT && !(lam_r32 <= FLT_MAX));
-        float tf = __int_as_float(0x7f800000);
-        if (SELECT && sa.do_select && n < cols)
-            tf = float_above(threshold_of(sa.policy, sa.thr_m, sa.stat[nc], so, rows));
-        {   // per-strip dequant tables: thread builds column `lane` for q in [w*32, w*32+32)
-            const double inv = __ddiv_rn(1.0, lam);
-            for (int e = w * 32; e < w * 32 + 32; ++e)
-                if (e <= 2 * qmax) lut[e][lane] = dequant_fast(e - qmax, inv, lam);
-        }
-        __syncthreads();
-        for (int sub = 0; sub < kCChunk; ++sub, ++g) {
-            const int slot = g % kCSlots;
-            const int k0 = ci.k0 + sub * kCR;
-            mbar_wait(&full[slot], (g / kCSlots) & 1);
-            const float* tile = ring + slot * kCT * kCR;
-            float lmax = 0.0f;
-#pragma unroll
-            for (int gq = 0; gq < 4; ++gq) {
-                float x[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) x[e] = tile[(16 * w + 4 * gq + e) * kCT + lane];
-                if (SELECT) {
-                    uint32_t pq, pr;
-                    select_quad_n<7>(x, adj_base, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, pq, pr, cnt, lmax);
-                    t0[lane][4 * w + gq] = pq;
-                    t1[lane][4 * w + gq] = pr;
-                } else {
-                    uint32_t u[4];
-                    float dmax = 0.0f;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) u[e] = qn(x[e], lam32, dmax);
-                    if (exact || !(dmax < 0.4999f)) {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(x[e], lam, qmaxf, kNearest));
-                    }
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[e], lds_f32((u[e] << 7) + adj_base))));
-                    t0[lane][4 * w + gq] = pack4u(u[0], u[1], u[2], u[3]);
-                }
-            }
-            if (SELECT) ret = fmaxf(ret, lmax >= tf ? lmax : 0.0f);
-            __syncthreads();  // slot consumed, staging complete
-            if (threadIdx.x == 0 && g + kCSlots < ntiles) {
-                fence_proxy_async();
-                issue(g + kCSlots, slot);
-            }
-            if (k0 < rows) {
-                if (SELECT) {
-                    store_T32(t0, sa.rq, sa.ldq, ci.n0, k0, cols, rows);
-                    if (sa.do_select) store_T32(t1, sa.red, sa.ldq, ci.n0, k0, cols, rows);
-                } else {
-                    store_T32(t0, qa.qT, qa.ldq, ci.n0, k0, cols, rows);
-                }
-            }
-            __syncthreads();  // staging reusable
-        }
-    }
-    if (SELECT) {
-        if (sa.do_select) {
-            const unsigned long long c64 = block_sum_u64(cnt, redu);
-            ret = block_max(ret, red);
-            if (threadIdx.x == 0) {
-                if (c64) atomicAdd(sa.nnz, c64);
-                atomicMax(sa.retmax, fbits(ret));
-            }
-        }
-    } else {
-        rm = block_max(rm, red);
-        if (threadIdx.x == 0 && qa.rmax) atomicMax(qa.rmax, fbits(rm));
-    }
-}
-
 // ============================================================ row kernels, r4
 // One 128-thread CTA (4 warps) per row, 8 CTAs per SM.  Compared with the
 // 256-thread ring kernels above: one CTA barrier per row instead of three (the
@@ -1362,8 +1117,8 @@ __device__ __forceinline__ void build_row_lut(float* lut, double lam, int qmax) 
     }
 }
 
-template <int U>
-__global__ void __launch_bounds__(kRT, kRCtasPerSM) k_select_rows_r4(const SelectArgs a) {
+template <int U, int MINB = kRCtasPerSM>
+__global__ void __launch_bounds__(kRT, MINB) k_select_rows_r4(const SelectArgs a) {
     XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
     __shared__ float lut[2][256];
@@ -1430,8 +1185,8 @@ __global__ void __launch_bounds__(kRT, kRCtasPerSM) k_select_rows_r4(const Selec
 
 // K1, A side: the row lives in registers (VPT float4 per thread), absmax ->
 // lambda -> table -> quantise -> residual max; two CTA barriers per row.
-template <int VPT>
-__global__ void __launch_bounds__(kRT, 4) k_quant_rows_r4(const QuantRowsArgs a) {
+template <int VPT, int MINB = 4>
+__global__ void __launch_bounds__(kRT, MINB) k_quant_rows_r4(const QuantRowsArgs a) {
     XG_PDL_WAIT();
     __shared__ float lut[2][256];
     __shared__ float red[2][kRT / 32];
@@ -1789,7 +1544,11 @@ void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
                          ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
     if (a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 8192 && r4_enabled()) {
         const int vpt = (a.cols + kRT * 4 - 1) / (kRT * 4);
-        const int cap = kNumSMs * (a.co_share > 0 ? a.co_share : 4);
+        static const int qctas = [] {
+            const char* e = getenv("XG_R4Q");  // tuning aid: CTAs per SM
+            return e ? atoi(e) : 4;
+        }();
+        const int cap = kNumSMs * (a.co_share > 0 ? a.co_share : qctas);
         const int g = a.rows < cap ? a.rows : cap;
         if (vpt <= 2) k_quant_rows_r4<2><<<g, kRT, 0, s>>>(a);
         else if (vpt <= 4) k_quant_rows_r4<4><<<g, kRT, 0, s>>>(a);
@@ -1818,11 +1577,6 @@ void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
 }
 
 
-int col_async_grid(int rows, int cols) {
-    const int items = ((cols + kCT - 1) / kCT) * ((rows + kCR * kCChunk - 1) / (kCR * kCChunk));
-    const int g = kNumSMs * 2;
-    return items < g ? items : g;
-}
 
 // Column-kernel shape (warps per CTA, ring slots per warp, CTAs per SM);
 // XG_COLW=WWxSLOTSxCTAS picks a compiled variant (tuning aid).
@@ -1869,14 +1623,6 @@ void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {
             return;
         }
     }
-    if (a.rounding == kNearest && async_enabled() && a.rows >= 512) {
-        alignas(64) CUtensorMap tm;
-        if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kCT, kCR)) {
-            set_dyn_smem(k_cols_T_async<false>, kColAsyncSmem);
-            k_cols_T_async<false><<<col_async_grid(a.rows, a.cols), kThreads, kColAsyncSmem, s>>>(tm, a, SelectArgs{});
-            return;
-        }
-    }
     dim3 grid((a.cols + kTN - 1) / kTN, (a.rows + kColTileRows - 1) / kColTileRows);
     if (a.rounding == kNearest) {
         set_dyn_smem(k_quant_cols_T_fast, kLutBytes);
@@ -1891,16 +1637,18 @@ void launch_select_rows(const SelectArgs& a, cudaStream_t s) {
     const bool aligned = (a.ld % 4 == 0) && (a.ldq % 4 == 0) && (a.cols % 4 == 0) &&
                          ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
     if (!a.fix_mode && a.rounding == kNearest && aligned && a.cols >= 512 && r4_enabled()) {
-        const int cap = kNumSMs * (a.co_share > 0 ? a.co_share : kRCtasPerSM);
+        // XG_R4SEL=UxCTAS tuning aid (U loads in flight per thread, CTAs per SM)
+        static const int2 cfg = [] {
+            int2 c = make_int2(4, kRCtasPerSM);
+            if (const char* e = getenv("XG_R4SEL")) sscanf(e, "%dx%d", &c.x, &c.y);
+            return c;
+        }();
+        const int cap = kNumSMs * (a.co_share > 0 ? a.co_share : cfg.y);
         const int g = a.rows < cap ? a.rows : cap;
-        k_select_rows_r4<4><<<g, kRT, 0, s>>>(a);
-        return;
-    }
-    if (!a.fix_mode && a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 16384 &&
-        async_enabled()) {
-        const int bytes = kRowSlots * a.cols * 4;
-        set_dyn_smem(k_select_rows_async, bytes);
-        k_select_rows_async<<<async_grid(a.rows, bytes), kThreads, bytes, s>>>(a);
+        if (cfg.x == 2) k_select_rows_r4<2, 8><<<g, kRT, 0, s>>>(a);
+        else if (cfg.x == 8) k_select_rows_r4<8, 6><<<g, kRT, 0, s>>>(a);
+        else if (cfg.y >= 12) k_select_rows_r4<4, 12><<<g, kRT, 0, s>>>(a);
+        else k_select_rows_r4<4><<<g, kRT, 0, s>>>(a);
         return;
     }
     if (a.fix_mode) k_fix_rows<<<grid_rows(a.rows), kThreads, 0, s>>>(a);
@@ -1920,14 +1668,6 @@ void launch_select_cols_T(const SelectArgs& a, cudaStream_t s) {
         alignas(64) CUtensorMap tm;
         if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) {
             launch_cols_any<true>(tm, QuantColsArgs{}, a, a.rows, a.cols, a.co_share, s);
-            return;
-        }
-    }
-    if (a.rounding == kNearest && async_enabled() && a.rows >= 512) {
-        alignas(64) CUtensorMap tm;
-        if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kCT, kCR)) {
-            set_dyn_smem(k_cols_T_async<true>, kColAsyncSmem);
-            k_cols_T_async<true><<<col_async_grid(a.rows, a.cols), kThreads, kColAsyncSmem, s>>>(tm, QuantColsArgs{}, a);
             return;
         }
     }
