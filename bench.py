@@ -187,7 +187,9 @@ def run_reference(args, world, rank):
         a = (z / np.sqrt((rng.standard_normal((m, k), dtype=np.float32) ** 2 * 3) / 3)).astype(np.float32)
         b = a.T.copy()
         thr = args.threshold or 0.01
-    rows = args.ref_rows
+    # larger slabs than the single-core baseline: the reference redoes all of
+    # B's quantisation per call, which a 16-row slab would over-weight
+    rows = args.ref_rows if args.ref_rows_set else 64
     vals = []
     for _ in range(args.warmup):
         pass  # CPU: no warm-up effect worth paying minutes for
@@ -465,7 +467,8 @@ def main():
     ap.add_argument("--n", type=int, default=N_DEFAULT)
     ap.add_argument("--k", type=int, default=K_DEFAULT)
     ap.add_argument("--threshold", type=float, default=None)
-    ap.add_argument("--ref-rows", type=int, default=16)
+    ap.add_argument("--ref-rows", type=int, default=None,
+                    help="row slab of the CPU samples (default 16 for cpu_baseline, 64 for --impl reference)")
     ap.add_argument("--ref-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true",
@@ -473,6 +476,9 @@ def main():
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded pipeline even at N=1 (needs torchrun / a process group)")
     args = ap.parse_args()
+    args.ref_rows_set = args.ref_rows is not None
+    if args.ref_rows is None:
+        args.ref_rows = 16
     world, rank, local = _dist_init()
     if args.impl == "reference":
         run_reference(args, world, rank)
