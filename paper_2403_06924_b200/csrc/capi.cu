@@ -86,16 +86,19 @@ struct Scratch {
     cudaStream_t s;
     std::vector<void*> ptrs;
     explicit Scratch(cudaStream_t s_) : s(s_) {
-        static bool init = false;
-        if (!init) {
-            int dev = 0;
-            cudaGetDevice(&dev);
+        // once per device: keep freed scratch cached in the pool
+        static std::mutex mu;
+        static bool init[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(mu);
+        if (!init[dev & 63]) {
             cudaMemPool_t pool;
             if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
                 uint64_t thr = ~0ull;
                 cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
             }
-            init = true;
+            init[dev & 63] = true;
         }
     }
     template <class T>

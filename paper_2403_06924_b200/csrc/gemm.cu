@@ -78,11 +78,8 @@ void run(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, c
     for (int i = 0; i < nops; ++i) encode(&maps.m[i], ops[i], args.K, is_b[i] ? BN : Cfg::BM);
     for (int i = nops; i < kMaxMaps; ++i) maps.m[i] = maps.m[0];
     auto kern = k_gemm_i8_tc<BN, NACC, EPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-        attr_set = true;
-    }
+    // function attributes are per device: set them for every device that runs the kernel
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     const int tiles = ((args.M + Cfg::BM - 1) / Cfg::BM) * ((args.N + BN - 1) / BN);
     const int grid = tiles < sm_count() ? tiles : sm_count();
     kern<<<grid, 256, Cfg::SMEM_BYTES, s>>>(maps, args);
@@ -96,11 +93,7 @@ void run2(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, 
     for (int i = 0; i < nops; ++i) encode(&maps.m[i], ops[i], args.K, is_b[i] ? 128 / PAIRS : 128);
     for (int i = nops; i < kMaxMaps; ++i) maps.m[i] = maps.m[0];
     auto kern = k_gemm_i8_tc2<NACC, EPI, PAIRS>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-        attr_set = true;
-    }
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     const int csize = 2 * PAIRS;
     const int tiles = ((args.M + 256 * PAIRS - 1) / (256 * PAIRS)) * ((args.N + 255) / 256);
     cudaLaunchConfig_t cfg = {};
@@ -116,14 +109,16 @@ void run2(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, 
     cfg.numAttrs = 1;
     // persistent grid: only as many clusters as can be co-resident (4-CTA
     // clusters cannot use every SM), so no cluster waits for a second wave
+    // co-resident clusters, queried once per process (all devices are the same part)
+    static std::once_flag once;
     static int max_clusters = 0;
-    if (!max_clusters) {
+    std::call_once(once, [&] {
         cfg.gridDim = dim3(csize * 512);
         if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters <= 0) {
             cudaGetLastError();
             max_clusters = sm_count() / csize;
         }
-    }
+    });
     cfg.gridDim = dim3(csize * (tiles < max_clusters ? tiles : max_clusters));
     static const int env_gm = [] { const char* e = getenv("XG_GEMM_GROUP"); return e ? atoi(e) : 0; }();
     static const int env_pf = [] { const char* e = getenv("XG_GEMM_PF"); return e ? atoi(e) : -1; }();
