@@ -325,6 +325,26 @@ def run_b200(args, world, rank, local):
                    "source": "profiles/r1c_gemm_traffic.json (ncu --set full, this kernel, C3)"}
     except (OSError, KeyError, ValueError):
         pass
+    # live reference point for the INT8 denominator (MEASURED_PEAKS.json has
+    # bf16 only): cuBLASLt int8 GEMM (torch._int_mm, s32 out, no epilogue) at
+    # the same shape; library call for context, never on the product path
+    cublaslt = None
+    try:
+        ia = torch.randint(-127, 128, (m, k), dtype=torch.int8, device="cuda")
+        ib = torch.randint(-127, 128, (n, k), dtype=torch.int8, device="cuda").t()
+        for _ in range(3):
+            torch._int_mm(ia, ib)
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(10):
+            torch._int_mm(ia, ib)
+        c1.record()
+        torch.cuda.synchronize()
+        cublaslt = 2.0 * m * n * k / (c0.elapsed_time(c1) / 10 * 1e-3) / 1e12
+        del ia, ib
+    except Exception:  # noqa: BLE001
+        pass
     cpu = None
     if not args.no_cpu_baseline:
         v, dt, kind = cpu_baseline_sample(a.cpu().numpy(), b.cpu().numpy(), thr, args.ref_rows, 1)
@@ -344,7 +364,9 @@ def run_b200(args, world, rank, local):
                      "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
                      "traffic": traffic,
                      "peak_source": f"2 x bf16_tflops ({bf16}) of MEASURED_PEAKS.json ({src}); INT8 dense = 2x bf16 on B200",
-                     "gemm_df_ms": t_df * 1e3, "gemm_comp_ms": t_cp * 1e3},
+                     "gemm_df_ms": t_df * 1e3, "gemm_comp_ms": t_cp * 1e3,
+                     "cublaslt_int8_tflops": cublaslt,
+                     "frac_of_cublaslt_int8": (achieved / cublaslt) if cublaslt else None},
         "clocks": clk.summary(),
         "gpu_launches": launches,
         "stage_ns": {kk: int(vv) for kk, vv in r.timings.items()},  # last timed call
