@@ -12,6 +12,8 @@ hdr = next(r for r in rows if "Kernel Name" in r)
 data = [dict(zip(hdr, r)) for r in rows[rows.index(hdr) + 1:] if len(r) == len(hdr)]
 agg = collections.OrderedDict()
 for d in data:
+    if "xg::" not in d["Kernel Name"] and "k_" not in d["Kernel Name"]:
+        continue  # library kernels of the bench's reference points (cuBLASLt, torch RNG)
     agg.setdefault(d["Kernel Name"].split("(")[0][-48:], []).append(float(d["Metric Value"]))
 steps = next((len(v) for n, v in agg.items() if "k_dispatch" in n), None) or min(len(v) for v in agg.values())
 tot = 0.0
