@@ -111,3 +111,19 @@ def test_sharded_remote_exact_means_widened():
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, XG_STATS_WIDEN="20"),
                        capture_output=True, text=True)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+def test_sharded_nccl_graph_replay():
+    """One-rank NCCL process group (torchrun): xigemm_sharded's eager first
+    call and its CUDA-graph replays (stages + NCCL collectives captured) equal
+    the single-GPU result bit for bit."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(root, "tools", "shard_graph_check.py")],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "equal single-GPU: True" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
