@@ -277,6 +277,35 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
     }
 }
 
+// VectorWise pieces of K1 for the host-buffer path, which quantises A in row
+// chunks as they arrive over PCIe (per-row scales make rows independent).
+void quantize_a_rows(Pipe& p, const float* a, int r0, int rows) {
+    using namespace xg;
+    QuantRowsArgs qa{};
+    qa.x = a + (int64_t)r0 * p.K; qa.rows = rows; qa.cols = p.K; qa.ld = p.K;
+    qa.bits = p.cfg->bits; qa.rounding = p.cfg->rounding;
+    qa.q = p.aq + (int64_t)r0 * p.ldk; qa.ldq = p.ldk;
+    qa.rmax = &p.sc->maxRA; qa.nonfinite = &p.sc->nonfinite;
+    qa.per_row = 1; qa.lam_out = p.la + r0; qa.gmax = &p.sc->maxA;
+    launch_quant_rows(qa, p.s);
+    check_launch("quantize A rows");
+}
+
+void quantize_b_vw(Pipe& p, const float* b) {
+    using namespace xg;
+    QuantColsArgs qb{};
+    qb.x = b; qb.rows = p.K; qb.cols = p.N; qb.ld = p.N;
+    qb.bits = p.cfg->bits; qb.rounding = p.cfg->rounding;
+    qb.qT = p.bqT; qb.ldq = p.ldk; qb.rmax = &p.sc->maxRB;
+    qb.nonfinite = &p.sc->nonfinite;
+    ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, p.s), "memset");
+    launch_absmax_cols(b, p.K, p.N, p.N, p.colmax, &p.sc->maxB, &p.sc->nonfinite, p.s);
+    check_launch("absmax B cols");
+    qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb;
+    launch_quant_cols_T(qb, p.s);
+    check_launch("quantize B");
+}
+
 void gemm_df(Pipe& p, float* out) {
     using namespace xg;
     KOperand ops[2] = {{p.aq, p.M, p.ldk}, {p.bqT, p.N, p.ldk}};
@@ -1567,12 +1596,116 @@ cudaStream_t host_stream() {
 }
 }  // namespace
 
+// Host-buffer pipeline with the PCIe transfers overlapped (VectorWise):
+//   copy stream: B, then A in row chunks, then C;
+//   compute stream: K1 of B once it has arrived, K1 of each A chunk as it
+//   arrives (per-row scales), then D_F GEMM, statistics, selection (they need
+//   all of A), then the compensation GEMM in the same row chunks;
+//   D2H stream: each chunk of the result as soon as its compensation is done.
+// Only H2D(A, B) + the non-overlappable middle + D2H remain on the critical
+// path (the PCIe link is full-duplex, ~52 GB/s each way on this box).
+void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, float alpha, float beta, int M,
+                       int K, int N, const xg_config* cfg, int reduce, float* out_h, xg_report* rep) {
+    req(K <= xg::gemm_max_inner(cfg->bits), "gemm_int: inner dimension permits 32-bit overflow");
+    cudaStream_t s = host_stream();
+    thread_local cudaStream_t s_in = nullptr, s_out = nullptr;
+    thread_local cudaEvent_t ev[24];
+    if (!s_in) {
+        ck(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "stream");
+        ck(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "stream");
+        for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    const int64_t ldk = pad16(K);
+    Scratch S(s);
+    float* da = S.get<float>((int64_t)M * K);
+    float* db = S.get<float>((int64_t)K * N);
+    float* dc = c_h ? S.get<float>((int64_t)M * N) : nullptr;
+    float* dout = S.get<float>((int64_t)M * N);
+    PipeWs w;
+    alloc_ws(w, M, N, ldk, [&](auto* tag, int64_t cnt) { return S.get<std::remove_pointer_t<decltype(tag)>>(cnt); });
+    // the workspace comes from the stream-ordered pool of `s`: the copy streams wait for it
+    ck(cudaEventRecord(ev[0], s), "event");
+    ck(cudaStreamWaitEvent(s_in, ev[0], 0), "wait");
+    ck(cudaStreamWaitEvent(s_out, ev[0], 0), "wait");
+    const int nch = M >= 4096 ? 4 : 2;
+    const int rc = ((M + nch - 1) / nch + 255) / 256 * 256;
+    int r0s[5], nchk = 0;
+    for (int r = 0; r < M && nchk < 4; r += rc) r0s[nchk++] = r;
+    r0s[nchk] = M;
+    // H2D: B, A chunks, C
+    ck(cudaMemcpyAsync(db, b_h, sizeof(float) * (size_t)K * N, cudaMemcpyHostToDevice, s_in), "h2d");
+    ck(cudaEventRecord(ev[1], s_in), "event");
+    for (int i = 0; i < nchk; ++i) {
+        const size_t off = (size_t)r0s[i] * K, cnt = (size_t)(r0s[i + 1] - r0s[i]) * K;
+        ck(cudaMemcpyAsync(da + off, a_h + off, sizeof(float) * cnt, cudaMemcpyHostToDevice, s_in), "h2d");
+        ck(cudaEventRecord(ev[2 + i], s_in), "event");
+    }
+    if (c_h) {
+        ck(cudaMemcpyAsync(dc, c_h, sizeof(float) * (size_t)M * N, cudaMemcpyHostToDevice, s_in), "h2d");
+        ck(cudaEventRecord(ev[6], s_in), "event");
+    }
+    // compute
+    PipeCall q{da, db, dc, alpha, beta, M, K, N, *cfg, reduce, dout};
+    Pipe p;
+    p.M = M; p.K = K; p.N = N; p.cfg = &q.cfg; p.s = s;
+    p.ldk = ldk;
+    p.vw = true;
+    p.sc = w.sc;
+    p.aq = w.aq; p.raq = w.raq; p.ared = w.ared;
+    p.bqT = w.bqT; p.rbqT = w.rbqT; p.bredT = w.bredT;
+    p.la = w.la; p.lb = w.lb; p.colmax = w.colmax;
+    ck(cudaMemsetAsync(p.sc, 0, sizeof(xg::DevScalars), s), "memset");
+    ck(cudaStreamWaitEvent(s, ev[1], 0), "wait");
+    quantize_b_vw(p, db);
+    for (int i = 0; i < nchk; ++i) {
+        ck(cudaStreamWaitEvent(s, ev[2 + i], 0), "wait");
+        quantize_a_rows(p, da, r0s[i], r0s[i + 1] - r0s[i]);
+    }
+    if (c_h) {
+        ck(cudaStreamWaitEvent(s, ev[6], 0), "wait");
+        xg::finite_max(dc, (int64_t)M * N, &p.sc->retB /*scratch, reset below*/, &p.sc->nonfinite, s);
+        check_launch("finite C");
+        ck(cudaMemsetAsync(&p.sc->retB, 0, sizeof(uint32_t), s), "memset");
+    }
+    xg::launch_lambdas(p.sc, cfg->bits, s);
+    check_launch("lambdas");
+    enqueue_stage(1, q, w, nullptr, s);  // D_F GEMM
+    enqueue_stage(2, q, w, nullptr, s);  // statistics, selection, dispatch
+    for (int i = 0; i < nchk; ++i) {     // compensation by row chunks, each shipped back at once
+        const int r0 = r0s[i], rows = r0s[i + 1] - r0s[i];
+        Pipe pi = p;
+        pi.M = rows;
+        pi.aq = p.aq + (int64_t)r0 * ldk; pi.raq = p.raq + (int64_t)r0 * ldk; pi.ared = p.ared + (int64_t)r0 * ldk;
+        pi.la = p.la + r0;
+        gemm_comp(pi, dout + (int64_t)r0 * N, dc ? dc + (int64_t)r0 * N : nullptr, alpha, beta);
+        ck(cudaEventRecord(ev[8 + i], s), "event");
+        ck(cudaStreamWaitEvent(s_out, ev[8 + i], 0), "wait");
+        ck(cudaMemcpyAsync(out_h + (int64_t)r0 * N, dout + (int64_t)r0 * N, sizeof(float) * (size_t)rows * N,
+                           cudaMemcpyDeviceToHost, s_out), "d2h");
+    }
+    xg::DevScalars h;
+    ck(cudaMemcpyAsync(&h, w.sc, sizeof h, cudaMemcpyDeviceToHost, s), "report");
+    ck(cudaEventRecord(ev[16], s_out), "event");
+    ck(cudaStreamWaitEvent(s, ev[16], 0), "wait");  // the scratch is released on s after the copies
+    ck(cudaStreamSynchronize(s), "pipeline");
+    EventTimer tm(false, s);
+    finish_report(h, reduce, tm, rep);
+}
+
 xg_status xg_xigemm_host(const float* a, const float* b, const float* c, float alpha, float beta,
                          int m, int k, int n, const xg_config* cfg, int reduce, float* out,
                          xg_report* rep) {
     return guarded([&] {
         validate_cfg(cfg);
         req(m >= 1 && k >= 1 && n >= 1, "xigemm: matrix dimensions must be >= 1");
+        static const bool overlap_off = [] {
+            const char* e = getenv("XG_HOST_NO_OVERLAP");
+            return e && *e == '1';
+        }();
+        if (!overlap_off && cfg->scheme == XG_Q_VECTORWISE && m >= 1024 && (n % 4) == 0) {
+            run_pipeline_host(a, b, c, alpha, beta, m, k, n, cfg, reduce, out, rep);
+            return;
+        }
         cudaStream_t s = host_stream();
         Scratch S(s);
         const size_t na = (size_t)m * k, nb = (size_t)k * n, nc = (size_t)m * n;

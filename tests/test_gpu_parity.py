@@ -383,3 +383,25 @@ def test_pipeline_nan_input_rejected():
         with pytest.raises(xg.InvalidArgument):
             xg.xigemm(a, b)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("shape", [(1024, 512, 384), (2300, 1024, 516), (4096, 256, 1024)])
+def test_host_entry_overlapped_equals_device(shape):
+    """xg_xigemm_host's overlapped schedule (B, then A in row chunks over PCIe,
+    K1 per chunk, compensation + D2H per chunk) equals the device-pointer call."""
+    m, k, n = shape
+    a = ol.random_dense(m, k, m, -3, 3)
+    b = ol.random_dense(k, n, n, -3, 3)
+    c = ol.random_dense(m, n, 9, -1, 1)
+    cfg = xg.XigemmConfig(threshold=0.05, density_limit=0.5, scheme=xg.QuantScheme.VectorWise,
+                          policy=xg.ReductionPolicy.AvgRule)
+    for cc, al, be in ((None, 1.0, 0.0), (c, 1.5, -0.25)):
+        res, rep = xg.xigemm_host(a, b, cc, al, be, cfg=cfg)
+        ref = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                        None if cc is None else torch.from_numpy(cc).cuda(), al, be, cfg)
+        assert beq(res, ref.result)
+        assert (rep.density_a, rep.density_b, rep.path) == (ref.density_a, ref.density_b, int(ref.path))
+    bad = a.copy()
+    bad[m - 1, k - 1] = np.inf
+    with pytest.raises(xg.InvalidArgument):
+        xg.xigemm_host(bad, b, cfg=cfg)
