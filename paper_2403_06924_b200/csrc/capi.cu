@@ -1627,10 +1627,14 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
     ck(cudaEventRecord(ev[0], s), "event");
     ck(cudaStreamWaitEvent(s_in, ev[0], 0), "wait");
     ck(cudaStreamWaitEvent(s_out, ev[0], 0), "wait");
-    const int nch = M >= 4096 ? 4 : 2;
+    static const int nch = [] {
+        const char* e = getenv("XG_HOST_CHUNKS");  // tuning aid
+        const int v = e ? atoi(e) : 8;
+        return v < 1 ? 1 : v > 8 ? 8 : v;
+    }();
     const int rc = ((M + nch - 1) / nch + 255) / 256 * 256;
-    int r0s[5], nchk = 0;
-    for (int r = 0; r < M && nchk < 4; r += rc) r0s[nchk++] = r;
+    int r0s[9], nchk = 0;
+    for (int r = 0; r < M && nchk < nch; r += rc) r0s[nchk++] = r;
     r0s[nchk] = M;
     // H2D: B, A chunks, C
     ck(cudaMemcpyAsync(db, b_h, sizeof(float) * (size_t)K * N, cudaMemcpyHostToDevice, s_in), "h2d");
@@ -1642,7 +1646,7 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
     }
     if (c_h) {
         ck(cudaMemcpyAsync(dc, c_h, sizeof(float) * (size_t)M * N, cudaMemcpyHostToDevice, s_in), "h2d");
-        ck(cudaEventRecord(ev[6], s_in), "event");
+        ck(cudaEventRecord(ev[10], s_in), "event");
     }
     // compute
     PipeCall q{da, db, dc, alpha, beta, M, K, N, *cfg, reduce, dout};
@@ -1662,7 +1666,7 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
         quantize_a_rows(p, da, r0s[i], r0s[i + 1] - r0s[i]);
     }
     if (c_h) {
-        ck(cudaStreamWaitEvent(s, ev[6], 0), "wait");
+        ck(cudaStreamWaitEvent(s, ev[10], 0), "wait");
         xg::finite_max(dc, (int64_t)M * N, &p.sc->retB /*scratch, reset below*/, &p.sc->nonfinite, s);
         check_launch("finite C");
         ck(cudaMemsetAsync(&p.sc->retB, 0, sizeof(uint32_t), s), "memset");
@@ -1678,15 +1682,15 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
         pi.aq = p.aq + (int64_t)r0 * ldk; pi.raq = p.raq + (int64_t)r0 * ldk; pi.ared = p.ared + (int64_t)r0 * ldk;
         pi.la = p.la + r0;
         gemm_comp(pi, dout + (int64_t)r0 * N, dc ? dc + (int64_t)r0 * N : nullptr, alpha, beta);
-        ck(cudaEventRecord(ev[8 + i], s), "event");
-        ck(cudaStreamWaitEvent(s_out, ev[8 + i], 0), "wait");
+        ck(cudaEventRecord(ev[11 + i], s), "event");
+        ck(cudaStreamWaitEvent(s_out, ev[11 + i], 0), "wait");
         ck(cudaMemcpyAsync(out_h + (int64_t)r0 * N, dout + (int64_t)r0 * N, sizeof(float) * (size_t)rows * N,
                            cudaMemcpyDeviceToHost, s_out), "d2h");
     }
     xg::DevScalars h;
     ck(cudaMemcpyAsync(&h, w.sc, sizeof h, cudaMemcpyDeviceToHost, s), "report");
-    ck(cudaEventRecord(ev[16], s_out), "event");
-    ck(cudaStreamWaitEvent(s, ev[16], 0), "wait");  // the scratch is released on s after the copies
+    ck(cudaEventRecord(ev[20], s_out), "event");
+    ck(cudaStreamWaitEvent(s, ev[20], 0), "wait");  // the scratch is released on s after the copies
     ck(cudaStreamSynchronize(s), "pipeline");
     EventTimer tm(false, s);
     finish_report(h, reduce, tm, rep);
