@@ -228,7 +228,7 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
         check_launch("absmax A");
     }
     if (!(phases & 2)) {
-        if (phases & 4) {
+        if ((phases & 4) && !p.vw) {  // per-tensor scales only (VectorWise reads la/lb)
             launch_lambdas(p.sc, bits, p.s);
             check_launch("lambdas");
         }
@@ -271,7 +271,7 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
     launch_quant_cols_T(qb, sb);
     check_launch("quantize B");
     if (co) join(p.s);
-    if (phases & 4) {
+    if ((phases & 4) && !p.vw) {  // per-tensor scales only (VectorWise reads la/lb)
         launch_lambdas(p.sc, bits, p.s);
         check_launch("lambdas");
     }
@@ -1700,9 +1700,7 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
         check_launch("finite C");
         ck(cudaMemsetAsync(&p.sc->retB, 0, sizeof(uint32_t), s), "memset");
     }
-    xg::launch_lambdas(p.sc, cfg->bits, s);
-    check_launch("lambdas");
-    enqueue_stage(1, q, w, nullptr, s);  // D_F GEMM
+    enqueue_stage(1, q, w, nullptr, s);  // D_F GEMM (VectorWise: no per-tensor lambdas needed)
     enqueue_stage(2, q, w, nullptr, s);  // statistics, selection, dispatch
     for (int i = 0; i < nchk; ++i) {     // compensation by row chunks, each shipped back at once
         const int r0 = r0s[i], rows = r0s[i + 1] - r0s[i];
