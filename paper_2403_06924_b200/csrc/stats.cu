@@ -146,7 +146,8 @@ __global__ void k_finalize_avg(const double* row_sum, const double* col_sum, int
 // One parallel scan of that slice decides; only then is the sequential sum
 // paid (the mean stays `lo` otherwise: it is never observable).
 constexpr int kChunk = 2048;
-__global__ void __launch_bounds__(kThreads)
+constexpr int kFallbackThreads = 1024;  // the membership scan is latency-bound: many loads in flight
+__global__ void __launch_bounds__(kFallbackThreads)
     k_fallback_avg(const float* __restrict__ d, int rows, int cols, int col_n, const int* flags,
                    const int* nflag, float* row_stat, float* col_stat, const double* row_sum,
                    const double* col_sum, const StatsDefer def) {
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kThreads)
             const float tlo = float_above(__dmul_rn(def.thr_m, (double)lo));
             const float thi = float_above(__dmul_rn(def.thr_m, (double)hi));
             int amb = 0;
-            for (int t = threadIdx.x; t < def.inner; t += kThreads) {
+            for (int t = threadIdx.x; t < def.inner; t += kFallbackThreads) {
                 const float x = is_row ? def.a[(int64_t)idx * def.lda + t]
                                        : def.b[(int64_t)t * def.ldb + (idx - rows)];
                 amb |= (fabsf(x) >= tlo && fabsf(x) < thi) ? 1 : 0;
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(kThreads)
         double s = 0.0;
         for (int base = 0; base < len; base += kChunk) {
             const int cnt = min(kChunk, len - base);
-            for (int t = threadIdx.x; t < cnt; t += kThreads) {
+            for (int t = threadIdx.x; t < cnt; t += kFallbackThreads) {
                 const int64_t off = is_row ? (int64_t)idx * cols + base + t
                                            : (int64_t)(base + t) * cols + (idx - rows);
                 buf[t] = d[off];
@@ -234,8 +235,8 @@ void launch_stats_final(const float* d, int rows, int cols, int col_n, int polic
     if (policy != kAvg) return;  // MinRule statistics are final after the partial pass (and min-reduce)
     k_finalize_avg<<<(rows + cols + 255) / 256, 256, 0, s>>>(row_sum, col_sum, rows, cols, col_n, row_stat,
                                                              col_stat, flags, nflag, def ? def->widen : 0);
-    k_fallback_avg<<<64, kThreads, 0, s>>>(d, rows, cols, col_n, flags, nflag, row_stat, col_stat, row_sum,
-                                           col_sum, def ? *def : StatsDefer{});
+    k_fallback_avg<<<64, kFallbackThreads, 0, s>>>(d, rows, cols, col_n, flags, nflag, row_stat, col_stat,
+                                                   row_sum, col_sum, def ? *def : StatsDefer{});
 }
 
 void launch_stats(const float* d, int rows, int cols, int policy, float* row_stat, float* col_stat,
