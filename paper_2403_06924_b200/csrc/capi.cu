@@ -1690,9 +1690,24 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
     ck(cudaMemsetAsync(p.sc, 0, sizeof(xg::DevScalars), s), "memset");
     ck(cudaStreamWaitEvent(s, ev[1], 0), "wait");
     quantize_b_vw(p, db);
+    if (reduce)
+        xg::launch_stats_partial(dout, M, N, cfg->policy, w.rstat, w.cstat, w.rsum, w.csum, &p.sc->nflag, s, 1);
+    // per A chunk as it lands: K1 (per-row scales), its rows of D_F, and their
+    // contribution to the row / column statistics
     for (int i = 0; i < nchk; ++i) {
+        const int r0 = r0s[i], rows = r0s[i + 1] - r0s[i];
         ck(cudaStreamWaitEvent(s, ev[2 + i], 0), "wait");
-        quantize_a_rows(p, da, r0s[i], r0s[i + 1] - r0s[i]);
+        quantize_a_rows(p, da, r0, rows);
+        Pipe pi = p;
+        pi.M = rows;
+        pi.aq = p.aq + (int64_t)r0 * ldk;
+        pi.la = p.la + r0;
+        gemm_df(pi, dout + (int64_t)r0 * N);
+        if (reduce) {
+            xg::launch_stats_partial(dout + (int64_t)r0 * N, rows, N, cfg->policy, w.rstat + r0, w.cstat,
+                                     w.rsum + r0, w.csum, &p.sc->nflag, s, 2);
+            check_launch("stats chunk");
+        }
     }
     if (c_h) {
         ck(cudaStreamWaitEvent(s, ev[10], 0), "wait");
@@ -1700,8 +1715,15 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
         check_launch("finite C");
         ck(cudaMemsetAsync(&p.sc->retB, 0, sizeof(uint32_t), s), "memset");
     }
-    enqueue_stage(1, q, w, nullptr, s);  // D_F GEMM (VectorWise: no per-tensor lambdas needed)
-    enqueue_stage(2, q, w, nullptr, s);  // statistics, selection, dispatch
+    if (reduce) {  // the means need every row: finalize + deferred exact check, then selection
+        const xg::StatsDefer def{da, K, db, N, K, cfg->threshold, 0};
+        xg::launch_stats_final(dout, M, N, M, cfg->policy, w.rstat, w.cstat, w.rsum, w.csum, w.flags,
+                               &p.sc->nflag, s, &def);
+        check_launch("stats final");
+    }
+    select_operands(p, da, db, reduce, w.rstat, w.cstat);
+    xg::launch_dispatch(p.sc, cfg->bits, (int64_t)M * K, (int64_t)K * N, cfg->density_limit, reduce, s);
+    check_launch("dispatch");
     for (int i = 0; i < nchk; ++i) {     // compensation by row chunks, each shipped back at once
         const int r0 = r0s[i], rows = r0s[i + 1] - r0s[i];
         Pipe pi = p;

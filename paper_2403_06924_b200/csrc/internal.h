@@ -121,8 +121,11 @@ void launch_stats(const float* d, int rows, int cols, int policy, float* row_sta
                   float* col_stat, double* row_sum, double* col_sum, int* flags, int* nflag,
                   cudaStream_t s, const StatsDefer* def = nullptr);
 // the two halves of launch_stats, split around the row-sharded column reduction
+// mode 0: initialise + accumulate; 1: initialise only; 2: accumulate only (row
+// pointers offset to a row chunk, column accumulators shared by all chunks)
 void launch_stats_partial(const float* d, int rows, int cols, int policy, float* row_stat,
-                          float* col_stat, double* row_sum, double* col_sum, int* nflag, cudaStream_t s);
+                          float* col_stat, double* row_sum, double* col_sum, int* nflag, cudaStream_t s,
+                          int mode = 0);
 void launch_stats_final(const float* d, int rows, int cols, int col_n, int policy, float* row_stat,
                         float* col_stat, double* row_sum, double* col_sum, int* flags, int* nflag,
                         cudaStream_t s, const StatsDefer* def);

@@ -213,19 +213,24 @@ __global__ void k_zero(double* a, int na, double* b, int nb, int* n) {
 }  // namespace
 
 void launch_stats_partial(const float* d, int rows, int cols, int policy, float* row_stat,
-                          float* col_stat, double* row_sum, double* col_sum, int* nflag, cudaStream_t s) {
+                          float* col_stat, double* row_sum, double* col_sum, int* nflag, cudaStream_t s,
+                          int mode) {
     dim3 grid((cols + kThreads * 4 - 1) / (kThreads * 4), (rows + kSlabRows - 1) / kSlabRows);
     if (policy == kAvg) {
         const int nz = rows > cols ? rows : cols;
-        k_zero<<<(nz + 255) / 256, 256, 0, s>>>(row_sum, rows, col_sum, cols, nflag);
-        k_stats_slab<kAvg><<<grid, kThreads, 0, s>>>(d, rows, cols, row_sum, col_sum, nullptr, nullptr);
+        if (mode != 2) k_zero<<<(nz + 255) / 256, 256, 0, s>>>(row_sum, rows, col_sum, cols, nflag);
+        if (mode != 1)
+            k_stats_slab<kAvg><<<grid, kThreads, 0, s>>>(d, rows, cols, row_sum, col_sum, nullptr, nullptr);
     } else {
         // the float bit patterns of |x| order like uints; FLT_MAX initial value (pipeline.cpp:237-238)
-        fill_u32(reinterpret_cast<uint32_t*>(row_stat), 0x7f7fffffu, rows, s);
-        fill_u32(reinterpret_cast<uint32_t*>(col_stat), 0x7f7fffffu, cols, s);
-        k_stats_slab<kMin><<<grid, kThreads, 0, s>>>(d, rows, cols, nullptr, nullptr,
-                                                      reinterpret_cast<uint32_t*>(row_stat),
-                                                      reinterpret_cast<uint32_t*>(col_stat));
+        if (mode != 2) {
+            fill_u32(reinterpret_cast<uint32_t*>(row_stat), 0x7f7fffffu, rows, s);
+            fill_u32(reinterpret_cast<uint32_t*>(col_stat), 0x7f7fffffu, cols, s);
+        }
+        if (mode != 1)
+            k_stats_slab<kMin><<<grid, kThreads, 0, s>>>(d, rows, cols, nullptr, nullptr,
+                                                          reinterpret_cast<uint32_t*>(row_stat),
+                                                          reinterpret_cast<uint32_t*>(col_stat));
     }
 }
 
