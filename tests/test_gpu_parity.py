@@ -393,14 +393,18 @@ def test_host_entry_overlapped_equals_device(shape):
     a = ol.random_dense(m, k, m, -3, 3)
     b = ol.random_dense(k, n, n, -3, 3)
     c = ol.random_dense(m, n, 9, -1, 1)
-    cfg = xg.XigemmConfig(threshold=0.05, density_limit=0.5, scheme=xg.QuantScheme.VectorWise,
-                          policy=xg.ReductionPolicy.AvgRule)
-    for cc, al, be in ((None, 1.0, 0.0), (c, 1.5, -0.25)):
-        res, rep = xg.xigemm_host(a, b, cc, al, be, cfg=cfg)
-        ref = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
-                        None if cc is None else torch.from_numpy(cc).cuda(), al, be, cfg)
-        assert beq(res, ref.result)
-        assert (rep.density_a, rep.density_b, rep.path) == (ref.density_a, ref.density_b, int(ref.path))
+    for pol in (xg.ReductionPolicy.AvgRule, xg.ReductionPolicy.MinRule):
+        cfg = xg.XigemmConfig(threshold=0.05 if pol == xg.ReductionPolicy.AvgRule else 0.5, density_limit=0.5,
+                              scheme=xg.QuantScheme.VectorWise, policy=pol)
+        for cc, al, be in ((None, 1.0, 0.0), (c, 1.5, -0.25)):
+            res, rep = xg.xigemm_host(a, b, cc, al, be, cfg=cfg)
+            ref = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                            None if cc is None else torch.from_numpy(cc).cuda(), al, be, cfg)
+            assert beq(res, ref.result)
+            assert (rep.density_a, rep.density_b, rep.path) == (ref.density_a, ref.density_b, int(ref.path))
+        full, _ = xg.xigemm_host(a, b, cfg=cfg, reduce=False)  # quantized_gemm_full_residual
+        assert beq(full, xg.quantized_gemm_full_residual(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                                                         cfg))
     bad = a.copy()
     bad[m - 1, k - 1] = np.inf
     with pytest.raises(xg.InvalidArgument):
