@@ -63,3 +63,28 @@ def test_no_cpu_fallback_without_device():
     import paper_2403_06924_b200 as xg
     with pytest.raises(Exception):
         xg.xigemm_host(np.ones((4, 4), np.float32), np.ones((4, 4), np.float32))
+
+
+def test_shard_api_validation_without_device():
+    """xg_shard_create rejects bad layouts with XG_EINVAL (the reference's
+    std::invalid_argument class) before touching the device."""
+    import ctypes as C
+    from paper_2403_06924_b200 import _lib
+    lib = _lib.lib()
+    cfg = _lib.XgConfig(8, 0.5, 0.3, 1, 0, 1)
+    h = C.c_void_p()
+    buf = (C.c_float * 16)()
+    rows = (C.c_int * 2)(4, 4)
+
+    def create(rank, nranks, rr, k, n, cfg_=cfg, a=buf, out=buf):
+        return lib.xg_shard_create(a, buf, None, 1.0, 0.0, rank, nranks, rr, k, n, C.byref(cfg_), 1, out,
+                                   C.byref(h))
+
+    assert create(2, 2, rows, 4, 4) == 1                         # rank out of range
+    assert create(0, 2, (C.c_int * 2)(4, 0), 4, 4) == 1          # empty shard
+    assert create(0, 2, rows, 16385, 4) == 1                     # int8 K limit (quantize.cpp:197-200)
+    assert create(0, 2, rows, 4, 4, a=None) == 1                 # null matrix
+    bad = _lib.XgConfig(8, 0.5, 1.5, 1, 0, 1)
+    assert create(0, 2, rows, 4, 4, cfg_=bad) == 1               # s outside (0, 1] (pipeline.cpp:153-160)
+    assert b"density limit" in lib.xg_last_error()
+    assert lib.xg_shard_step(None, 0, None) == 1
