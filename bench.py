@@ -278,27 +278,29 @@ def run_b200(args, world, rank, local):
     value = ops * world / (ms * 1e-3) / 1e12
 
     # ---- e2e through the host-buffer C-ABI call (pinned host buffers) ----
-    ah = torch.empty((m, k), dtype=torch.float32, pin_memory=True)
-    bh = torch.empty((k, n), dtype=torch.float32, pin_memory=True)
-    oh = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
-    ah.copy_(a)
-    bh.copy_(b)
-    an, bn, on = ah.numpy(), bh.numpy(), oh.numpy()
-    for _ in range(2):
-        xg.xigemm_host(an, bn, cfg=cfg, out=on)
-    e2e_steps = max(3, min(args.steps, 10))
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        xg.xigemm_host(an, bn, cfg=cfg, out=on)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_val = ops * world / e2e_s / 1e12
-    # host path result equals the device path result
-    assert np.array_equal(on.view(np.uint32), out.cpu().numpy().view(np.uint32))
+    e2e_val = None
+    if not args.no_e2e:
+        ah = torch.empty((m, k), dtype=torch.float32, pin_memory=True)
+        bh = torch.empty((k, n), dtype=torch.float32, pin_memory=True)
+        oh = torch.empty((m, n), dtype=torch.float32, pin_memory=True)
+        ah.copy_(a)
+        bh.copy_(b)
+        an, bn, on = ah.numpy(), bh.numpy(), oh.numpy()
+        for _ in range(2):
+            xg.xigemm_host(an, bn, cfg=cfg, out=on)
+        e2e_steps = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            xg.xigemm_host(an, bn, cfg=cfg, out=on)
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e_val = ops * world / e2e_s / 1e12
+        # host path result equals the device path result
+        assert np.array_equal(on.view(np.uint32), out.cpu().numpy().view(np.uint32))
 
     if rank != 0:
         return
@@ -315,14 +317,14 @@ def run_b200(args, world, rank, local):
     achieved = kops / tk / 1e12
     traffic = None
     try:  # DRAM bytes per launch of that kernel from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r1d_gemm_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1e_gemm_traffic.json")) as f:
             tr = json.load(f)
         key = "void k_gemm_i8_tc2<1, 4, 1>" if t_cp >= t_df else "void k_gemm_i8_tc2<1, 1, 1>"
         traffic = {"dram_bytes_per_launch": tr[key]["bytes_per_launch"],
                    # int8 operands in (A'q, RBq, RAq, B'q | Aq, Bq), fp32 D_F in (compensation), fp32 out
                    "algorithmic_bytes_per_launch": (2 * (m * k + k * n) + 8 * m * n) if t_cp >= t_df
                    else (m * k + k * n + 4 * m * n),
-                   "source": "profiles/r1d_gemm_traffic.json (ncu --set full, this kernel, C3)"}
+                   "source": "profiles/r1e_gemm_traffic.json (ncu --set full, this kernel, C3)"}
     except (OSError, KeyError, ValueError):
         pass
     # live reference point for the INT8 denominator (MEASURED_PEAKS.json has
@@ -359,7 +361,7 @@ def run_b200(args, world, rank, local):
         "data": "synthetic Student-t(3) (device SplitMix64 generator), seeds A=1 B=2",
         "config": _config(args, thr, dens),
         "e2e": {"value": e2e_val, "unit": "TFLOP/s",
-                "h2d_bytes_per_step": 4 * (m * k + k * n), "d2h_bytes_per_step": 4 * m * n},
+                "h2d_bytes_per_step": 4 * (m * k + k * n), "d2h_bytes_per_step": 4 * m * n} if e2e_val else None,
         "roofline": {"bound": "tensor", "kernel": name, "achieved": achieved,
                      "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
                      "traffic": traffic,
@@ -493,6 +495,7 @@ def main():
                     help="row slab of the CPU samples (default 16 for cpu_baseline, 64 for --impl reference)")
     ap.add_argument("--ref-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent full problems per GPU instead of the row-sharded pipeline")
     ap.add_argument("--sharded", action="store_true",
