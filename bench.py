@@ -347,6 +347,26 @@ def run_b200(args, world, rank, local):
         del ia, ib
     except Exception:  # noqa: BLE001
         pass
+    # accuracy (BASELINE.json metric, second half): relative Frobenius error
+    # e_delta = ||C64 - C||_F / ||C64||_F against an FP64 GEMM of the same
+    # inputs (metrics.cpp:7-33), for xigemm and the paper's two baselines
+    accuracy = None
+    if not args.no_accuracy:
+        try:
+            c64 = a.double() @ b.double()
+            nref = torch.linalg.norm(c64)
+
+            def e_delta(x):
+                return float(torch.linalg.norm(c64 - x.double()) / nref)
+
+            accuracy = {"reference": "FP64 GEMM of the same fp32 inputs (torch float64 matmul on the GPU)",
+                        "e_delta_xigemm": e_delta(out),
+                        "e_delta_origin": e_delta(xg.quantized_gemm_direct(a, b, cfg)),
+                        "e_delta_full_residual": e_delta(xg.quantized_gemm_full_residual(a, b, cfg)),
+                        "e_delta_fp32_gemm": e_delta(a @ b)}
+            del c64
+        except Exception as ex:  # noqa: BLE001
+            accuracy = {"error": str(ex)[:200]}
     cpu = None
     if not args.no_cpu_baseline:
         v, dt, kind = cpu_baseline_sample(a.cpu().numpy(), b.cpu().numpy(), thr, args.ref_rows, 1)
@@ -371,6 +391,7 @@ def run_b200(args, world, rank, local):
                      "frac_of_cublaslt_int8": (achieved / cublaslt) if cublaslt else None},
         "clocks": clk.summary(),
         "gpu_launches": launches,
+        "accuracy": accuracy,
         "stage_ns": {kk: int(vv) for kk, vv in r.timings.items()},  # last timed call
     }
     if cpu:
@@ -496,6 +517,7 @@ def main():
     ap.add_argument("--ref-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
+    ap.add_argument("--no-accuracy", action="store_true", help="skip the FP64-GEMM error report")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent full problems per GPU instead of the row-sharded pipeline")
     ap.add_argument("--sharded", action="store_true",
