@@ -194,10 +194,19 @@ Aux& aux_stream() {
     }
     return x;
 }
-// Opt-in (XG_COSCHED=1): measured slower on B200 at C3 (quant 220->281 us,
-// reduce 309->454 us) -- the persistent grids split the SMs but the two sides
-// do not finish together, so each runs part of the time at half width.
+// A-side and B-side kernels of K1 and K3 on two streams (graph branches), each
+// with its full persistent grid, so the second side fills the SMs the first
+// one's tail frees: K1 203 -> 191 us at C3 (K3 unchanged).  XG_COSCHED=0
+// serialises them; XG_COSCHED=1 also splits the grids per SM (measured
+// slower: 220 -> 281 us for K1, 309 -> 454 us for K3).
 bool coschedule_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("XG_COSCHED");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+bool coschedule_share() {
     static const bool on = [] {
         const char* e = getenv("XG_COSCHED");
         return e && *e == '1';
@@ -243,7 +252,7 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
     qa.bits = bits; qa.rounding = rnd;
     qa.q = p.aq; qa.ldq = p.ldk;
     qa.rmax = &p.sc->maxRA; qa.nonfinite = &p.sc->nonfinite;
-    qa.co_share = co ? 2 : 0;
+    qa.co_share = co && coschedule_share() ? 2 : 0;
     if (p.vw) {
         qa.per_row = 1; qa.lam_out = p.la; qa.gmax = &p.sc->maxA;
     } else {
@@ -257,7 +266,7 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
     qb.bits = bits; qb.rounding = rnd;
     qb.qT = p.bqT; qb.ldq = p.ldk; qb.rmax = &p.sc->maxRB;
     qb.nonfinite = &p.sc->nonfinite;
-    qb.co_share = co ? 1 : 0;
+    qb.co_share = co && coschedule_share() ? 1 : 0;
     if (p.vw) {
         ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, sb), "memset");
         launch_absmax_cols(b, p.K, p.N, p.N, p.colmax, &p.sc->maxB, &p.sc->nonfinite, sb);
@@ -344,10 +353,10 @@ void select_operands(Pipe& p, const float* a, const float* b, int reduce, const 
     {
     const bool co = coschedule_enabled();
     cudaStream_t s2 = co ? fork(p.s) : p.s;
-    sa.co_share = co ? 4 : 0;
+    sa.co_share = co && coschedule_share() ? 4 : 0;
     launch_select_rows(sa, p.s);
     check_launch("select A");
-    sb.co_share = co ? 1 : 0;
+    sb.co_share = co && coschedule_share() ? 1 : 0;
     launch_select_cols_T(sb, s2);
     check_launch("select B");
     if (co) join(p.s);
