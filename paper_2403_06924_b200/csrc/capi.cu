@@ -173,6 +173,7 @@ struct Pipe {
     int8_t *aq, *bqT, *raq, *rbqT, *ared, *bredT;
     double *la, *lb;
     uint32_t* colmax;
+    bool pre_init = false;  // colmax / statistics accumulators already initialised
 };
 
 // Second stream for the independent A-side / B-side memory-bound kernels of
@@ -268,7 +269,7 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
     qb.nonfinite = &p.sc->nonfinite;
     qb.co_share = co && coschedule_share() ? 1 : 0;
     if (p.vw) {
-        ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, sb), "memset");
+        if (!p.pre_init) ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, sb), "memset");
         launch_absmax_cols(b, p.K, p.N, p.N, p.colmax, &p.sc->maxB, &p.sc->nonfinite, sb);
         check_launch("absmax B cols");
         qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb;
@@ -539,8 +540,11 @@ int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* du
     p.bqT = w.bqT; p.rbqT = w.rbqT; p.bredT = w.bredT;
     p.la = w.la; p.lb = w.lb; p.colmax = w.colmax;
     const int M = q.M, K = q.K, N = q.N;
+    p.pre_init = true;  // stage 0 initialises everything in one launch
     if (stage == 0) {
-        ck(cudaMemsetAsync(p.sc, 0, sizeof(xg::DevScalars), s), "memset");
+        xg::launch_pipe_init(p.sc, sizeof(xg::DevScalars), p.colmax, N, w.rsum, w.csum, w.rstat, w.cstat, M,
+                             q.cfg.policy, q.reduce, s);
+        check_launch("init");
         if (q.c) {
             xg::finite_max(q.c, (int64_t)M * N, &p.sc->retB /*scratch, reset below*/, &p.sc->nonfinite, s);
             check_launch("finite C");
@@ -560,9 +564,11 @@ int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* du
                 return e ? atoi(e) : 0;
             }();
             const xg::StatsDefer def{q.a, K, q.b, N, K, q.cfg.threshold, widen};
-            xg::launch_stats(q.out, M, N, q.cfg.policy, w.rstat, w.cstat, w.rsum, w.csum, w.flags,
-                             &p.sc->nflag, s, dump ? nullptr : &def);
-            check_launch("stats", q.cfg.policy == XG_AVG_RULE ? 4 : 3);
+            // accumulators were initialised by stage 0 (launch_pipe_init)
+            xg::launch_stats_partial(q.out, M, N, q.cfg.policy, w.rstat, w.cstat, w.rsum, w.csum, &p.sc->nflag, s, 2);
+            xg::launch_stats_final(q.out, M, N, M, q.cfg.policy, w.rstat, w.cstat, w.rsum, w.csum, w.flags,
+                                   &p.sc->nflag, s, dump ? nullptr : &def);
+            check_launch("stats", q.cfg.policy == XG_AVG_RULE ? 3 : 1);
         }
         select_operands(p, q.a, q.b, q.reduce, w.rstat, w.cstat);
         xg::launch_dispatch(p.sc, q.cfg.bits, (int64_t)M * K, (int64_t)K * N, q.cfg.density_limit, q.reduce, s);
@@ -579,8 +585,8 @@ int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* du
 }
 
 // ---- CUDA-graph cache ------------------------------------------------------
-// A repeated call (same pointers, shapes and configuration) replays the four
-// stage groups as CUDA graphs captured on a private stream, over a workspace
+// A repeated call (same pointers, shapes and configuration) replays the whole
+// pipeline as one CUDA graph captured on a private stream, over a workspace
 // owned by the cache entry: no per-call allocation, TMA-map encoding or
 // per-kernel launch overhead on the host, so the GPU is not left idle between
 // kernels.  Entries are captured on their second use; at most kGraphEntries

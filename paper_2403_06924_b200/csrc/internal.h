@@ -120,6 +120,9 @@ struct StatsDefer {
 void launch_stats(const float* d, int rows, int cols, int policy, float* row_stat,
                   float* col_stat, double* row_sum, double* col_sum, int* flags, int* nflag,
                   cudaStream_t s, const StatsDefer* def = nullptr);
+// zero the device scalars / column maxima and initialise the statistics accumulators
+void launch_pipe_init(void* sc, int sc_bytes, uint32_t* colmax, int N, double* rsum, double* csum,
+                      float* rstat, float* cstat, int M, int policy, int reduce, cudaStream_t s);
 // the two halves of launch_stats, split around the row-sharded column reduction
 // mode 0: initialise + accumulate; 1: initialise only; 2: accumulate only (row
 // pointers offset to a row chunk, column accumulators shared by all chunks)

@@ -212,6 +212,38 @@ __global__ void k_zero(double* a, int na, double* b, int nb, int* n) {
 
 }  // namespace
 
+// One launch for all the per-call initialisation of the device pipeline:
+// device scalars, column-max accumulators and the statistics accumulators
+// (fp64 sums for AvgRule, FLT_MAX bit patterns for MinRule).
+__global__ void k_pipe_init(uint32_t* sc, int sc_words, uint32_t* colmax, int N, double* rsum,
+                            double* csum, uint32_t* rmin, uint32_t* cmin, int M, int policy, int reduce) {
+    XG_PDL_WAIT();
+    const int n = max(max(M, N), sc_words);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (i < sc_words) sc[i] = 0u;
+        if (i < N && colmax) colmax[i] = 0u;
+        if (reduce) {
+            if (policy == kAvg) {
+                if (i < M) rsum[i] = 0.0;
+                if (i < N) csum[i] = 0.0;
+            } else {
+                if (i < M) rmin[i] = 0x7f7fffffu;
+                if (i < N) cmin[i] = 0x7f7fffffu;
+            }
+        }
+    }
+}
+
+void launch_pipe_init(void* sc, int sc_bytes, uint32_t* colmax, int N, double* rsum, double* csum,
+                      float* rstat, float* cstat, int M, int policy, int reduce, cudaStream_t s) {
+    const int n = M > N ? M : N;
+    int blocks = (n + 255) / 256;
+    blocks = blocks < 1 ? 1 : blocks > 1024 ? 1024 : blocks;
+    k_pipe_init<<<blocks, 256, 0, s>>>(reinterpret_cast<uint32_t*>(sc), sc_bytes / 4, colmax, N, rsum, csum,
+                                        reinterpret_cast<uint32_t*>(rstat), reinterpret_cast<uint32_t*>(cstat), M,
+                                        policy, reduce);
+}
+
 void launch_stats_partial(const float* d, int rows, int cols, int policy, float* row_stat,
                           float* col_stat, double* row_sum, double* col_sum, int* nflag, cudaStream_t s,
                           int mode) {
