@@ -129,7 +129,7 @@ void validate_cfg(const xg_config* c) {
     req(c->rounding == XG_FLOOR || c->rounding == XG_NEAREST, "bad rounding mode");
 }
 
-xg::ScaleRef sref(const double* p, int stride) { return xg::ScaleRef{p, stride}; }
+xg::ScaleRef sref(const double* p, int stride, const float2* r = nullptr) { return xg::ScaleRef{p, stride, r}; }
 
 struct EventTimer {
     bool on;
@@ -172,6 +172,7 @@ struct Pipe {
     xg::DevScalars* sc;
     int8_t *aq, *bqT, *raq, *rbqT, *ared, *bredT;
     double *la, *lb;
+    float2 *lar = nullptr, *lbr = nullptr;  // ff_recip of la / lb (VectorWise), may be null
     uint32_t* colmax;
     bool pre_init = false;  // colmax / statistics accumulators already initialised
 };
@@ -255,7 +256,7 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
     qa.rmax = &p.sc->maxRA; qa.nonfinite = &p.sc->nonfinite;
     qa.co_share = co && coschedule_share() ? 2 : 0;
     if (p.vw) {
-        qa.per_row = 1; qa.lam_out = p.la; qa.gmax = &p.sc->maxA;
+        qa.per_row = 1; qa.lam_out = p.la; qa.rcp_out = p.lar; qa.gmax = &p.sc->maxA;
     } else {
         qa.per_row = 0; qa.tensor_max = &p.sc->maxA;
     }
@@ -272,7 +273,7 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
         if (!p.pre_init) ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, sb), "memset");
         launch_absmax_cols(b, p.K, p.N, p.N, p.colmax, &p.sc->maxB, &p.sc->nonfinite, sb);
         check_launch("absmax B cols");
-        qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb;
+        qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb; qb.rcp_out = p.lbr;
     } else {
         launch_absmax_global(b, (int64_t)p.K * p.N, &p.sc->maxB, &p.sc->nonfinite, sb);
         check_launch("absmax B");
@@ -296,7 +297,7 @@ void quantize_a_rows(Pipe& p, const float* a, int r0, int rows) {
     qa.bits = p.cfg->bits; qa.rounding = p.cfg->rounding;
     qa.q = p.aq + (int64_t)r0 * p.ldk; qa.ldq = p.ldk;
     qa.rmax = &p.sc->maxRA; qa.nonfinite = &p.sc->nonfinite;
-    qa.per_row = 1; qa.lam_out = p.la + r0; qa.gmax = &p.sc->maxA;
+    qa.per_row = 1; qa.lam_out = p.la + r0; qa.rcp_out = p.lar ? p.lar + r0 : nullptr; qa.gmax = &p.sc->maxA;
     launch_quant_rows(qa, p.s);
     check_launch("quantize A rows");
 }
@@ -311,7 +312,7 @@ void quantize_b_vw(Pipe& p, const float* b) {
     ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, p.s), "memset");
     launch_absmax_cols(b, p.K, p.N, p.N, p.colmax, &p.sc->maxB, &p.sc->nonfinite, p.s);
     check_launch("absmax B cols");
-    qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb;
+    qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb; qb.rcp_out = p.lbr;
     launch_quant_cols_T(qb, p.s);
     check_launch("quantize B");
 }
@@ -325,8 +326,8 @@ void gemm_df(Pipe& p, float* out) {
     g.amap[0][0] = g.amap[0][1] = 0;
     g.bmap[0][0] = g.bmap[0][1] = 1;
     g.out_f32 = out;
-    g.rs[0][0] = g.rs[0][1] = p.vw ? sref(p.la, 1) : sref(&p.sc->lamA, 0);
-    g.cs[0][0] = g.cs[0][1] = p.vw ? sref(p.lb, 1) : sref(&p.sc->lamB, 0);
+    g.rs[0][0] = g.rs[0][1] = p.vw ? sref(p.la, 1, p.lar) : sref(&p.sc->lamA, 0, &p.sc->rA);
+    g.cs[0][0] = g.cs[0][1] = p.vw ? sref(p.lb, 1, p.lbr) : sref(&p.sc->lamB, 0, &p.sc->rB);
     gemm_i8(EPI_DF, ops, isb, 2, g, p.s);
     check_launch("gemm D_F");
 }
@@ -384,13 +385,13 @@ void gemm_comp(Pipe& p, float* out, const float* c, float alpha, float beta) {
                        {p.raq, p.M, p.ldk}, {p.bqT, p.N, p.ldk},  {p.bredT, p.N, p.ldk}};
     int isb[6] = {0, 0, 1, 0, 1, 1};
     // dr1 = X1 * RBq : left scale (aq or a_red) per row / per tensor, right lambda_RB
-    const ScaleRef r1d = p.vw ? sref(p.la, 1) : sref(&p.sc->lamA, 0);
-    const ScaleRef r1s = p.vw ? sref(p.la, 1) : sref(&p.sc->lamAred, 0);
-    const ScaleRef c1 = sref(&p.sc->lamRB, 0);
+    const ScaleRef r1d = p.vw ? sref(p.la, 1, p.lar) : sref(&p.sc->lamA, 0, &p.sc->rA);
+    const ScaleRef r1s = p.vw ? sref(p.la, 1, p.lar) : sref(&p.sc->lamAred, 0, &p.sc->rAred);
+    const ScaleRef c1 = sref(&p.sc->lamRB, 0, &p.sc->rRB);
     // dr2 = RAq * Y2 : lambda_RA, right scale (bq or b_red)
-    const ScaleRef r2 = sref(&p.sc->lamRA, 0);
-    const ScaleRef c2d = p.vw ? sref(p.lb, 1) : sref(&p.sc->lamB, 0);
-    const ScaleRef c2s = p.vw ? sref(p.lb, 1) : sref(&p.sc->lamBred, 0);
+    const ScaleRef r2 = sref(&p.sc->lamRA, 0, &p.sc->rRA);
+    const ScaleRef c2d = p.vw ? sref(p.lb, 1, p.lbr) : sref(&p.sc->lamB, 0, &p.sc->rB);
+    const ScaleRef c2s = p.vw ? sref(p.lb, 1, p.lbr) : sref(&p.sc->lamBred, 0, &p.sc->rBred);
     if (p.M >= 256 && (p.N % 4) == 0 && !getenv("XG_GEMM_1CTA")) {
         // Two single-accumulator pair GEMMs with double-buffered TMEM (pipeline.cpp:141-145
         // order): out = fl(D_F + deq(dr1)), then out = fl(out + deq(dr2)) and alpha/beta.
@@ -492,6 +493,7 @@ struct PipeWs {
     xg::DevScalars* sc;
     int8_t *aq, *raq, *ared, *bqT, *rbqT, *bredT;
     double *la, *lb;
+    float2 *lar, *lbr;
     uint32_t* colmax;
     float *rstat, *cstat;
     double *rsum, *csum;
@@ -509,6 +511,8 @@ void alloc_ws(PipeWs& w, int M, int N, int64_t ldk, Get&& get) {
     w.bredT = get((int8_t*)nullptr, N * ldk);
     w.la = get((double*)nullptr, M);
     w.lb = get((double*)nullptr, N);
+    w.lar = get((float2*)nullptr, M);
+    w.lbr = get((float2*)nullptr, N);
     w.colmax = get((uint32_t*)nullptr, N);
     w.rstat = get((float*)nullptr, M);
     w.cstat = get((float*)nullptr, N);
@@ -538,7 +542,7 @@ int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* du
     p.sc = w.sc;
     p.aq = w.aq; p.raq = w.raq; p.ared = w.ared;
     p.bqT = w.bqT; p.rbqT = w.rbqT; p.bredT = w.bredT;
-    p.la = w.la; p.lb = w.lb; p.colmax = w.colmax;
+    p.la = w.la; p.lb = w.lb; p.lar = w.lar; p.lbr = w.lbr; p.colmax = w.colmax;
     const int M = q.M, K = q.K, N = q.N;
     p.pre_init = true;  // stage 0 initialises everything in one launch
     if (stage == 0) {
@@ -862,6 +866,8 @@ void run_direct(const float* a, const float* b, int M, int K, int N, const xg_co
     p.bqT = S.get<int8_t>(N * p.ldk);
     p.la = S.get<double>(M);
     p.lb = S.get<double>(N);
+    p.lar = S.get<float2>(M);
+    p.lbr = S.get<float2>(N);
     p.colmax = S.get<uint32_t>(N);
     ck(cudaMemsetAsync(p.sc, 0, sizeof(xg::DevScalars), s), "memset");
     quantize_operands(p, a, b);
@@ -1422,7 +1428,7 @@ Pipe shard_pipe(ShardState& h, cudaStream_t s) {
     p.sc = h.w.sc;
     p.aq = h.w.aq; p.raq = h.w.raq; p.ared = h.w.ared;
     p.bqT = h.w.bqT; p.rbqT = h.w.rbqT; p.bredT = h.w.bredT;
-    p.la = h.w.la; p.lb = h.w.lb; p.colmax = h.w.colmax;
+    p.la = h.w.la; p.lb = h.w.lb; p.lar = h.w.lar; p.lbr = h.w.lbr; p.colmax = h.w.colmax;
     return p;
 }
 
@@ -1701,7 +1707,7 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
     p.sc = w.sc;
     p.aq = w.aq; p.raq = w.raq; p.ared = w.ared;
     p.bqT = w.bqT; p.rbqT = w.rbqT; p.bredT = w.bredT;
-    p.la = w.la; p.lb = w.lb; p.colmax = w.colmax;
+    p.la = w.la; p.lb = w.lb; p.lar = w.lar; p.lbr = w.lbr; p.colmax = w.colmax;
     ck(cudaMemsetAsync(p.sc, 0, sizeof(xg::DevScalars), s), "memset");
     ck(cudaStreamWaitEvent(s, ev[1], 0), "wait");
     quantize_b_vw(p, db);
@@ -1717,6 +1723,7 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
         pi.M = rows;
         pi.aq = p.aq + (int64_t)r0 * ldk;
         pi.la = p.la + r0;
+        pi.lar = p.lar ? p.lar + r0 : nullptr;
         gemm_df(pi, dout + (int64_t)r0 * N);
         if (reduce) {
             xg::launch_stats_partial(dout + (int64_t)r0 * N, rows, N, cfg->policy, w.rstat + r0, w.cstat,
@@ -1745,6 +1752,7 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
         pi.M = rows;
         pi.aq = p.aq + (int64_t)r0 * ldk; pi.raq = p.raq + (int64_t)r0 * ldk; pi.ared = p.ared + (int64_t)r0 * ldk;
         pi.la = p.la + r0;
+        pi.lar = p.lar ? p.lar + r0 : nullptr;
         gemm_comp(pi, dout + (int64_t)r0 * N, dc ? dc + (int64_t)r0 * N : nullptr, alpha, beta);
         ck(cudaEventRecord(ev[11 + i], s), "event");
         ck(cudaStreamWaitEvent(s_out, ev[11 + i], 0), "wait");

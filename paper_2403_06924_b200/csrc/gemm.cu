@@ -122,7 +122,9 @@ void run2(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, 
     cfg.gridDim = dim3(csize * (tiles < max_clusters ? tiles : max_clusters));
     static const int env_gm = [] { const char* e = getenv("XG_GEMM_GROUP"); return e ? atoi(e) : 0; }();
     static const int env_pf = [] { const char* e = getenv("XG_GEMM_PF"); return e ? atoi(e) : -1; }();
+    static const int env_dbg = [] { const char* e = getenv("XG_GEMM_DEBUG"); return e ? atoi(e) : 0; }();
     GemmArgs a2 = args;
+    a2.debug |= env_dbg;
     if (a2.group_m <= 0) a2.group_m = env_gm;
     if (a2.pf_dist <= 0) a2.pf_dist = env_pf >= 0 ? env_pf : kDefaultPrefetch;
     EpiMaps em;

@@ -32,7 +32,9 @@ enum EpiMode : int {
 struct ScaleRef {  // per-row (stride 1) or per-tensor (stride 0) fp64 scales
     const double* p;
     int stride;
+    const float2* r;  // optional ff_recip(p[i]) written by the scale's producer (same stride)
     __device__ __forceinline__ double at(int i) const { return p[(int64_t)i * stride]; }
+    __device__ __forceinline__ float2 rcp(int i) const { return r ? r[(int64_t)i * stride] : ff_recip(at(i)); }
 };
 
 constexpr int kMaxMaps = 6;
@@ -392,7 +394,7 @@ struct Gemm2Cfg {
     static constexpr int THREADS = 384;
     static constexpr int EPI_WARPS = 8;
     // per epilogue warp: NSTG staging tiles of 32x32 fp32 (128B-swizzled, TMA
-    // store / load) and NACC x 32 fp64 column reciprocals
+    // store / load) and NACC x 32 float-float column reciprocals
     static constexpr int NSTG = LOADS_DIN ? 2 : 1;
     static constexpr int STG_BYTES = 32 * 32 * 4;
     static constexpr int EPI_BYTES = EPI_WARPS * NSTG * STG_BYTES;
@@ -594,14 +596,20 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_expect_tx(&mybar[0], Cfg::STG_BYTES);
                 tma_load_2d(stg[0], &emaps.din, &mybar[0], colbase, rowbase);
             }
-            mbar_wait(&tfull[buf], bphase);
-            tc_fence_after();
+            // row scales (fp64 for the rare exact redo) and their float-float
+            // reciprocals, precomputed by the scale's producer (ScaleRef::r)
             double r0 = 1.0, r1 = 1.0;
             if (row_ok) {
                 r0 = args.rs[ts][sel].at(row);
                 if (NACC > 1) r1 = args.rs[1][sel].at(row);
             }
-            const float2 i0 = ff_recip(r0), i1 = ff_recip(r1);
+            float2 i0 = make_float2(1.0f, 0.0f), i1 = i0;
+            if (row_ok) {
+                i0 = args.rs[ts][sel].rcp(row);
+                if (NACC > 1) i1 = args.rs[1][sel].rcp(row);
+            }
+            mbar_wait(&tfull[buf], bphase);
+            tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * Cfg::ACC_COLS +
                                    half * (Cfg::BN / 2);
 #pragma unroll 1
@@ -616,8 +624,8 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 // column reciprocals of this chunk, broadcast through shared memory
                 const int mycol = min(col0 + lane, args.N - 1);
-                scw[lane] = ff_recip(args.cs[ts][sel].at(mycol));
-                if (NACC > 1) scw[32 + lane] = ff_recip(args.cs[1][sel].at(mycol));
+                scw[lane] = args.cs[ts][sel].rcp(mycol);
+                if (NACC > 1) scw[32 + lane] = args.cs[1][sel].rcp(mycol);
                 uint32_t acc[NACC][32];
 #pragma unroll
                 for (int a = 0; a < NACC; ++a) tmem_ld32(tbase + a * Cfg::BN + c * 32, acc[a]);

@@ -23,6 +23,9 @@ struct DevScalars {
     double densA, densB;
     int path;
     int pad1;
+    // float-float reciprocals (common.cuh: ff_recip) of the per-tensor scales above,
+    // written next to them so the GEMM epilogues do no fp64 division
+    float2 rA, rB, rRA, rRB, rAred, rBred;
 };
 
 struct QuantRowsArgs {
@@ -33,6 +36,7 @@ struct QuantRowsArgs {
     int per_row;            // 1: PerRow scales computed here; 0: per-tensor from *tensor_max
     const uint32_t* tensor_max;  // float bits (per-tensor)
     double* lam_out;        // [rows] (per_row) — may be null
+    float2* rcp_out;        // [rows] ff_recip(lam) next to lam_out — may be null
     int8_t* q;              // [rows x ldq]
     int64_t ldq;
     uint32_t* gmax;         // atomicMax of max|x| (float bits), may be null
@@ -50,6 +54,7 @@ struct QuantColsArgs {
     const uint32_t* colmax;  // float bits [cols] (per_col)
     const uint32_t* tensor_max;
     double* lam_out;         // [cols] (per_col)
+    float2* rcp_out;         // [cols] ff_recip(lam) next to lam_out — may be null
     int8_t* qT;              // [cols x ldq] transposed (K-major)
     int64_t ldq;
     uint32_t* rmax;

@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows(const QuantRowsArgs a) 
         if (a.per_row) {
             lam = compute_scale((double)m, a.bits);  // slice_max_abs: fp64 max == float max
             if (threadIdx.x == 0 && a.lam_out) a.lam_out[r] = lam;
+            if (threadIdx.x == 0 && a.rcp_out) a.rcp_out[r] = ff_recip(lam);
         } else {
             lam = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
         }
@@ -221,6 +222,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows_generic(const QuantRows
         if (a.per_row) {
             lam = compute_scale((double)m, a.bits);
             if (threadIdx.x == 0 && a.lam_out) a.lam_out[r] = lam;
+            if (threadIdx.x == 0 && a.rcp_out) a.rcp_out[r] = ff_recip(lam);
         } else {
             lam = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
         }
@@ -385,6 +387,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_cols_T(const QuantColsArgs a
                                      : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
         lam_s[threadIdx.x] = lam;
         if (a.per_col && blockIdx.y == 0 && a.lam_out && n0 + (int)threadIdx.x < a.cols) a.lam_out[n] = lam;
+        if (a.per_col && blockIdx.y == 0 && a.rcp_out && n0 + (int)threadIdx.x < a.cols) a.rcp_out[n] = ff_recip(lam);
     }
     __syncthreads();
     build_col_luts(lut, lam_s, qmax);
@@ -717,6 +720,7 @@ __global__ void __launch_bounds__(NT) k_quant_rows_fast(const QuantRowsArgs a) {
         if (a.per_row) {
             lam = compute_scale((double)m, a.bits);
             if (threadIdx.x == 0 && a.lam_out) a.lam_out[r] = lam;
+            if (threadIdx.x == 0 && a.rcp_out) a.rcp_out[r] = ff_recip(lam);
         } else {
             lam = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
         }
@@ -859,6 +863,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_cols_T_fast(const QuantColsA
                                      : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
         lam_s[threadIdx.x] = lam;
         if (a.per_col && blockIdx.y == 0 && a.lam_out && n0 + (int)threadIdx.x < a.cols) a.lam_out[n] = lam;
+        if (a.per_col && blockIdx.y == 0 && a.rcp_out && n0 + (int)threadIdx.x < a.cols) a.rcp_out[n] = ff_recip(lam);
     }
     __syncthreads();
     build_col_luts(lut, lam_s, qmax);
@@ -1044,6 +1049,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows_async(const QuantRowsAr
         if (a.per_row) {
             lam = compute_scale((double)m, a.bits);
             if (threadIdx.x == 0 && a.lam_out) a.lam_out[r] = lam;
+            if (threadIdx.x == 0 && a.rcp_out) a.rcp_out[r] = ff_recip(lam);
         } else {
             lam = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
         }
@@ -1229,6 +1235,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_quant_rows_r4(const QuantRowsArgs
         if (a.per_row) {
             lam = compute_scale((double)m, a.bits);
             if (threadIdx.x == 0 && a.lam_out) a.lam_out[r] = lam;
+            if (threadIdx.x == 0 && a.rcp_out) a.rcp_out[r] = ff_recip(lam);
         } else {
             lam = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
         }
@@ -1345,6 +1352,7 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
         if (SELECT) lam = sa.vec ? sa.lam[nc] : lam_t;
         else lam = qa.per_col ? compute_scale((double)__uint_as_float(qa.colmax[nc]), bits) : lam_t;
         if (!SELECT && qa.per_col && qa.lam_out && chunk == 0 && w == 0 && n < cols) qa.lam_out[n] = lam;
+        if (!SELECT && qa.per_col && qa.rcp_out && chunk == 0 && w == 0 && n < cols) qa.rcp_out[n] = ff_recip(lam);
         const float lam32 = __double2float_rn(lam);
         const bool exact = !(lam32 <= FLT_MAX) || (SELECT && !(lam_r32 <= FLT_MAX));
         float tf = __int_as_float(0x7f800000);
@@ -1448,6 +1456,8 @@ __global__ void k_lambdas(DevScalars* sc, int bits) {
     XG_PDL_WAIT();
     sc->lamA = compute_scale((double)__uint_as_float(sc->maxA), bits);
     sc->lamB = compute_scale((double)__uint_as_float(sc->maxB), bits);
+    sc->rA = ff_recip(sc->lamA);
+    sc->rB = ff_recip(sc->lamB);
 }
 
 // Density, dispatch (pipeline.cpp:106-111) and the per-tensor scales the
@@ -1458,6 +1468,10 @@ __global__ void k_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, dou
     sc->lamRB = compute_scale((double)__uint_as_float(sc->maxRB), bits);
     sc->lamAred = compute_scale((double)__uint_as_float(sc->retA), bits);
     sc->lamBred = compute_scale((double)__uint_as_float(sc->retB), bits);
+    sc->rRA = ff_recip(sc->lamRA);
+    sc->rRB = ff_recip(sc->lamRB);
+    sc->rAred = ff_recip(sc->lamAred);
+    sc->rBred = ff_recip(sc->lamBred);
     if (reduce) {
         const double da = __ddiv_rn((double)sc->nnzA, (double)MK);
         const double db = __ddiv_rn((double)sc->nnzB, (double)KN);
