@@ -1100,6 +1100,8 @@ extern "C" double xg_debug_gemm_df(int m, int n, int k, int flags, int iters) {
         float* out = S.get<float>((int64_t)m * n);
         double* la = S.get<double>(m);
         double* lb = S.get<double>(n);
+        float2* lar = S.get<float2>(m);
+        float2* lbr = S.get<float2>(n);
         // random int8 operands in [-127, 127] (flag 16: zeros), scales 1.0
         if (flags & 16) {
             ck(cudaMemsetAsync(a, 0, m * ldk, s), "memset");
@@ -1113,6 +1115,15 @@ extern "C" double xg_debug_gemm_df(int m, int n, int k, int flags, int iters) {
             for (size_t i = 0; i < h.size(); ++i) h[i] = 127.0 / (3.0 + 0.001 * (double)(i % 977));
             ck(cudaMemcpyAsync(la, h.data(), 8 * (size_t)m, cudaMemcpyHostToDevice, s), "h2d");
             ck(cudaMemcpyAsync(lb, h.data(), 8 * (size_t)n, cudaMemcpyHostToDevice, s), "h2d");
+            // their float-float reciprocals as the pipeline's scale producers write them
+            std::vector<float2> r(h.size());
+            for (size_t i = 0; i < h.size(); ++i) {
+                const double ia = 1.0 / h[i];
+                const float hi = (float)ia;
+                r[i] = make_float2(hi, (float)(ia - (double)hi));
+            }
+            ck(cudaMemcpyAsync(lar, r.data(), 8 * (size_t)m, cudaMemcpyHostToDevice, s), "h2d");
+            ck(cudaMemcpyAsync(lbr, r.data(), 8 * (size_t)n, cudaMemcpyHostToDevice, s), "h2d");
             ck(cudaStreamSynchronize(s), "sync");
         }
         xg::KOperand ops[2] = {{a, m, ldk}, {bt, n, ldk}};
@@ -1122,8 +1133,8 @@ extern "C" double xg_debug_gemm_df(int m, int n, int k, int flags, int iters) {
         g.amap[0][0] = g.amap[0][1] = 0;
         g.bmap[0][0] = g.bmap[0][1] = 1;
         g.out_f32 = out;
-        g.rs[0][0] = g.rs[0][1] = sref(la, 1);
-        g.cs[0][0] = g.cs[0][1] = sref(lb, 1);
+        g.rs[0][0] = g.rs[0][1] = sref(la, 1, lar);
+        g.cs[0][0] = g.cs[0][1] = sref(lb, 1, lbr);
         g.debug = flags;
         for (int i = 0; i < 2; ++i) xg::gemm_i8(xg::EPI_DF, ops, isb, 2, g, s);
         cudaEvent_t e0, e1;

@@ -194,6 +194,9 @@ __device__ __forceinline__ float2 ff_recip(double lam) {
 }
 
 __device__ __forceinline__ float dq_ff(int32_t p, float2 a, float2 b, bool& slow) {
+    // the reference's 0 / (la*lb) with la*lb positive and finite (compute_scale's
+    // range), also when a scale is outside ff_recip's range (NaN marker)
+    if (p == 0) return 0.0f;
     const float ch = __fmul_rn(a.x, b.x);
     const float ce = __fmaf_rn(a.x, b.x, -ch);
     const float cl = __fmaf_rn(a.x, b.y, __fmaf_rn(a.y, b.x, ce));
@@ -221,11 +224,17 @@ __device__ __forceinline__ float dq_ff(int32_t p, float2 a, float2 b, bool& slow
 
 // Epilogue fast form for |p| < 2^24 (p exact as a float, the common case: a
 // K=8192 int8 product of random data stays near 1e5): y = pf*(ch + cl) with
-// pf*ch exact as t1 + e1, |y - p/(la*lb)| <= 2^-44.5|y|.  The midpoint test is
-// done on the float bit patterns: |r| < 2^(e-24) - 2^(e-40) with e = f's
-// exponent (ulp(f)/2 minus a margin 8x the error bound).  Elements that fail
-// (|p| >= 2^24, power-of-two f, out-of-range magnitude, ~2^-15 of random
-// ones) set their bit in `slowmask` and are redone by dq_slow.
+// pf*ch exact as t1 + e1, |y - p/(la*lb)| <= 2^-44.5|y|.  Accepted when
+// |r| <= 2^(e-24) - 2^(e-39), e the exponent of the float just below |f|:
+// half the gap to f's lower neighbour minus a margin 8x the error bound, so y
+// and the reference's q lie strictly on f's side of both neighbouring
+// midpoints (for a power of two f the lower gap is ulp(f)/2, and e is one
+// less).  No range tests are needed: ff_recip's ranges give ch in
+// [2^-100, 2^100], so for 0 < |p| < 2^24 f is normal and finite and every
+// error term is exact or far below the margin; p = 0 gives f = r = +0
+// (accepted: the reference's +0); a non-finite scale marker makes r NaN
+// (rejected).  Elements that fail (|p| >= 2^24, ~2^-15 of random ones) set
+// their bit in `slowmask` and are redone by dq_slow.
 __device__ __forceinline__ float dq_ff24(int32_t p, float2 a, float2 b, uint32_t& slowmask,
                                          uint32_t bit) {
     const float ch = __fmul_rn(a.x, b.x);
@@ -237,12 +246,12 @@ __device__ __forceinline__ float dq_ff24(int32_t p, float2 a, float2 b, uint32_t
     const float lo = __fmaf_rn(pf, cl, e1);
     const float f = __fadd_rn(t1, lo);
     const float r = __fadd_rn(__fsub_rn(t1, f), lo);
-    const uint32_t fb = __float_as_uint(f);
-    const uint32_t ef = fb & 0x7f800000u;
-    const bool ok = (ef - (42u << 23)) < (212u << 23) && (fb << 9) != 0u &&
-                    (__float_as_uint(r) & 0x7fffffffu) < ef - (24u << 23) - 256u &&
-                    (uint32_t)(p + 0x1000000) < 0x2000000u;
-    slowmask |= (ok || p == 0) ? 0u : bit;
+    // exponent of the float just below |f| (fb - 1): one less than f's own for a
+    // power of two, whose lower neighbour is only ulp(f)/2 away
+    const int ef = (int)((__float_as_uint(f) - 1u) & 0x7f800000u);
+    const float thr = __int_as_float(max(ef - ((24 << 23) + 256), 0));
+    const bool ok = fabsf(pf) < 16777216.0f && fabsf(r) <= thr;
+    slowmask |= ok ? 0u : bit;
     return f;
 }
 

@@ -216,7 +216,9 @@ __global__ void __launch_bounds__(256, 1)
     k_gemm_i8_tc(const __grid_constant__ TmaMaps maps, const GemmArgs args) {
     using Cfg = GemmCfg<BN, NACC>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-byte alignment by pointer arithmetic on the shared array (not through
+    // uintptr_t) so the compiler keeps shared-space accesses (LDS/STS, not LD/ST)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = (uint64_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
     uint64_t* empty = full + Cfg::STAGES;
     uint64_t* tfull = empty + Cfg::STAGES;
@@ -418,7 +420,9 @@ __global__ void __launch_bounds__(384, 1)
                   const __grid_constant__ EpiMaps emaps) {
     using Cfg = Gemm2Cfg<NACC, EPI>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-byte alignment by pointer arithmetic on the shared array (not through
+    // uintptr_t) so the compiler keeps shared-space accesses (LDS/STS, not LD/ST)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     float* epi_stage = (float*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);  // 1024-aligned
     double* epi_scale = (double*)((uint8_t*)epi_stage + Cfg::EPI_BYTES);
     uint64_t* full = (uint64_t*)((uint8_t*)epi_scale + Cfg::SCL_BYTES);

@@ -277,7 +277,8 @@ def _dq_ff(p, la, lb):
 
 def _dq_ref(p, la, lb):
     # quantize.cpp:183: static_cast<float>(p / (la * scales_b.col_scale(j))) in fp64
-    return (p.astype(np.float64) / (la * lb)).astype(np.float32)
+    with np.errstate(over="ignore"):  # fp64 quotients beyond float range become inf, as in C++
+        return (p.astype(np.float64) / (la * lb)).astype(np.float32)
 
 
 def test_dq_ff_random_exact():
@@ -298,6 +299,27 @@ def test_dq_ff_random_exact():
     small = np.abs(p.astype(np.int64)) < 2**24
     assert (flags[small] != 0).mean() < 1e-3  # fast path decides nearly all |p| < 2^24
     assert (flags[~small] >= 2).mean() < 1e-3  # the split form decides nearly all the rest
+
+
+def test_dq_ff_extreme_scales_exact():
+    """Scales across and beyond the float-float reciprocal range (1/lambda near
+    2^-50 and 2^50, where products approach 2^-100 / 2^100), small and large p,
+    powers of two: the epilogue's test needs no explicit range checks there."""
+    rng = np.random.default_rng(99)
+    n = 1 << 20
+    p = np.concatenate([rng.integers(-300, 300, n // 2, dtype=np.int64),
+                        rng.integers(-2**31, 2**31, n // 4, dtype=np.int64),
+                        np.left_shift(1, rng.integers(0, 31, n // 4)) * rng.choice([-1, 1], n // 4)])
+    p = np.clip(p, -2**31, 2**31 - 1).astype(np.int32)
+    ea = rng.uniform(-53, 53, n)
+    eb = rng.uniform(-53, 53, n)
+    la = np.exp2(ea)
+    lb = np.exp2(eb)
+    la[: n // 8] = np.exp2(np.round(ea[: n // 8]))  # exact powers of two
+    lb[n // 8: n // 4] = np.exp2(np.round(eb[n // 8: n // 4]))
+    got, _ = _dq_ff(p, la, lb)
+    ref = _dq_ref(p, la, lb)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
 
 
 def test_dq_ff_near_midpoints_exact():

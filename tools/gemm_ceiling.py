@@ -21,11 +21,13 @@ def sample(stop, out):
 
 
 n = int(os.environ.get("N", "8192"))
+shape = tuple(int(v) for v in os.environ.get("SHAPE", f"{n},{n},{n}").split(","))  # M,N,K
 iters = int(os.environ.get("ITERS", "200"))
 cfgs = [(16, "zeros full"), (18, "zeros no-epi"), (0, "random full"), (2, "random no-epi"),
         (1, "random no-TMA"), (3, "random MMA only"), (4, "random ld-only epi"), (8, "random no-store"),
         (32, "random no-MMA"), (34, "TMA only"), (64, "no-math"), (72, "no-math no-store"),
-        (128, "fp32 math")]
+        (128, "fp32 math"), (33, "epilogue only"), (41, "epi only no-store"), (97, "epi only no-math"),
+        (37, "epi only TMEM drain")]
 sel = os.environ.get("CFGS")
 if sel:
     cfgs = [c for c in cfgs if str(c[0]) in sel.split(",")]
@@ -34,7 +36,7 @@ for flags, name in cfgs:
     stop, smp = threading.Event(), []
     th = threading.Thread(target=sample, args=(stop, smp))
     th.start()
-    ms = L.xg_debug_gemm_df(n, n, n, flags, iters)
+    ms = L.xg_debug_gemm_df(*shape, flags, iters)
     stop.set()
     th.join()
     mid = smp[len(smp) // 4: 3 * len(smp) // 4] or smp
@@ -43,5 +45,5 @@ for flags, name in cfgs:
     rs = 0
     for s in mid:
         rs |= s[2]
-    print(f"{name:18s} {ms:.3f} ms  {2 * n**3 / ms / 1e9:5.0f} TOPS  sm {clk} MHz  {pw:.0f} W  reasons 0x{rs:x}",
+    print(f"{name:18s} {ms:.3f} ms  {2 * shape[0] * shape[1] * shape[2] / ms / 1e9:5.0f} TOPS  sm {clk} MHz  {pw:.0f} W  reasons 0x{rs:x}",
           flush=True)
