@@ -593,10 +593,13 @@ __global__ void __launch_bounds__(384, 1)
             const bool row_ok = row < args.M;
             const int colbase = nb * Cfg::BN + half * (Cfg::BN / 2);
             const int nchunk = (args.debug & 2) ? 0 : min(Cfg::BN / 2 / 32, (args.N - colbase + 31) / 32);
-            if (Cfg::LOADS_DIN && lane == 0 && nchunk > 0) {  // D_F chunk 0 while the MMA still runs
-                // dual term 1 reads back what term 0 stored: wait for the stores themselves
-                if (term) bulk_wait<0>(), fence_proxy_async();
-                else bulk_wait_read<0>();
+            // Dual term 1 reads back what term 0 just produced.  It walks the chunks
+            // in reverse: the last two term-0 chunks are still in their staging
+            // tiles (chunk c in stg[c & 1]) and are updated in place; older ones
+            // are reloaded once term 0's store of that chunk has landed.
+            const bool rev = Cfg::LOADS_DIN && Cfg::NSTG == 2 && nterms == 2 && term == 1;
+            if (Cfg::LOADS_DIN && lane == 0 && nchunk > 0 && !rev) {  // D_F chunk 0 while the MMA still runs
+                bulk_wait_read<0>();
                 mbar_expect_tx(&mybar[0], Cfg::STG_BYTES);
                 tma_load_2d(stg[0], &emaps.din, &mybar[0], colbase, rowbase);
             }
@@ -617,14 +620,22 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * Cfg::ACC_COLS +
                                    half * (Cfg::BN / 2);
 #pragma unroll 1
-            for (int c = 0; c < nchunk; ++c) {
+            for (int i = 0; i < nchunk; ++i) {
+                const int c = rev ? nchunk - 1 - i : i;
                 const int col0 = colbase + c * 32;
                 const int sb = (Cfg::NSTG == 2) ? (c & 1) : 0;
                 float* tile = stg[sb];
-                if (Cfg::LOADS_DIN && lane == 0 && c + 1 < nchunk) {  // prefetch the next D_F chunk
+                const bool resident = rev && i < 2;
+                if (Cfg::LOADS_DIN && lane == 0 && i + 1 < nchunk && !(rev && i + 1 < 2)) {
+                    // prefetch the next D_F chunk into the tile the previous chunk's store read out
+                    const int cn = rev ? c - 1 : c + 1;
+                    if (rev) {  // term 0's store of chunk cn (at most 3 newer groups) has landed
+                        bulk_wait<3>();
+                        fence_proxy_async();
+                    }
                     bulk_wait_read<0>();
-                    mbar_expect_tx(&mybar[(c + 1) & 1], Cfg::STG_BYTES);
-                    tma_load_2d(stg[(c + 1) & 1], &emaps.din, &mybar[(c + 1) & 1], col0 + 32, rowbase);
+                    mbar_expect_tx(&mybar[cn & 1], Cfg::STG_BYTES);
+                    tma_load_2d(stg[cn & 1], &emaps.din, &mybar[cn & 1], colbase + cn * 32, rowbase);
                 }
                 // column reciprocals of this chunk, broadcast through shared memory
                 const int mycol = min(col0 + lane, args.N - 1);
@@ -634,13 +645,18 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int a = 0; a < NACC; ++a) tmem_ld32(tbase + a * Cfg::BN + c * 32, acc[a]);
                 tmem_ld_wait();
-                if (c == nchunk - 1) {  // accumulator drained: hand TMEM back to the MMA early
+                if (i == nchunk - 1) {  // accumulator drained: hand TMEM back to the MMA early
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(tempty_leader0 + buf * 8);
                 }
                 if (args.debug & 4) continue;  // probe: TMEM drain only
-                if (Cfg::LOADS_DIN) {
+                if (resident) {  // term-0 result in place: its own store must have read it out
+                    if (lane == 0) {
+                        if (i == 0) bulk_wait_read<0>();
+                        else bulk_wait_read<1>();
+                    }
+                } else if (Cfg::LOADS_DIN) {
                     mbar_wait(&mybar[sb], dph[sb]);
                     dph[sb] ^= 1;
                 } else if (lane == 0) {
