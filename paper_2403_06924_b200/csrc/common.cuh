@@ -454,9 +454,12 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
     return r;
 }
+// Arrive on a barrier of another CTA of the cluster (the pair leader's TMEM
+// "empty" barriers).  Default .release.cta semantics: what it publishes is
+// TMEM reads, ordered by tcgen05.fence::before_thread_sync, not generic
+// memory, so no cluster-scope release fence (MEMBAR.ALL.GPU) is needed.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-                 : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
