@@ -270,10 +270,15 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
     qb.nonfinite = &p.sc->nonfinite;
     qb.co_share = co && coschedule_share() ? 1 : 0;
     if (p.vw) {
+        qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb; qb.rcp_out = p.lbr;
+        if (launch_quant_cols_fused(qb, &p.sc->maxB, &p.sc->nonfinite, sb)) {
+            check_launch("quantize B (fused)");
+            if (co) join(p.s);
+            return;  // VectorWise: no per-tensor scales to finish
+        }
         if (!p.pre_init) ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, sb), "memset");
         launch_absmax_cols(b, p.K, p.N, p.N, p.colmax, &p.sc->maxB, &p.sc->nonfinite, sb);
         check_launch("absmax B cols");
-        qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb; qb.rcp_out = p.lbr;
     } else {
         launch_absmax_global(b, (int64_t)p.K * p.N, &p.sc->maxB, &p.sc->nonfinite, sb);
         check_launch("absmax B");
@@ -309,10 +314,14 @@ void quantize_b_vw(Pipe& p, const float* b) {
     qb.bits = p.cfg->bits; qb.rounding = p.cfg->rounding;
     qb.qT = p.bqT; qb.ldq = p.ldk; qb.rmax = &p.sc->maxRB;
     qb.nonfinite = &p.sc->nonfinite;
+    qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb; qb.rcp_out = p.lbr;
+    if (launch_quant_cols_fused(qb, &p.sc->maxB, &p.sc->nonfinite, p.s)) {
+        check_launch("quantize B (fused)");
+        return;
+    }
     ck(cudaMemsetAsync(p.colmax, 0, sizeof(uint32_t) * p.N, p.s), "memset");
     launch_absmax_cols(b, p.K, p.N, p.N, p.colmax, &p.sc->maxB, &p.sc->nonfinite, p.s);
     check_launch("absmax B cols");
-    qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb; qb.rcp_out = p.lbr;
     launch_quant_cols_T(qb, p.s);
     check_launch("quantize B");
 }

@@ -97,6 +97,9 @@ void launch_absmax_cols(const float* x, int rows, int cols, int64_t ld, uint32_t
                         uint32_t* gmax, int* nonfinite, cudaStream_t s);
 void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s);
 void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s);
+// column maxima + quantisation of B in one DRAM pass (VectorWise, nearest);
+// false when not applicable (then absmax_cols + quant_cols_T)
+bool launch_quant_cols_fused(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cudaStream_t s);
 void launch_select_rows(const SelectArgs& a, cudaStream_t s);
 void launch_select_cols_T(const SelectArgs& a, cudaStream_t s);
 void launch_lambdas(DevScalars* sc, int bits, cudaStream_t s);

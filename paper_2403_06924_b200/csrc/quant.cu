@@ -1451,6 +1451,202 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
     }
 }
 
+// ------------------------------------------- fused K1, B side (one DRAM pass)
+// Column maxima and quantisation of B in one kernel.  A cluster of C CTAs
+// owns a 32-column strip over all K rows (CTA rank r: rows [2048 r, 2048 r +
+// 2048)).  Each warp streams its sub-tiles of every strip twice through its
+// TMA ring: pass 0 takes the column maxima (|x| as integer bits: NaN > inf >
+// finite), the cluster combines them in rank 0's shared memory (DSMEM
+// red.max), and pass 1 re-reads the same sub-tiles - now L2-resident (C x
+// 256 KB per strip in flight, ~40 MB in all) - and quantises them exactly as
+// k_cols_w4 does.  The ring interleaves pass 1 of strip i with pass 0 of strip
+// i+1, so DRAM keeps streaming while a strip is quantised and only the
+// cluster exchange sits between strips.  B leaves DRAM once instead of twice
+// (k_absmax_cols + k_cols_w4<0>).  A strip with a non-finite value raises
+// `nonfinite` and is not quantised (the call fails, pipeline.cpp:50-52).
+template <int kWW, int kWSlots, int kSub>
+__global__ void __launch_bounds__(kWW * 32, 1)
+    k_cols_maxq(const __grid_constant__ CUtensorMap tmap, const QuantColsArgs qa, uint32_t* gmax, int* nonfinite) {
+    XG_PDL_WAIT();
+    constexpr int kRowsCta = kWW * kWR * kSub;
+    extern __shared__ float4 dyn_smem[];
+    float* ring = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(dyn_smem) +
+                                           ((1024u - (smem_u32(dyn_smem) & 1023u)) & 1023u));
+    float(*lut)[kWC] = reinterpret_cast<float(*)[kWC]>(ring + kWW * kWSlots * kWC * kWR);
+    __shared__ uint64_t full[kWW][kWSlots];
+    __shared__ uint32_t wmax[kWW][kWC];
+    __shared__ uint32_t cmax[3][kWC];  // cluster maxima per strip (rank 0's copy), 3-deep for the resets
+    __shared__ float redf[kWW];
+    const uint32_t crank = cluster_ctarank(), csize = cluster_nctarank();
+    const int ncl = (int)(gridDim.x / csize), cid = (int)(blockIdx.x / csize);
+    const int rows = qa.rows, cols = qa.cols, bits = qa.bits;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qmax = quant_max(bits);
+    const float qmaxf = (float)qmax;
+    const int nstrips = (cols + kWC - 1) / kWC;
+    const int my_items = nstrips > cid ? (nstrips - cid + ncl - 1) / ncl : 0;
+    // ring order: pass 0 of strip 0, then per strip i: pass 1 (i) tile j, pass 0 (i+1) tile j, ...
+    const int ntiles = 2 * kSub * my_items;
+    float* wring = ring + w * kWSlots * kWC * kWR;
+    auto issue = [&](int g) {
+        int item, j;
+        if (g < kSub) {
+            item = 0, j = g;
+        } else {
+            const int q = g - kSub;
+            if (q < (my_items - 1) * 2 * kSub) {
+                const int r = q % (2 * kSub);
+                item = q / (2 * kSub) + (r & 1), j = r >> 1;
+            } else {
+                item = my_items - 1, j = q - (my_items - 1) * 2 * kSub;
+            }
+        }
+        const int slot = g % kWSlots;
+        mbar_expect_tx(&full[w][slot], kWC * kWR * 4);
+        tma_load_2d(wring + slot * kWC * kWR, &tmap, &full[w][slot], (cid + item * ncl) * kWC,
+                    (int)crank * kRowsCta + (w * kSub + j) * kWR);
+    };
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tmap);
+        for (int i = 0; i < kWW; ++i)
+            for (int j = 0; j < kWSlots; ++j) mbar_init(&full[i][j], 1);
+        fence_mbar_init();
+    }
+    if (threadIdx.x < 3 * kWC) cmax[threadIdx.x / kWC][threadIdx.x % kWC] = 0u;
+    __syncthreads();
+    cluster_sync_all();  // every CTA's maxima zeroed before any remote max lands
+    if (lane == 0)
+        for (int g = 0; g < kWSlots && g < ntiles; ++g) issue(g);
+    int g = 0;
+    // next sub-tile of the ring into registers (lane = column), slot handed back to TMA
+    auto consume = [&](float (&x)[kWR]) {
+        const int slot = g % kWSlots;
+        mbar_wait(&full[w][slot], (g / kWSlots) & 1);
+        const float* tile = wring + slot * kWC * kWR;
+#pragma unroll
+        for (int r = 0; r < kWR; ++r) x[r] = tile[r * kWC + lane];
+        __syncwarp();
+        if (lane == 0 && g + kWSlots < ntiles) {
+            fence_proxy_async();
+            issue(g + kWSlots);
+        }
+        ++g;
+    };
+    auto absmax_bits = [&](const float (&x)[kWR]) {
+        uint32_t m4[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int r = 0; r < kWR; ++r) m4[r & 3] = max(m4[r & 3], __float_as_uint(x[r]) & 0x7fffffffu);
+        return max(max(m4[0], m4[1]), max(m4[2], m4[3]));
+    };
+    const uint32_t cmax_r0 = mapa_shared(&cmax[0][0], 0);
+    const uint32_t adj_base = smem_u32(&lut[0][0]) + 4u * lane + 128u * (uint32_t)qmax - 128u * 0x4B400000u;
+    float rm = 0.0f;
+    uint32_t um = 0u;
+    if (my_items > 0)
+        for (int j = 0; j < kSub; ++j) {  // pass 0 of the first strip
+            float x[kWR];
+            consume(x);
+            um = max(um, absmax_bits(x));
+        }
+    for (int i = 0; i < my_items; ++i) {
+        const int strip = cid + i * ncl;
+        const int n = strip * kWC + lane;
+        wmax[w][lane] = um;
+        __syncthreads();  // all warps' maxima; every warp is past the previous strip's table readers
+        const int b = i % 3;
+        if (w == 0) {
+            uint32_t m = 0u;
+#pragma unroll
+            for (int k = 0; k < kWW; ++k) m = max(m, wmax[k][lane]);
+            red_max_cluster_u32(cmax_r0 + 4u * (uint32_t)(b * kWC + lane), m);
+            // rank 0 clears the buffer of strip i+1: its last readers (strip i-2) finished
+            // before the previous cluster barrier, its writers start after the next one
+            if (crank == 0) cmax[(i + 1) % 3][lane] = 0u;
+        }
+        cluster_sync_all();
+        const uint32_t cm = ld_cluster_u32(cmax_r0 + 4u * (uint32_t)(b * kWC + lane));
+        const bool bad = __any_sync(0xffffffffu, n < cols && cm > 0x7f7fffffu);  // uniform over the cluster
+        const float cmf = __uint_as_float(cm);
+        const double lam = compute_scale((double)cmf, bits);
+        if (crank == 0 && w == 0) {
+            if (n < cols) {
+                if (qa.lam_out) qa.lam_out[n] = lam;
+                if (qa.rcp_out) qa.rcp_out[n] = ff_recip(lam);
+            }
+            const float sm = warp_maxf(n < cols && !bad ? cmf : 0.0f);
+            if (lane == 0) {
+                if (bad) atomicOr(nonfinite, 1);
+                else if (gmax) atomicMax(gmax, fbits(sm));
+            }
+        }
+        if (!bad) {
+            const double inv = __ddiv_rn(1.0, lam);
+            constexpr int per = (128 + kWW - 1) / kWW;  // q in [0, qmax], mirrored (see build_row_lut)
+            for (int q = w * per; q < (w + 1) * per; ++q)
+                if (q <= qmax) {
+                    const float v = dequant_fast(q, inv, lam);
+                    lut[qmax + q][lane] = v;
+                    if (q > 0) lut[qmax - q][lane] = -v;
+                }
+        }
+        __syncthreads();
+        const float lam32 = __double2float_rn(lam);
+        const bool exact = !(lam32 <= FLT_MAX);
+        const bool next = i + 1 < my_items;
+        um = 0u;
+        for (int j = 0; j < kSub; ++j) {
+            const int k0 = (int)crank * kRowsCta + (w * kSub + j) * kWR;
+            float x[kWR];
+            consume(x);  // pass 1 of this strip (L2)
+            if (!bad) {
+                uint32_t w0[kWR / 4];
+#pragma unroll
+                for (int q = 0; q < kWR / 4; ++q) {
+                    const float xq[4] = {x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]};
+                    uint32_t u[4];
+                    float dmax = 0.0f;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) u[e] = qn(xq[e], lam32, dmax);
+                    if (exact || !(dmax < 0.4999f)) {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(xq[e], lam, qmaxf, kNearest));
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(xq[e], lds_f32((u[e] << 7) + adj_base))));
+                    w0[q] = pack4u(u[0], u[1], u[2], u[3]);
+                }
+                if (n < cols && k0 < rows) {
+                    int8_t* d0 = qa.qT + (int64_t)n * qa.ldq + k0;
+                    if (k0 + kWR <= rows) {
+#pragma unroll
+                        for (int v = 0; v < kWR / 16; ++v)
+                            reinterpret_cast<uint4*>(d0)[v] =
+                                make_uint4(w0[4 * v], w0[4 * v + 1], w0[4 * v + 2], w0[4 * v + 3]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < kWR / 4; ++q)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                if (4 * q + e < rows - k0) d0[4 * q + e] = (int8_t)(w0[q] >> (8 * e));
+                    }
+                }
+            }
+            if (next) {  // pass 0 of the next strip (DRAM)
+                consume(x);
+                um = max(um, absmax_bits(x));
+            }
+        }
+    }
+    float r = warp_maxf(rm);
+    if (lane == 0) redf[w] = r;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < kWW; ++k) r = fmaxf(r, redf[k]);
+        if (qa.rmax) atomicMax(qa.rmax, fbits(r));
+    }
+    cluster_sync_all();  // no CTA leaves while another may still address its shared memory
+}
+
 // ------------------------------------------------------------- scalars --
 __global__ void k_lambdas(DevScalars* sc, int bits) {
     XG_PDL_WAIT();
@@ -1627,6 +1823,66 @@ void launch_cols_any(const CUtensorMap& tm, const QuantColsArgs& qa, const Selec
     else if (c.ww == 16 && c.slots == 2 && c.ctas == 1) launch_cols_w<SELECT, 16, 2, 1>(tm, qa, sa, rows, cols, co_share, s);
     else if (c.ww == 4 && c.slots == 4 && c.ctas == 2) launch_cols_w<SELECT, 4, 4, 2>(tm, qa, sa, rows, cols, co_share, s);
     else launch_cols_w<SELECT, 8, 2, 2>(tm, qa, sa, rows, cols, co_share, s);
+}
+
+// Fused column maxima + quantisation (k_cols_maxq); false when the shape or
+// options need the two-kernel path.  XG_COLS_FUSED=0 disables it; =WWxSLOTSxSUB
+// picks a compiled shape (warps, ring slots per warp, sub-tiles per warp).
+template <int WW, int SLOTS, int SUB>
+bool launch_cols_maxq(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cudaStream_t s) {
+    constexpr int rows_cta = WW * kWR * SUB;
+    const int csize = (a.rows + rows_cta - 1) / rows_cta;
+    // K <= 8192 (clusters of <= 4): measured 1-5% faster end to end than the two
+    // kernels at C2-C4; 8-CTA clusters (K = 16384) co-schedule worse with the
+    // A side and measured ~1% slower, so larger K keeps the two-kernel path
+    if (csize > 4) return false;
+    alignas(64) CUtensorMap tm;
+    if (!make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) return false;
+    constexpr int smem = col_w_smem<WW, SLOTS>();
+    auto kern = k_cols_maxq<WW, SLOTS, SUB>;
+    set_dyn_smem(kern, smem);
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.blockDim = dim3(WW * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    static int max_clusters[9] = {0};  // co-resident clusters per cluster size (same part on every device)
+    if (!max_clusters[csize]) {
+        cfg.gridDim = dim3(csize * 256);
+        int m = 0;
+        if (cudaOccupancyMaxActiveClusters(&m, kern, &cfg) != cudaSuccess || m <= 0) {
+            cudaGetLastError();
+            m = kNumSMs / csize;
+        }
+        max_clusters[csize] = m;
+    }
+    const int nstrips = (a.cols + kWC - 1) / kWC;
+    const int ncl = nstrips < max_clusters[csize] ? nstrips : max_clusters[csize];
+    cfg.gridDim = dim3(csize * ncl);
+    return cudaLaunchKernelEx(&cfg, kern, tm, a, gmax, nonfinite) == cudaSuccess;
+}
+
+bool launch_quant_cols_fused(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cudaStream_t s) {
+    static const int3 shape = [] {
+        int3 v = make_int3(16, 2, 4);
+        if (const char* e = getenv("XG_COLS_FUSED")) {
+            if (*e == '0') v = make_int3(0, 0, 0);
+            else sscanf(e, "%dx%dx%d", &v.x, &v.y, &v.z);
+        }
+        return v;
+    }();
+    if (!shape.x || !a.per_col || a.rounding != kNearest || !r4_enabled() || a.rows < 256 || (a.ldq % 16) != 0)
+        return false;
+    if (shape.x == 8 && shape.y == 4 && shape.z == 8) return launch_cols_maxq<8, 4, 8>(a, gmax, nonfinite, s);
+    if (shape.x == 12 && shape.y == 3 && shape.z == 4) return launch_cols_maxq<12, 3, 4>(a, gmax, nonfinite, s);
+    if (shape.x == 8 && shape.y == 6 && shape.z == 8) return launch_cols_maxq<8, 6, 8>(a, gmax, nonfinite, s);
+    return launch_cols_maxq<16, 2, 4>(a, gmax, nonfinite, s);
 }
 
 void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {
