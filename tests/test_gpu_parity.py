@@ -404,6 +404,10 @@ def test_pipeline_nan_input_rejected():
         a[1, 2] = 0.0
         with pytest.raises(xg.InvalidArgument):
             xg.xigemm(a, b)
+        b[k - 1, n - 1] = 1.0
+        b[k // 2, n // 2] = float("-inf")  # a middle column strip of the fused B-side kernel
+        with pytest.raises(xg.InvalidArgument):
+            xg.xigemm(a, b)
     torch.cuda.synchronize()
 
 
@@ -431,3 +435,24 @@ def test_host_entry_overlapped_equals_device(shape):
     bad[m - 1, k - 1] = np.inf
     with pytest.raises(xg.InvalidArgument):
         xg.xigemm_host(bad, b, cfg=cfg)
+
+
+@pytest.mark.parametrize("k,n", [(256, 33), (300, 100), (2047, 64), (2049, 96), (5000, 1000), (8192, 200),
+                                 (4100, 31)])
+def test_fused_column_quantisation(oracle, k, n):
+    """K1 for B through the one-pass cluster kernel (quant.cu: k_cols_maxq, used
+    for VectorWise when K <= 8192): Bq, its column scales, max|RB| -> RBq match
+    the oracle bit for bit on ragged K (cluster of 1-4 CTAs, partial sub-tiles)
+    and ragged N (partial column strips)."""
+    m = 40
+    a = ol.random_dense(m, k, k + 1, -3, 3)
+    b = ol.random_dense(k, n, k + n, -5, 5)
+    b[k // 2, n // 3] = 40.0  # one dominant column
+    cfg = xg.XigemmConfig(threshold=0.05, density_limit=0.3, scheme=xg.QuantScheme.VectorWise,
+                          policy=xg.ReductionPolicy.AvgRule)
+    rep, d = xg.xigemm_dump(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), cfg)
+    rc, bq, lb = oracle.quantize(b, 8, 2, 1)
+    assert rc == 0 and beq(d["bq"], bq) and beq(d["bq_scales"], lb)
+    rc, rb = oracle.residual(b, bq, lb, 2)
+    rc, rbq, lrb = oracle.quantize(rb, 8, 0, 1)
+    assert beq(d["rbq"], rbq) and beq(d["rbq_scale"], lrb)
