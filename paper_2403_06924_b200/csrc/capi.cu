@@ -427,6 +427,9 @@ void gemm_comp(Pipe& p, float* out, const float* c, float alpha, float beta) {
         }();
         if (!split) {  // one launch, both terms per tile (TMEM buffers alternate by term)
             g.dual = 1;
+            // two operand pairs live per tile: half the raster group of the single GEMM
+            // keeps more of them in L2 (measured at C3: 8 -> 0.712 ms, 16 -> 0.720, 4 -> 0.738)
+            g.group_m = 8;
             gemm_i8(EPI_ACC, ops, isb, 6, g, p.s);
             check_launch("gemm compensate");
             return;

@@ -125,7 +125,7 @@ void run2(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, 
     static const int env_dbg = [] { const char* e = getenv("XG_GEMM_DEBUG"); return e ? atoi(e) : 0; }();
     GemmArgs a2 = args;
     a2.debug |= env_dbg;
-    if (a2.group_m <= 0) a2.group_m = env_gm;
+    if (env_gm > 0) a2.group_m = env_gm;  // tuning aid overrides the caller's choice
     if (a2.pf_dist <= 0) a2.pf_dist = env_pf >= 0 ? env_pf : kDefaultPrefetch;
     EpiMaps em;
     std::memset(&em, 0, sizeof em);
