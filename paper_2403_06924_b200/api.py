@@ -144,7 +144,9 @@ def _p(t) -> C.c_void_p:
 
 
 def _s() -> C.c_void_p:
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    # the raw handle of the current stream without building a torch Stream object
+    # (a few microseconds per call on the pipeline's latency-bound host path)
+    return C.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
 
 
 def _nscales(scheme, rows, cols) -> int:
@@ -404,9 +406,16 @@ def get_abs_min_vectors(d):
     return _ret(r, host), _ret(c, host)
 
 
+def _fast_dev(x) -> bool:  # already a contiguous fp32 CUDA tensor: used as is
+    return isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
+
+
 def _pipeline(a, b, c, alpha, beta, cfg: XigemmConfig, reduce: bool, dump: bool, out=None):
-    x, host = _dev(a, torch.float32)
-    y, _ = _dev(b, torch.float32)
+    if _fast_dev(a) and _fast_dev(b):
+        x, host, y = a, False, b
+    else:
+        x, host = _dev(a, torch.float32)
+        y, _ = _dev(b, torch.float32)
     if x.dim() != 2 or y.dim() != 2 or x.shape[1] != y.shape[0]:
         raise InvalidArgument("xigemm: inner dimensions do not match")
     m, k = x.shape

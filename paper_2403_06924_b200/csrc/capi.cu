@@ -175,6 +175,7 @@ struct Pipe {
     float2 *lar = nullptr, *lbr = nullptr;  // ff_recip of la / lb (VectorWise), may be null
     uint32_t* colmax;
     bool pre_init = false;  // colmax / statistics accumulators already initialised
+    unsigned long long *stamp_df = nullptr, *stamp_comp = nullptr;  // DevScalars::ts slots of the GEMMs
 };
 
 // Second stream for the independent A-side / B-side memory-bound kernels of
@@ -335,6 +336,7 @@ void gemm_df(Pipe& p, float* out) {
     g.amap[0][0] = g.amap[0][1] = 0;
     g.bmap[0][0] = g.bmap[0][1] = 1;
     g.out_f32 = out;
+    g.stamp = p.stamp_df;
     g.rs[0][0] = g.rs[0][1] = p.vw ? sref(p.la, 1, p.lar) : sref(&p.sc->lamA, 0, &p.sc->rA);
     g.cs[0][0] = g.cs[0][1] = p.vw ? sref(p.lb, 1, p.lbr) : sref(&p.sc->lamB, 0, &p.sc->rB);
     gemm_i8(EPI_DF, ops, isb, 2, g, p.s);
@@ -427,6 +429,7 @@ void gemm_comp(Pipe& p, float* out, const float* c, float alpha, float beta) {
         }();
         if (!split) {  // one launch, both terms per tile (TMEM buffers alternate by term)
             g.dual = 1;
+            g.stamp = p.stamp_comp;
             // two operand pairs live per tile: half the raster group of the single GEMM
             // keeps more of them in L2 (measured at C3: 8 -> 0.712 ms, 16 -> 0.720, 4 -> 0.738)
             g.group_m = 8;
@@ -555,11 +558,13 @@ int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* du
     p.aq = w.aq; p.raq = w.raq; p.ared = w.ared;
     p.bqT = w.bqT; p.rbqT = w.rbqT; p.bredT = w.bredT;
     p.la = w.la; p.lb = w.lb; p.lar = w.lar; p.lbr = w.lbr; p.colmax = w.colmax;
+    p.stamp_df = &w.sc->ts[1];
+    p.stamp_comp = &w.sc->ts[3];
     const int M = q.M, K = q.K, N = q.N;
     p.pre_init = true;  // stage 0 initialises everything in one launch
     if (stage == 0) {
         xg::launch_pipe_init(p.sc, sizeof(xg::DevScalars), p.colmax, N, w.rsum, w.csum, w.rstat, w.cstat, M,
-                             q.cfg.policy, q.reduce, s);
+                             q.cfg.policy, q.reduce, s, &w.sc->ts[0]);
         check_launch("init");
         if (q.c) {
             xg::finite_max(q.c, (int64_t)M * N, &p.sc->retB /*scratch, reset below*/, &p.sc->nonfinite, s);
@@ -790,13 +795,24 @@ void finish_report(const xg::DevScalars& h, int reduce, EventTimer& tm, xg_repor
         rep->path = h.path;
         rep->nnz_a = reduce ? (int64_t)h.nnzA : 0;
         rep->nnz_b = reduce ? (int64_t)h.nnzB : 0;
-        rep->ns_quant = tm.ns(0, 1);
-        rep->ns_xxmm = tm.ns(1, 2) + tm.ns(3, 4);
-        rep->ns_reduce = tm.ns(2, 3);
+        // stage times from the kernels' own %globaltimer stamps when all were
+        // written (pair GEMM path): no host event queries after the wait, which
+        // measured ~17 us of idle GPU per call; the graph's events otherwise
+        const unsigned long long* t = h.ts;
+        if (t[0] && t[1] >= t[0] && t[2] >= t[1] && t[3] >= t[2] && t[4] >= t[3]) {
+            rep->ns_quant = (double)(t[1] - t[0]);
+            rep->ns_gemm_df = (double)(t[2] - t[1]);
+            rep->ns_reduce = (double)(t[3] - t[2]);
+            rep->ns_gemm_comp = (double)(t[4] - t[3]);
+        } else {
+            rep->ns_quant = tm.ns(0, 1);
+            rep->ns_gemm_df = tm.ns(1, 2);
+            rep->ns_reduce = tm.ns(2, 3);
+            rep->ns_gemm_comp = tm.ns(3, 4);
+        }
+        rep->ns_xxmm = rep->ns_gemm_df + rep->ns_gemm_comp;
         rep->ns_package = 0.0;
         rep->stats_fallbacks = h.nflag;
-        rep->ns_gemm_df = tm.ns(1, 2);
-        rep->ns_gemm_comp = tm.ns(3, 4);
     }
 }
 

@@ -71,6 +71,7 @@ struct GemmArgs {
                    // out = fl(din + deq); term 1: [1], finalize), TMEM buffers alternate by term
     int group_m;   // pair kernel: tile-raster group height in 256-row units (0: default)
     int pf_dist;   // pair kernel: L2 prefetch distance in k-blocks (0: off)
+    unsigned long long* stamp;  // pair kernel: [0] %globaltimer at begin, [1] max at CTA exit (null: off)
 };
 
 template <int BN, int NACC>
@@ -470,6 +471,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tmem_base = *tmem_slot;
     // everything above overlaps the predecessor's tail under a programmatic edge
     XG_PDL_WAIT();
+    if (args.stamp && blockIdx.x == 0 && threadIdx.x == 0) args.stamp[0] = globaltimer_ns();
     const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
     const int nterms = (EPI == EPI_ACC && args.dual) ? 2 : 1;
 
@@ -785,6 +787,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         tmem_dealloc2(tmem_base, Cfg::TMEM_COLS);
     }
+    if (args.stamp && threadIdx.x == 128) atomicMax(&args.stamp[1], globaltimer_ns());  // stores landed above
 }
 
 }  // namespace xg

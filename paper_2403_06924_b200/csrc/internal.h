@@ -26,6 +26,9 @@ struct DevScalars {
     // float-float reciprocals (common.cuh: ff_recip) of the per-tensor scales above,
     // written next to them so the GEMM epilogues do no fp64 division
     float2 rA, rB, rRA, rRB, rAred, rBred;
+    // %globaltimer stamps of the graph path's stage boundaries (ns): pipeline
+    // start, D_F GEMM begin / end, compensation begin / end; 0 = not written
+    unsigned long long ts[5];
 };
 
 struct QuantRowsArgs {
@@ -130,7 +133,8 @@ void launch_stats(const float* d, int rows, int cols, int policy, float* row_sta
                   cudaStream_t s, const StatsDefer* def = nullptr);
 // zero the device scalars / column maxima and initialise the statistics accumulators
 void launch_pipe_init(void* sc, int sc_bytes, uint32_t* colmax, int N, double* rsum, double* csum,
-                      float* rstat, float* cstat, int M, int policy, int reduce, cudaStream_t s);
+                      float* rstat, float* cstat, int M, int policy, int reduce, cudaStream_t s,
+                      unsigned long long* ts0 = nullptr);
 // the two halves of launch_stats, split around the row-sharded column reduction
 // mode 0: initialise + accumulate; 1: initialise only; 2: accumulate only (row
 // pointers offset to a row chunk, column accumulators shared by all chunks)

@@ -216,8 +216,11 @@ __global__ void k_zero(double* a, int na, double* b, int nb, int* n) {
 // device scalars, column-max accumulators and the statistics accumulators
 // (fp64 sums for AvgRule, FLT_MAX bit patterns for MinRule).
 __global__ void k_pipe_init(uint32_t* sc, int sc_words, uint32_t* colmax, int N, double* rsum,
-                            double* csum, uint32_t* rmin, uint32_t* cmin, int M, int policy, int reduce) {
+                            double* csum, uint32_t* rmin, uint32_t* cmin, int M, int policy, int reduce,
+                            unsigned long long* ts0) {
     XG_PDL_WAIT();
+    unsigned long long t0 = 0;
+    if (ts0 && blockIdx.x == 0 && threadIdx.x == 0) t0 = globaltimer_ns();
     const int n = max(max(M, N), sc_words);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         if (i < sc_words) sc[i] = 0u;
@@ -232,16 +235,21 @@ __global__ void k_pipe_init(uint32_t* sc, int sc_words, uint32_t* colmax, int N,
             }
         }
     }
+    if (ts0 && blockIdx.x == 0) {  // the scalars (block 0's range) are zero: stamp the start
+        __syncthreads();
+        if (threadIdx.x == 0) *ts0 = t0;
+    }
 }
 
 void launch_pipe_init(void* sc, int sc_bytes, uint32_t* colmax, int N, double* rsum, double* csum,
-                      float* rstat, float* cstat, int M, int policy, int reduce, cudaStream_t s) {
+                      float* rstat, float* cstat, int M, int policy, int reduce, cudaStream_t s,
+                      unsigned long long* ts0) {
     const int n = M > N ? M : N;
     int blocks = (n + 255) / 256;
     blocks = blocks < 1 ? 1 : blocks > 1024 ? 1024 : blocks;
     k_pipe_init<<<blocks, 256, 0, s>>>(reinterpret_cast<uint32_t*>(sc), sc_bytes / 4, colmax, N, rsum, csum,
                                         reinterpret_cast<uint32_t*>(rstat), reinterpret_cast<uint32_t*>(cstat), M,
-                                        policy, reduce);
+                                        policy, reduce, ts0);
 }
 
 void launch_stats_partial(const float* d, int rows, int cols, int policy, float* row_stat,
