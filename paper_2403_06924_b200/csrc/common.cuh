@@ -301,7 +301,21 @@ __device__ __forceinline__ T warp_sum(T v) {
 // Programmatic dependent launch: a kernel that may be started before its
 // predecessor in the graph has finished (programmatic edge) waits here before
 // touching any memory the predecessor writes.  A no-op without such an edge.
+// Programmatic dependent launch: wait for the predecessor grid (and its
+// memory), then let the successor grid launch at once - its CTAs run their
+// prologue where resources free up and park in their own wait, instead of
+// being launched only when this grid has exited.  XG_PDL_EARLY=0 at build
+// time keeps the implicit trigger at grid completion.
+#ifndef XG_PDL_EARLY
+#define XG_PDL_EARLY 1
+#endif
+#if XG_PDL_EARLY
+#define XG_PDL_WAIT() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+#else
 #define XG_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#endif
+// wait only (successor launched at grid completion): the persistent GEMMs
+#define XG_PDL_WAIT_ONLY() asm volatile("griddepcontrol.wait;" ::: "memory")
 
 // --------------------------------------------------------------- PTX: misc --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

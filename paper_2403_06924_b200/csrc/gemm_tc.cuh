@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    XG_PDL_WAIT();
+    XG_PDL_WAIT_ONLY();
     const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
 
     if (warp == 0) {
@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     // everything above overlaps the predecessor's tail under a programmatic edge
-    XG_PDL_WAIT();
+    XG_PDL_WAIT_ONLY();
     if (args.stamp && blockIdx.x == 0 && threadIdx.x == 0) args.stamp[0] = globaltimer_ns();
     const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
     const int nterms = (EPI == EPI_ACC && args.dual) ? 2 : 1;
