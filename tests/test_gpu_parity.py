@@ -456,3 +456,45 @@ def test_fused_column_quantisation(oracle, k, n):
     rc, rb = oracle.residual(b, bq, lb, 2)
     rc, rbq, lrb = oracle.quantize(rb, 8, 0, 1)
     assert beq(d["rbq"], rbq) and beq(d["rbq_scale"], lrb)
+
+
+def test_concurrent_calls_from_threads():
+    """The C-ABI is re-entrant (SURVEY 8(b) threading contract): several host
+    threads calling xigemm at once - same shape (one takes the cached graph,
+    the others the stream-ordered eager path) and different shapes/configs -
+    each get exactly their sequential result."""
+    import threading
+    cases = []
+    for i, (m, k, n) in enumerate([(512, 1024, 384), (512, 1024, 384), (300, 2048, 260), (1024, 512, 1000),
+                                   (512, 1024, 384), (777, 1536, 129)]):
+        a = torch.from_numpy(ol.random_dense(m, k, 100 + i, -3, 3)).cuda()
+        b = torch.from_numpy(ol.random_dense(k, n, 200 + i, -3, 3)).cuda()
+        cfg = xg.XigemmConfig(threshold=0.05, density_limit=0.3, scheme=xg.QuantScheme.VectorWise,
+                              policy=xg.ReductionPolicy.AvgRule if i % 2 == 0 else xg.ReductionPolicy.MinRule)
+        cases.append((a, b, cfg))
+    want = [xg.xigemm(a, b, cfg=cfg) for a, b, cfg in cases]
+    torch.cuda.synchronize()
+    got = [None] * len(cases)
+    errs = []
+
+    def run(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    a, b, cfg = cases[i]
+                    r = xg.xigemm(a, b, cfg=cfg)
+                s.synchronize()
+                got[i] = r
+        except Exception as e:  # noqa: BLE001 - reported below
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(len(cases))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for w, g in zip(want, got):
+        assert beq(g.result, w.result)
+        assert (g.density_a, g.density_b, int(g.path)) == (w.density_a, w.density_b, int(w.path))
