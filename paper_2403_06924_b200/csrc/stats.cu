@@ -18,7 +18,7 @@ namespace xg {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kSlabRows = 32;
+constexpr int kSlabRows = 64;  // rows per CTA (measured at C3: 64 -> 56.9 us, 32 -> 61.1; half the column atomics)
 
 // One pass over D_F: each thread owns 4 adjacent columns of a 32-row slab.
 template <int POLICY>
@@ -165,6 +165,9 @@ __global__ void __launch_bounds__(kFallbackThreads)
             const float tlo = float_above(__dmul_rn(def.thr_m, (double)lo));
             const float thi = float_above(__dmul_rn(def.thr_m, (double)hi));
             int amb = 0;
+            // unrolled so a thread's loads (strided for a column) are all in flight at
+            // once instead of one DRAM round trip per iteration (9.6 -> ~3 us at C3)
+#pragma unroll 8
             for (int t = threadIdx.x; t < def.inner; t += kFallbackThreads) {
                 const float x = is_row ? def.a[(int64_t)idx * def.lda + t]
                                        : def.b[(int64_t)t * def.ldb + (idx - rows)];
