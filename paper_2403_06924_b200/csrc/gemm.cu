@@ -85,14 +85,14 @@ void run(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, c
     kern<<<grid, 256, Cfg::SMEM_BYTES, s>>>(maps, args);
 }
 
-template <int NACC, int EPI, int PAIRS>
+template <int NACC, int EPI, int PAIRS, int ST = 0>
 void run2(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, cudaStream_t s) {
-    using Cfg = Gemm2Cfg<NACC, EPI>;
+    using Cfg = Gemm2Cfg<NACC, EPI, ST>;
     TmaMaps maps;
     std::memset(&maps, 0, sizeof maps);
     for (int i = 0; i < nops; ++i) encode(&maps.m[i], ops[i], args.K, is_b[i] ? 128 / PAIRS : 128);
     for (int i = nops; i < kMaxMaps; ++i) maps.m[i] = maps.m[0];
-    auto kern = k_gemm_i8_tc2<NACC, EPI, PAIRS>;
+    auto kern = k_gemm_i8_tc2<NACC, EPI, PAIRS, ST>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     const int csize = 2 * PAIRS;
     const int tiles = ((args.M + 256 * PAIRS - 1) / (256 * PAIRS)) * ((args.N + 255) / 256);
@@ -173,7 +173,10 @@ void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const Gemm
         switch (epi) {
             case EPI_DF: mc ? run2<1, EPI_DF, 2>(ops, is_b, nops, args, s) : run2<1, EPI_DF, 1>(ops, is_b, nops, args, s); return;
             case EPI_COMP: mc ? run2<2, EPI_COMP, 2>(ops, is_b, nops, args, s) : run2<2, EPI_COMP, 1>(ops, is_b, nops, args, s); return;
-            case EPI_ACC: run2<1, EPI_ACC, 1>(ops, is_b, nops, args, s); return;
+            case EPI_ACC:  // 4 stages where the epilogue bounds the tile (K <= 4096), see Gemm2Cfg
+                if (args.K <= 4096) run2<1, EPI_ACC, 1, 4>(ops, is_b, nops, args, s);
+                else run2<1, EPI_ACC, 1>(ops, is_b, nops, args, s);
+                return;
         }
     }
     switch (epi) {

@@ -380,7 +380,7 @@ namespace xg {
 // (128+256) for the 1-CTA 128x256 tile: 64 B/clk/SM at full MMA rate.  The
 // accumulator rows 0-127 land in the leader's TMEM, 128-255 in the peer's.
 // 8 epilogue warps (two per TMEM lane quadrant, one per 128-column half).
-template <int NACC, int EPI = EPI_DF>
+template <int NACC, int EPI = EPI_DF, int ST = 0>
 struct Gemm2Cfg {
     static constexpr int BM = 128;   // rows per CTA (pair M = 256)
     static constexpr int BN = 256;   // pair N
@@ -390,7 +390,12 @@ struct Gemm2Cfg {
     static constexpr int B_BYTES = BNH * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr bool LOADS_DIN = EPI == EPI_COMP || EPI == EPI_ACC;
-    static constexpr int STAGES = LOADS_DIN ? 4 : 5;
+    // 5 stages but for the two-accumulator EPI_COMP (no room): the D_F GEMM at 4
+    // stages is 11% slower at 8192^3, the compensation GEMM 0.711 -> 0.639 ms
+    // with the fifth; ST overrides (the launcher picks 4 for the compensation at
+    // K <= 4096, where its epilogue, not the MMA, bounds the tile: 5 measured
+    // 1.04 -> 1.09 ms at C4)
+    static constexpr int STAGES = ST > 0 ? ST : ((LOADS_DIN && NACC > 1) ? 4 : 5);
     static constexpr int ACC_COLS = NACC * BN;
     static constexpr int ACC_BUFS = (512 / ACC_COLS) >= 2 ? 2 : 1;
     static constexpr int TMEM_COLS = 512;
@@ -402,7 +407,14 @@ struct Gemm2Cfg {
     static constexpr int STG_BYTES = 32 * 32 * 4;
     static constexpr int EPI_BYTES = EPI_WARPS * NSTG * STG_BYTES;
     static constexpr int SCL_BYTES = EPI_WARPS * NACC * 32 * 8;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + SCL_BYTES + 1024 + 512;
+    // alignment slack for the 1024-byte (128B-swizzle) tiles: the dynamic window
+    // starts after the driver's 1 KiB on sm_100, so none is consumed in practice;
+    // the kernel traps if more than the slack would be needed
+    static constexpr int ALIGN_SLACK = LOADS_DIN ? 512 : 1024;
+    static constexpr int BAR_BYTES = 256;  // 2*STAGES + 4 + 2*EPI_WARPS mbarriers + the TMEM slot
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + SCL_BYTES + ALIGN_SLACK + BAR_BYTES;
+    static_assert(SMEM_BYTES <= 232448, "shared memory over the 227 KiB per-block limit");
+    static_assert((2 * STAGES + 4 + 2 * EPI_WARPS) * 8 + 4 <= BAR_BYTES, "barrier area");
     static constexpr int GROUP_M = 16;  // in 256-row units (measured: 16 > 8 > 32 at 8192^3)
     static_assert(ACC_COLS * ACC_BUFS <= 512, "TMEM overflow");
 };
@@ -415,15 +427,17 @@ struct Gemm2Cfg {
 // Epilogue: TMEM -> registers -> exact dequant -> 128B-swizzled smem tile ->
 // TMA store; EPI_COMP prefetches its D_F tile by TMA into the same staging
 // tile while the accumulator is still being produced.
-template <int NACC, int EPI, int PAIRS>
+template <int NACC, int EPI, int PAIRS, int ST = 0>
 __global__ void __launch_bounds__(384, 1)
     k_gemm_i8_tc2(const __grid_constant__ TmaMaps maps, const GemmArgs args,
                   const __grid_constant__ EpiMaps emaps) {
-    using Cfg = Gemm2Cfg<NACC, EPI>;
+    using Cfg = Gemm2Cfg<NACC, EPI, ST>;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment by pointer arithmetic on the shared array (not through
     // uintptr_t) so the compiler keeps shared-space accesses (LDS/STS, not LD/ST)
-    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+    if (pad > (uint32_t)Cfg::ALIGN_SLACK) __trap();  // see Gemm2Cfg::ALIGN_SLACK
+    uint8_t* smem = smem_raw + pad;
     float* epi_stage = (float*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);  // 1024-aligned
     double* epi_scale = (double*)((uint8_t*)epi_stage + Cfg::EPI_BYTES);
     uint64_t* full = (uint64_t*)((uint8_t*)epi_scale + Cfg::SCL_BYTES);
