@@ -44,14 +44,16 @@ void encode(CUtensorMap* m, const KOperand& op, int K, int box_rows) {
         throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
-// fp32 M x N row-major matrix, 32x32 boxes, 128-byte swizzle (epilogue tiles)
-void encode_f32_sw128(CUtensorMap* m, const float* p, int rows, int cols) {
+// fp32 M x N row-major matrix, 32-row boxes of box_cols (32: 128-byte swizzle,
+// 16: 64-byte swizzle) - the epilogue staging tiles
+void encode_f32_sw128(CUtensorMap* m, const float* p, int rows, int cols, int box_cols = 32) {
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
-    cuuint32_t box[2] = {32, 32};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, 32};
     cuuint32_t estr[2] = {1, 1};
     const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, estr,
-                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         throw std::runtime_error("cuTensorMapEncodeTiled (f32) failed: " + std::to_string((int)r));
@@ -129,8 +131,9 @@ void run2(const KOperand* ops, const int* is_b, int nops, const GemmArgs& args, 
     if (a2.pf_dist <= 0) a2.pf_dist = env_pf >= 0 ? env_pf : kDefaultPrefetch;
     EpiMaps em;
     std::memset(&em, 0, sizeof em);
-    encode_f32_sw128(&em.out, args.out_f32, args.M, args.N);
-    encode_f32_sw128(&em.din, (EPI == EPI_COMP || EPI == EPI_ACC) ? args.df_in : args.out_f32, args.M, args.N);
+    encode_f32_sw128(&em.out, args.out_f32, args.M, args.N, Cfg::CHW);
+    encode_f32_sw128(&em.din, (EPI == EPI_COMP || EPI == EPI_ACC) ? args.df_in : args.out_f32, args.M, args.N,
+                     Cfg::CHW);
     cudaLaunchKernelEx(&cfg, kern, maps, a2, em);
 }
 

@@ -395,7 +395,11 @@ struct Gemm2Cfg {
     // with the fifth; ST overrides (the launcher picks 4 for the compensation at
     // K <= 4096, where its epilogue, not the MMA, bounds the tile: 5 measured
     // 1.04 -> 1.09 ms at C4)
-    static constexpr int STAGES = ST > 0 ? ST : ((LOADS_DIN && NACC > 1) ? 4 : 5);
+    static constexpr int STAGES = ST > 0 ? ST : (LOADS_DIN ? (NACC > 1 ? 4 : 6) : 5);
+    // epilogue chunk width (columns per TMEM load / staging tile): 16 for the
+    // six-stage compensation GEMM, whose two 32x16 staging tiles per warp leave
+    // room for the sixth stage (64B-swizzled tiles), else 32 (128B swizzle)
+    static constexpr int CHW = (EPI == EPI_ACC && STAGES == 6) ? 16 : 32;
     static constexpr int ACC_COLS = NACC * BN;
     static constexpr int ACC_BUFS = (512 / ACC_COLS) >= 2 ? 2 : 1;
     static constexpr int TMEM_COLS = 512;
@@ -404,14 +408,14 @@ struct Gemm2Cfg {
     // per epilogue warp: NSTG staging tiles of 32x32 fp32 (128B-swizzled, TMA
     // store / load) and NACC x 32 float-float column reciprocals
     static constexpr int NSTG = LOADS_DIN ? 2 : 1;
-    static constexpr int STG_BYTES = 32 * 32 * 4;
+    static constexpr int STG_BYTES = 32 * CHW * 4;
     static constexpr int EPI_BYTES = EPI_WARPS * NSTG * STG_BYTES;
     static constexpr int SCL_BYTES = EPI_WARPS * NACC * 32 * 8;
     // alignment slack for the 1024-byte (128B-swizzle) tiles: the dynamic window
     // starts after the driver's 1 KiB on sm_100, so none is consumed in practice;
     // the kernel traps if more than the slack would be needed
     static constexpr int ALIGN_SLACK = LOADS_DIN ? 512 : 1024;
-    static constexpr int BAR_BYTES = 256;  // 2*STAGES + 4 + 2*EPI_WARPS mbarriers + the TMEM slot
+    static constexpr int BAR_BYTES = STAGES > 5 ? 512 : 256;  // 2*STAGES + 4 + 2*EPI_WARPS mbarriers + the TMEM slot
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + SCL_BYTES + ALIGN_SLACK + BAR_BYTES;
     static_assert(SMEM_BYTES <= 232448, "shared memory over the 227 KiB per-block limit");
     static_assert((2 * STAGES + 4 + 2 * EPI_WARPS) * 8 + 4 <= BAR_BYTES, "barrier area");
@@ -590,12 +594,16 @@ __global__ void __launch_bounds__(384, 1)
         const int half = (warp - 4) >> 2;  // 128-column half of the tile
         const int we = warp - 4;           // epilogue warp index 0..7
         const uint32_t tempty_leader0 = mapa_shared(&tempty[0], rank & ~1u);
-        float* stg[2] = {epi_stage + we * Cfg::NSTG * 1024,
-                         epi_stage + (we * Cfg::NSTG + Cfg::NSTG - 1) * 1024};
+        constexpr int CW = Cfg::CHW;  // chunk width (columns)
+        constexpr int KV = CW / 4;     // 16-byte units per staged row
+        float* stg[2] = {epi_stage + we * Cfg::NSTG * (32 * CW),
+                         epi_stage + (we * Cfg::NSTG + Cfg::NSTG - 1) * (32 * CW)};
         float2* scw = reinterpret_cast<float2*>(epi_scale) + we * NACC * 32;
         uint64_t* mybar = dbar + 2 * we;
         uint32_t dph[2] = {0, 0};
-        const int sw = lane & 7;  // 128B swizzle: chunk k of row `lane` sits at k ^ (lane & 7)
+        // 128B swizzle (32 columns): unit k of row `lane` sits at k ^ (lane & 7);
+        // 64B swizzle (16 columns): at k ^ ((lane >> 1) & 3)
+        const int sw = CW == 32 ? (lane & 7) : ((lane >> 1) & 3);
         int buf = 0;
         uint32_t bphase = 0;
         for (int t = cluster_id; t < num_tiles; t += nclusters)
@@ -608,7 +616,7 @@ __global__ void __launch_bounds__(384, 1)
             const int row = rowbase + lane;
             const bool row_ok = row < args.M;
             const int colbase = nb * Cfg::BN + half * (Cfg::BN / 2);
-            const int nchunk = (args.debug & 2) ? 0 : min(Cfg::BN / 2 / 32, (args.N - colbase + 31) / 32);
+            const int nchunk = (args.debug & 2) ? 0 : min(Cfg::BN / 2 / CW, (args.N - colbase + CW - 1) / CW);
             // Dual term 1 reads back what term 0 just produced.  It walks the chunks
             // in reverse: the last two term-0 chunks are still in their staging
             // tiles (chunk c in stg[c & 1]) and are updated in place; older ones
@@ -638,7 +646,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 1
             for (int i = 0; i < nchunk; ++i) {
                 const int c = rev ? nchunk - 1 - i : i;
-                const int col0 = colbase + c * 32;
+                const int col0 = colbase + c * CW;
                 const int sb = (Cfg::NSTG == 2) ? (c & 1) : 0;
                 float* tile = stg[sb];
                 const bool resident = rev && i < 2;
@@ -651,15 +659,15 @@ __global__ void __launch_bounds__(384, 1)
                     }
                     bulk_wait_read<0>();
                     mbar_expect_tx(&mybar[cn & 1], Cfg::STG_BYTES);
-                    tma_load_2d(stg[cn & 1], &emaps.din, &mybar[cn & 1], colbase + cn * 32, rowbase);
+                    tma_load_2d(stg[cn & 1], &emaps.din, &mybar[cn & 1], colbase + cn * CW, rowbase);
                 }
                 // column reciprocals of this chunk, broadcast through shared memory
                 const int mycol = min(col0 + lane, args.N - 1);
                 scw[lane] = args.cs[ts][sel].rcp(mycol);
                 if (NACC > 1) scw[32 + lane] = args.cs[1][sel].rcp(mycol);
-                uint32_t acc[NACC][32];
+                uint32_t acc[NACC][CW];
 #pragma unroll
-                for (int a = 0; a < NACC; ++a) tmem_ld32(tbase + a * Cfg::BN + c * 32, acc[a]);
+                for (int a = 0; a < NACC; ++a) tmem_ld_cols<CW>(tbase + a * Cfg::BN + c * CW, acc[a]);
                 tmem_ld_wait();
                 if (i == nchunk - 1) {  // accumulator drained: hand TMEM back to the MMA early
                     tc_fence_before();
@@ -679,24 +687,24 @@ __global__ void __launch_bounds__(384, 1)
                     bulk_wait_read<0>();  // staging tile free again
                 }
                 __syncwarp();
-                float4* rowp = reinterpret_cast<float4*>(tile + lane * 32);
-                float res[32];
+                float4* rowp = reinterpret_cast<float4*>(tile + lane * CW);
+                float res[CW];
                 if constexpr (EPI == EPI_DF) {
                     bool slow = false;
                     if (args.debug & 64) {  // probe: no dequant math
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) res[j] = __int_as_float(acc[0][j]);
+                        for (int j = 0; j < CW; ++j) res[j] = __int_as_float(acc[0][j]);
                     } else if (args.debug & 128) {  // probe: fp32 math of similar count
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) res[j] = __fmul_rn(__fmul_rn((float)(int32_t)acc[0][j], i0.x), scw[j].x);
+                        for (int j = 0; j < CW; ++j) res[j] = __fmul_rn(__fmul_rn((float)(int32_t)acc[0][j], i0.x), scw[j].x);
                     } else {
                         uint32_t sm = 0;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) res[j] = dq_ff24((int32_t)acc[0][j], i0, scw[j], sm, 1u << j);
+                        for (int j = 0; j < CW; ++j) res[j] = dq_ff24((int32_t)acc[0][j], i0, scw[j], sm, 1u << j);
                         if (sm) {  // rare: exact redo of the flagged elements
                             const ScaleRef c0 = args.cs[0][sel];
 #pragma unroll
-                            for (int j = 0; j < 32; ++j)
+                            for (int j = 0; j < CW; ++j)
                                 if (sm & (1u << j))
                                     res[j] = dq_slow((int32_t)acc[0][j], i0, scw[j], r0, c0.at(min(col0 + j, args.N - 1)));
                         }
@@ -707,19 +715,19 @@ __global__ void __launch_bounds__(384, 1)
                     // In place over res[] (register budget: 168/thread); the rare
                     // exact redo re-reads din from the staging tile.
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
+                    for (int k = 0; k < KV; ++k) {
                         const float4 d = rowp[k ^ sw];
                         res[4 * k] = d.x; res[4 * k + 1] = d.y; res[4 * k + 2] = d.z; res[4 * k + 3] = d.w;
                     }
                     uint32_t sm = 0;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
+                    for (int j = 0; j < CW; ++j)
                         res[j] = __fadd_rn(res[j], dq_ff24((int32_t)acc[0][j], i0, scw[j], sm, 1u << j));
                     if (sm) {  // rare: exact redo of the flagged elements
                         const ScaleRef c0 = args.cs[ts][sel];
-                        const float* rowf = tile + lane * 32;
+                        const float* rowf = tile + lane * CW;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
+                        for (int j = 0; j < CW; ++j)
                             if (sm & (1u << j))
                                 res[j] = __fadd_rn(rowf[(((j >> 2) ^ sw) << 2) | (j & 3)],
                                                    dq_slow((int32_t)acc[0][j], i0, scw[j], r0,
@@ -728,7 +736,7 @@ __global__ void __launch_bounds__(384, 1)
                     if (fin) {  // pipeline.cpp:195-202 (non-fused)
                         const float* cin = args.c_in + (int64_t)row * args.N + col0;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
+                        for (int j = 0; j < CW; ++j) {
                             if (args.has_c) {
                                 const float cv = (row_ok && col0 + j < args.N) ? cin[j] : 0.0f;
                                 res[j] = __fadd_rn(__fmul_rn(args.alpha, res[j]), __fmul_rn(args.beta, cv));
@@ -739,29 +747,29 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 } else {
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
+                    for (int k = 0; k < KV; ++k) {
                         const float4 d = rowp[k ^ sw];
                         res[4 * k] = d.x; res[4 * k + 1] = d.y; res[4 * k + 2] = d.z; res[4 * k + 3] = d.w;
                     }
                     const ScaleRef c0 = args.cs[0][sel], c1 = args.cs[1][sel];
                     const float* cin = args.c_in + (int64_t)row * args.N + col0;
-                    float t1[32], t2[32];
+                    float t1[CW], t2[CW];
                     uint32_t sm1 = 0, sm2 = 0;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
+                    for (int j = 0; j < CW; ++j) {
                         t1[j] = dq_ff24((int32_t)acc[0][j], i0, scw[j], sm1, 1u << j);
                         t2[j] = dq_ff24((int32_t)acc[1 % NACC][j], i1, scw[32 + j], sm2, 1u << j);
                     }
                     if (sm1 | sm2) {  // rare: exact redo of the flagged elements
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
+                        for (int j = 0; j < CW; ++j) {
                             const int cj = min(col0 + j, args.N - 1);
                             if (sm1 & (1u << j)) t1[j] = dq_slow((int32_t)acc[0][j], i0, scw[j], r0, c0.at(cj));
                             if (sm2 & (1u << j)) t2[j] = dq_slow((int32_t)acc[1 % NACC][j], i1, scw[32 + j], r1, c1.at(cj));
                         }
                     }
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
+                    for (int j = 0; j < CW; ++j) {
                         float v = __fadd_rn(__fadd_rn(res[j], t1[j]), t2[j]);  // pipeline.cpp:141-145
                         if (args.has_c) {                                // pipeline.cpp:195-202
                             const float cv = (row_ok && col0 + j < args.N) ? cin[j] : 0.0f;
@@ -773,7 +781,7 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
+                for (int k = 0; k < KV; ++k)
                     rowp[k ^ sw] = make_float4(res[4 * k], res[4 * k + 1], res[4 * k + 2], res[4 * k + 3]);
                 fence_proxy_async();
                 __syncwarp();
