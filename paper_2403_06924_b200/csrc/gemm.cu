@@ -176,10 +176,7 @@ void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const Gemm
         switch (epi) {
             case EPI_DF: mc ? run2<1, EPI_DF, 2>(ops, is_b, nops, args, s) : run2<1, EPI_DF, 1>(ops, is_b, nops, args, s); return;
             case EPI_COMP: mc ? run2<2, EPI_COMP, 2>(ops, is_b, nops, args, s) : run2<2, EPI_COMP, 1>(ops, is_b, nops, args, s); return;
-            case EPI_ACC:  // 4 stages where the epilogue bounds the tile (K <= 4096), see Gemm2Cfg
-                if (args.K <= 4096) run2<1, EPI_ACC, 1, 4>(ops, is_b, nops, args, s);
-                else run2<1, EPI_ACC, 1>(ops, is_b, nops, args, s);
-                return;
+            case EPI_ACC: run2<1, EPI_ACC, 1>(ops, is_b, nops, args, s); return;
         }
     }
     switch (epi) {

@@ -390,16 +390,15 @@ struct Gemm2Cfg {
     static constexpr int B_BYTES = BNH * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr bool LOADS_DIN = EPI == EPI_COMP || EPI == EPI_ACC;
-    // 5 stages but for the two-accumulator EPI_COMP (no room): the D_F GEMM at 4
-    // stages is 11% slower at 8192^3, the compensation GEMM 0.711 -> 0.639 ms
-    // with the fifth; ST overrides (the launcher picks 4 for the compensation at
-    // K <= 4096, where its epilogue, not the MMA, bounds the tile: 5 measured
-    // 1.04 -> 1.09 ms at C4)
+    // Stages of the operand ring: the D_F GEMM at 4 stages is 11% slower than at 5
+    // (8192^3); the compensation GEMM, whose operands miss L2 more, went 0.711 ->
+    // 0.639 -> 0.608 ms with a fifth and a sixth (C3; at K <= 4096 unchanged
+    // within 1%).  The two-accumulator EPI_COMP has room for 4.  ST overrides.
     static constexpr int STAGES = ST > 0 ? ST : (LOADS_DIN ? (NACC > 1 ? 4 : 6) : 5);
     // epilogue chunk width (columns per TMEM load / staging tile): 16 for the
     // six-stage compensation GEMM, whose two 32x16 staging tiles per warp leave
     // room for the sixth stage (64B-swizzled tiles), else 32 (128B swizzle)
-    static constexpr int CHW = (EPI == EPI_ACC && STAGES == 6) ? 16 : 32;
+    static constexpr int CHW = (EPI == EPI_ACC && STAGES >= 5) ? 16 : 32;
     static constexpr int ACC_COLS = NACC * BN;
     static constexpr int ACC_BUFS = (512 / ACC_COLS) >= 2 ? 2 : 1;
     static constexpr int TMEM_COLS = 512;
