@@ -11,7 +11,8 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libxigemm_b200.so")
+# XG_LIB_PATH: load another build of the library (A/B timing aid)
+LIB_PATH = os.environ.get("XG_LIB_PATH") or os.path.join(PKG, "lib", "libxigemm_b200.so")
 
 
 class XgError(RuntimeError):

@@ -176,7 +176,10 @@ void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const Gemm
         switch (epi) {
             case EPI_DF: mc ? run2<1, EPI_DF, 2>(ops, is_b, nops, args, s) : run2<1, EPI_DF, 1>(ops, is_b, nops, args, s); return;
             case EPI_COMP: mc ? run2<2, EPI_COMP, 2>(ops, is_b, nops, args, s) : run2<2, EPI_COMP, 1>(ops, is_b, nops, args, s); return;
-            case EPI_ACC: run2<1, EPI_ACC, 1>(ops, is_b, nops, args, s); return;
+            case EPI_ACC:  // K <= 4096: the epilogue bounds the tile - deeper D_F prefetch, 5 stages
+                if (args.K <= 4096) run2<1, EPI_ACC, 1, 5>(ops, is_b, nops, args, s);
+                else run2<1, EPI_ACC, 1>(ops, is_b, nops, args, s);
+                return;
         }
     }
     switch (epi) {

@@ -406,7 +406,10 @@ struct Gemm2Cfg {
     static constexpr int EPI_WARPS = 8;
     // per epilogue warp: NSTG staging tiles of 32x32 fp32 (128B-swizzled, TMA
     // store / load) and NACC x 32 float-float column reciprocals
-    static constexpr int NSTG = LOADS_DIN ? 2 : 1;
+    // staging tiles per epilogue warp; D_F loads run NSTG-1 chunks ahead.  The
+    // five-stage compensation variant (K <= 4096, where the epilogue bounds the
+    // tile) spends the sixth stage's 32 KB on four tiles instead of two
+    static constexpr int NSTG = LOADS_DIN ? ((EPI == EPI_ACC && ST == 5) ? 4 : 2) : 1;
     static constexpr int STG_BYTES = 32 * CHW * 4;
     static constexpr int EPI_BYTES = EPI_WARPS * NSTG * STG_BYTES;
     static constexpr int SCL_BYTES = EPI_WARPS * NACC * 32 * 8;
@@ -414,10 +417,11 @@ struct Gemm2Cfg {
     // starts after the driver's 1 KiB on sm_100, so none is consumed in practice;
     // the kernel traps if more than the slack would be needed
     static constexpr int ALIGN_SLACK = LOADS_DIN ? 512 : 1024;
-    static constexpr int BAR_BYTES = STAGES > 5 ? 512 : 256;  // 2*STAGES + 4 + 2*EPI_WARPS mbarriers + the TMEM slot
+    static constexpr int NBUF = NSTG > 2 ? NSTG : 2;  // D_F load barriers per epilogue warp
+    static constexpr int BAR_BYTES = (2 * STAGES + 4 + NBUF * EPI_WARPS) * 8 + 4 <= 256 ? 256 : 512;
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + SCL_BYTES + ALIGN_SLACK + BAR_BYTES;
     static_assert(SMEM_BYTES <= 232448, "shared memory over the 227 KiB per-block limit");
-    static_assert((2 * STAGES + 4 + 2 * EPI_WARPS) * 8 + 4 <= BAR_BYTES, "barrier area");
+    static_assert((2 * STAGES + 4 + NBUF * EPI_WARPS) * 8 + 4 <= BAR_BYTES, "barrier area");
     static constexpr int GROUP_M = 16;  // in 256-row units (measured: 16 > 8 > 32 at 8192^3)
     static_assert(ACC_COLS * ACC_BUFS <= 512, "TMEM overflow");
 };
@@ -447,8 +451,9 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* empty = full + Cfg::STAGES;
     uint64_t* tfull = empty + Cfg::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint64_t* dbar = tempty + 2;  // [EPI_WARPS][2] D_F tile loads
-    uint32_t* tmem_slot = (uint32_t*)(dbar + 2 * Cfg::EPI_WARPS);
+    constexpr int NBUF = Cfg::NBUF;
+    uint64_t* dbar = tempty + 2;  // [EPI_WARPS][NBUF] D_F tile loads
+    uint32_t* tmem_slot = (uint32_t*)(dbar + NBUF * Cfg::EPI_WARPS);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -473,7 +478,7 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 2 * Cfg::EPI_WARPS);
         }
-        for (int b = 0; b < 2 * Cfg::EPI_WARPS; ++b) mbar_init(&dbar[b], 1);
+        for (int b = 0; b < NBUF * Cfg::EPI_WARPS; ++b) mbar_init(&dbar[b], 1);
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
@@ -595,11 +600,12 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t tempty_leader0 = mapa_shared(&tempty[0], rank & ~1u);
         constexpr int CW = Cfg::CHW;  // chunk width (columns)
         constexpr int KV = CW / 4;     // 16-byte units per staged row
-        float* stg[2] = {epi_stage + we * Cfg::NSTG * (32 * CW),
-                         epi_stage + (we * Cfg::NSTG + Cfg::NSTG - 1) * (32 * CW)};
+        constexpr int NS = Cfg::NSTG;   // staging tiles of this warp: chunk c uses tile c % NS
+        constexpr int PD = NS - 1;      // D_F prefetch distance in chunks
+        float* const stg0 = epi_stage + we * NS * (32 * CW);
         float2* scw = reinterpret_cast<float2*>(epi_scale) + we * NACC * 32;
-        uint64_t* mybar = dbar + 2 * we;
-        uint32_t dph[2] = {0, 0};
+        uint64_t* mybar = dbar + NBUF * we;
+        uint32_t dph = 0;  // bit b: phase of tile b's load barrier
         // 128B swizzle (32 columns): unit k of row `lane` sits at k ^ (lane & 7);
         // 64B swizzle (16 columns): at k ^ ((lane >> 1) & 3)
         const int sw = CW == 32 ? (lane & 7) : ((lane >> 1) & 3);
@@ -617,14 +623,17 @@ __global__ void __launch_bounds__(384, 1)
             const int colbase = nb * Cfg::BN + half * (Cfg::BN / 2);
             const int nchunk = (args.debug & 2) ? 0 : min(Cfg::BN / 2 / CW, (args.N - colbase + CW - 1) / CW);
             // Dual term 1 reads back what term 0 just produced.  It walks the chunks
-            // in reverse: the last two term-0 chunks are still in their staging
-            // tiles (chunk c in stg[c & 1]) and are updated in place; older ones
+            // in reverse: the last NS term-0 chunks are still in their staging
+            // tiles (chunk c in tile c % NS) and are updated in place; older ones
             // are reloaded once term 0's store of that chunk has landed.
-            const bool rev = Cfg::LOADS_DIN && Cfg::NSTG == 2 && nterms == 2 && term == 1;
-            if (Cfg::LOADS_DIN && lane == 0 && nchunk > 0 && !rev) {  // D_F chunk 0 while the MMA still runs
+            const bool rev = Cfg::LOADS_DIN && NS >= 2 && nterms == 2 && term == 1;
+            const int nres = rev ? min(NS, nchunk) : 0;
+            if (Cfg::LOADS_DIN && lane == 0 && !rev) {  // the first D_F chunks while the MMA still runs
                 bulk_wait_read<0>();
-                mbar_expect_tx(&mybar[0], Cfg::STG_BYTES);
-                tma_load_2d(stg[0], &emaps.din, &mybar[0], colbase, rowbase);
+                for (int cc = 0; cc < PD && cc < nchunk; ++cc) {
+                    mbar_expect_tx(&mybar[cc % NS], Cfg::STG_BYTES);
+                    tma_load_2d(stg0 + (cc % NS) * (32 * CW), &emaps.din, &mybar[cc % NS], colbase + cc * CW, rowbase);
+                }
             }
             // row scales (fp64 for the rare exact redo) and their float-float
             // reciprocals, precomputed by the scale's producer (ScaleRef::r)
@@ -646,19 +655,19 @@ __global__ void __launch_bounds__(384, 1)
             for (int i = 0; i < nchunk; ++i) {
                 const int c = rev ? nchunk - 1 - i : i;
                 const int col0 = colbase + c * CW;
-                const int sb = (Cfg::NSTG == 2) ? (c & 1) : 0;
-                float* tile = stg[sb];
-                const bool resident = rev && i < 2;
-                if (Cfg::LOADS_DIN && lane == 0 && i + 1 < nchunk && !(rev && i + 1 < 2)) {
-                    // prefetch the next D_F chunk into the tile the previous chunk's store read out
-                    const int cn = rev ? c - 1 : c + 1;
-                    if (rev) {  // term 0's store of chunk cn (at most 3 newer groups) has landed
-                        bulk_wait<3>();
+                const int sb = c % NS;
+                float* tile = stg0 + sb * (32 * CW);
+                const bool resident = i < nres;
+                if (Cfg::LOADS_DIN && lane == 0 && i + PD < nchunk && !(rev && i + PD < nres)) {
+                    // prefetch the chunk PD ahead into the tile the previous chunk's store read out
+                    const int cn = rev ? c - PD : c + PD;
+                    if (rev) {  // term 0's store of chunk cn (at most NS+1 newer groups) has landed
+                        bulk_wait<NS + 1>();
                         fence_proxy_async();
                     }
                     bulk_wait_read<0>();
-                    mbar_expect_tx(&mybar[cn & 1], Cfg::STG_BYTES);
-                    tma_load_2d(stg[cn & 1], &emaps.din, &mybar[cn & 1], colbase + cn * CW, rowbase);
+                    mbar_expect_tx(&mybar[cn % NS], Cfg::STG_BYTES);
+                    tma_load_2d(stg0 + (cn % NS) * (32 * CW), &emaps.din, &mybar[cn % NS], colbase + cn * CW, rowbase);
                 }
                 // column reciprocals of this chunk, broadcast through shared memory
                 const int mycol = min(col0 + lane, args.N - 1);
@@ -680,8 +689,8 @@ __global__ void __launch_bounds__(384, 1)
                         else bulk_wait_read<1>();
                     }
                 } else if (Cfg::LOADS_DIN) {
-                    mbar_wait(&mybar[sb], dph[sb]);
-                    dph[sb] ^= 1;
+                    mbar_wait(&mybar[sb], (dph >> sb) & 1u);
+                    dph ^= 1u << sb;
                 } else if (lane == 0) {
                     bulk_wait_read<0>();  // staging tile free again
                 }
