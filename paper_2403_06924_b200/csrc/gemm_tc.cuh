@@ -398,7 +398,7 @@ struct Gemm2Cfg {
     // epilogue chunk width (columns per TMEM load / staging tile): 16 for the
     // six-stage compensation GEMM, whose two 32x16 staging tiles per warp leave
     // room for the sixth stage (64B-swizzled tiles), else 32 (128B swizzle)
-    static constexpr int CHW = (EPI == EPI_ACC && STAGES >= 5) ? 16 : 32;
+    static constexpr int CHW = ((EPI == EPI_ACC && STAGES >= 5) || EPI == EPI_DF) ? 16 : 32;
     static constexpr int ACC_COLS = NACC * BN;
     static constexpr int ACC_BUFS = (512 / ACC_COLS) >= 2 ? 2 : 1;
     static constexpr int TMEM_COLS = 512;
@@ -409,7 +409,7 @@ struct Gemm2Cfg {
     // staging tiles per epilogue warp; D_F loads run NSTG-1 chunks ahead.  The
     // five-stage compensation variant (K <= 4096, where the epilogue bounds the
     // tile) spends the sixth stage's 32 KB on four tiles instead of two
-    static constexpr int NSTG = LOADS_DIN ? ((EPI == EPI_ACC && ST == 5) ? 4 : 2) : 1;
+    static constexpr int NSTG = LOADS_DIN ? ((EPI == EPI_ACC && ST == 5) ? 4 : 2) : (CHW == 16 ? 2 : 1);
     static constexpr int STG_BYTES = 32 * CHW * 4;
     static constexpr int EPI_BYTES = EPI_WARPS * NSTG * STG_BYTES;
     static constexpr int SCL_BYTES = EPI_WARPS * NACC * 32 * 8;
@@ -692,7 +692,7 @@ __global__ void __launch_bounds__(384, 1)
                     mbar_wait(&mybar[sb], (dph >> sb) & 1u);
                     dph ^= 1u << sb;
                 } else if (lane == 0) {
-                    bulk_wait_read<0>();  // staging tile free again
+                    bulk_wait_read<NS - 1>();  // this chunk's staging tile free again
                 }
                 __syncwarp();
                 float4* rowp = reinterpret_cast<float4*>(tile + lane * CW);
