@@ -675,10 +675,14 @@ __device__ __forceinline__ float fmax_nan(float a, float b) {
     asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
     return r;
 }
+// u = RN(x*lam32 + 1.5*2^23) rounds the exact product to an integer in one FMA
+// (ties to even; a tie is excluded by the test below), and the distance of the
+// exact product from that integer comes from a second FMA: 4 instructions.
+// |x*lam32 - x*lam| <= 2^-24*|x*lam| <= 8e-6 for |x*lam| <= qmax, far inside the
+// 1e-4 margin, so the reference's llround(double(x)*lam) is the same integer.
 __device__ __forceinline__ uint32_t qn(float x, float lam32, float& dmax) {
-    const float t = __fmul_rn(x, lam32);
-    const float u = __fadd_rn(t, kMagic);
-    dmax = fmax_nan(dmax, fabsf(__fsub_rn(t, __fsub_rn(u, kMagic))));
+    const float u = __fmaf_rn(x, lam32, kMagic);
+    dmax = fmax_nan(dmax, fabsf(__fmaf_rn(x, lam32, -__fsub_rn(u, kMagic))));
     return __float_as_uint(u);
 }
 __device__ __forceinline__ uint32_t ubits(int q) { return (uint32_t)(q + 0x4B400000); }
