@@ -498,3 +498,21 @@ def test_concurrent_calls_from_threads():
     for w, g in zip(want, got):
         assert beq(g.result, w.result)
         assert (g.density_a, g.density_b, int(g.path)) == (w.density_a, w.density_b, int(w.path))
+
+
+@pytest.mark.parametrize("m,k,n", [(300, 5000, 260), (520, 8200, 1000), (257, 4100, 33)])
+def test_pipeline_vs_oracle_long_k_ragged(oracle, m, k, n):
+    """K > 4096 with ragged M / N: the six-stage compensation GEMM (16-column
+    epilogue chunks, two staging tiles) and the D_F GEMM on partial tiles, both
+    policies, against the oracle bit for bit."""
+    a = ol.random_dense(m, k, m + k, -4, 4)
+    b = ol.random_dense(k, n, k + n, -4, 4)
+    cm = ol.random_dense(m, n, m + n, -1, 1)
+    for pol in (0, 1):
+        c = ol.cfg(bits=8, threshold=0.05 if pol == 0 else 0.6, density_limit=0.5, scheme=1, policy=pol, rounding=1)
+        rc, ref, orep = oracle.xigemm(a, b, c=cm, alpha=0.75, beta=1.5, config=c)
+        assert rc == 0
+        rep = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), torch.from_numpy(cm).cuda(),
+                        0.75, 1.5, cfg_from(c))
+        assert beq(rep.result, ref), (m, k, n, pol)
+        assert (rep.density_a, rep.density_b, int(rep.path)) == (orep.density_a, orep.density_b, orep.path)
