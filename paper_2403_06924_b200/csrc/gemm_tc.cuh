@@ -395,20 +395,20 @@ struct Gemm2Cfg {
     // 0.639 -> 0.608 ms with a fifth and a sixth (C3; at K <= 4096 unchanged
     // within 1%).  The two-accumulator EPI_COMP has room for 4.  ST overrides.
     static constexpr int STAGES = ST > 0 ? ST : (LOADS_DIN ? (NACC > 1 ? 4 : 6) : 5);
-    // epilogue chunk width (columns per TMEM load / staging tile): 16 for the
-    // six-stage compensation GEMM, whose two 32x16 staging tiles per warp leave
-    // room for the sixth stage (64B-swizzled tiles), else 32 (128B swizzle)
+    // epilogue chunk width (columns per TMEM load / staging tile): 16 (64B-swizzled
+    // 32x16 tiles) for the compensation GEMM, whose smaller staging tiles leave
+    // room for the sixth stage, and for the D_F GEMM (two tiles in the space of
+    // one 32x32: stores overlap the next chunk); 32 (128B swizzle) for EPI_COMP
     static constexpr int CHW = ((EPI == EPI_ACC && STAGES >= 5) || EPI == EPI_DF) ? 16 : 32;
     static constexpr int ACC_COLS = NACC * BN;
     static constexpr int ACC_BUFS = (512 / ACC_COLS) >= 2 ? 2 : 1;
     static constexpr int TMEM_COLS = 512;
     static constexpr int THREADS = 384;
     static constexpr int EPI_WARPS = 8;
-    // per epilogue warp: NSTG staging tiles of 32x32 fp32 (128B-swizzled, TMA
-    // store / load) and NACC x 32 float-float column reciprocals
-    // staging tiles per epilogue warp; D_F loads run NSTG-1 chunks ahead.  The
-    // five-stage compensation variant (K <= 4096, where the epilogue bounds the
-    // tile) spends the sixth stage's 32 KB on four tiles instead of two
+    // per epilogue warp: NSTG staging tiles of 32 x CHW fp32 (TMA store / load;
+    // D_F loads run NSTG-1 chunks ahead) and NACC x 32 float-float column
+    // reciprocals.  The five-stage compensation variant (K <= 4096, where the
+    // epilogue bounds the tile) spends the sixth stage's 32 KB on four tiles
     static constexpr int NSTG = LOADS_DIN ? ((EPI == EPI_ACC && ST == 5) ? 4 : 2) : (CHW == 16 ? 2 : 1);
     static constexpr int STG_BYTES = 32 * CHW * 4;
     static constexpr int EPI_BYTES = EPI_WARPS * NSTG * STG_BYTES;
