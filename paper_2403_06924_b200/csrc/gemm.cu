@@ -156,6 +156,13 @@ int pair_count(const GemmArgs& args) {
 
 }  // namespace
 
+bool pair_gemm_used(int M, int N) {
+    GemmArgs a{};
+    a.M = M;
+    a.N = N;
+    return use_pair_kernel(a) && (N % 4) == 0;
+}
+
 bool make_tmap_f32(void* tmap, const float* p, int rows, int cols, int64_t ld, int box_cols,
                    int box_rows) {
     if ((reinterpret_cast<uintptr_t>(p) & 15) || ((ld * 4) % 16)) return false;

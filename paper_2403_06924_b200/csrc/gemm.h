@@ -25,4 +25,8 @@ bool make_tmap_f32(void* tmap /* CUtensorMap* */, const float* p, int rows, int 
 void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const GemmArgs& args,
              cudaStream_t s);
 
+// Both pipeline GEMMs of an M x N problem run the pair kernel (whose
+// %globaltimer stamps give the report's stage times).
+bool pair_gemm_used(int M, int N);
+
 }  // namespace xg
