@@ -385,7 +385,9 @@ def run_b200(args, world, rank, local):
                 "h2d_bytes_per_step": 4 * (m * k + k * n), "d2h_bytes_per_step": 4 * m * n} if e2e_val else None,
         "roofline": {"bound": "tensor", "kernel": name, "achieved": achieved,
                      "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
-                     "traffic": traffic,
+                     # dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full)
+                     "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                     "traffic_detail": traffic,
                      "peak_source": f"2 x bf16_tflops ({bf16}) of MEASURED_PEAKS.json ({src}); INT8 dense = 2x bf16 on B200",
                      "gemm_df_ms": t_df * 1e3, "gemm_comp_ms": t_cp * 1e3,
                      "cublaslt_int8_tflops": cublaslt,
