@@ -72,6 +72,12 @@ struct GemmArgs {
     int group_m;   // pair kernel: tile-raster group height in 256-row units (0: default)
     int pf_dist;   // pair kernel: L2 prefetch distance in k-blocks (0: off)
     unsigned long long* stamp;  // pair kernel: [0] %globaltimer at begin, [1] max at CTA exit (null: off)
+    // pair kernel: the last CTA to finish copies rep_words words from rep_src to
+    // rep_dst (the caller's pinned report, device-mapped) - no D2H copy node
+    unsigned* done;
+    const uint32_t* rep_src;
+    uint32_t* rep_dst;
+    int rep_words;
 };
 
 template <int BN, int NACC>
@@ -818,6 +824,21 @@ __global__ void __launch_bounds__(384, 1)
         tmem_dealloc2(tmem_base, Cfg::TMEM_COLS);
     }
     if (args.stamp && threadIdx.x == 128) atomicMax(&args.stamp[1], globaltimer_ns());  // stores landed above
+    if (args.done) {
+        __syncthreads();  // this CTA's stamp is in
+        uint32_t* last = tmem_slot + 1;  // spare word of the barrier area
+        if (threadIdx.x == 0) {
+            __threadfence();
+            *last = atomicAdd(args.done, 1u) == gridDim.x - 1 ? 1u : 0u;
+        }
+        __syncthreads();
+        if (*last) {
+            __threadfence();
+            for (int i = threadIdx.x; i < args.rep_words; i += blockDim.x)
+                args.rep_dst[i] = *reinterpret_cast<const volatile uint32_t*>(args.rep_src + i);
+            __threadfence_system();
+        }
+    }
 }
 
 }  // namespace xg

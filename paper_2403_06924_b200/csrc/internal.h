@@ -29,6 +29,8 @@ struct DevScalars {
     // %globaltimer stamps of the graph path's stage boundaries (ns): pipeline
     // start, D_F GEMM begin / end, compensation begin / end; 0 = not written
     unsigned long long ts[5];
+    unsigned done;  // CTAs of the compensation GEMM finished (the last one writes the report)
+    unsigned pad2;
 };
 
 struct QuantRowsArgs {
