@@ -516,3 +516,26 @@ def test_pipeline_vs_oracle_long_k_ragged(oracle, m, k, n):
                         0.75, 1.5, cfg_from(c))
         assert beq(rep.result, ref), (m, k, n, pol)
         assert (rep.density_a, rep.density_b, int(rep.path)) == (orep.density_a, orep.density_b, orep.path)
+
+
+def test_graph_cache_alternating_shapes_reports():
+    """Alternating problems through the graph cache (captured on second use;
+    the report scalars come from the compensation GEMM's last CTA, the stage
+    times from kernel stamps): every call returns the first call's result,
+    densities and path, and non-negative stage times."""
+    probs = []
+    for i, (m, k, n) in enumerate([(512, 1024, 640), (768, 2048, 256), (300, 4100, 260)]):
+        a = torch.from_numpy(ol.random_dense(m, k, 300 + i, -3, 3)).cuda()
+        b = torch.from_numpy(ol.random_dense(k, n, 400 + i, -3, 3)).cuda()
+        cfg = xg.XigemmConfig(threshold=0.05, density_limit=0.3, scheme=xg.QuantScheme.VectorWise,
+                              policy=xg.ReductionPolicy.AvgRule)
+        probs.append((a, b, cfg))
+    first = [xg.xigemm(a, b, cfg=cfg) for a, b, cfg in probs]
+    for _ in range(4):
+        for (a, b, cfg), f in zip(probs, first):
+            r = xg.xigemm(a, b, cfg=cfg)
+            assert beq(r.result, f.result)
+            assert (r.density_a, r.density_b, int(r.path), r.nnz_a, r.nnz_b) == \
+                   (f.density_a, f.density_b, int(f.path), f.nnz_a, f.nnz_b)
+            assert all(v >= 0 for v in r.timings.values())
+            assert r.timings["xxmm"] > 0
