@@ -189,11 +189,15 @@ def run_reference(args, world, rank):
         thr = args.threshold or 0.01
     # larger slabs than the single-core baseline: the reference redoes all of
     # B's quantisation per call, which a 16-row slab would over-weight
-    rows = args.ref_rows if args.ref_rows_set else 64
+    # exactly --steps K steps (or --ref-steps); each a bounded sample: 64-row
+    # slabs (~4-5 s per step on the GPU box's cores), smaller beyond 30 steps so
+    # the whole run stays within a few minutes
+    nsteps = max(1, args.steps if args.ref_steps is None else args.ref_steps)
+    rows = args.ref_rows if args.ref_rows_set else (64 if nsteps <= 30 else max(8, 64 * 30 // nsteps))
     vals = []
     for _ in range(args.warmup):
         pass  # CPU: no warm-up effect worth paying minutes for
-    for _ in range(max(1, args.steps if args.ref_steps is None else args.ref_steps)):
+    for _ in range(nsteps):
         v, dt, kind = cpu_baseline_sample(a, b, thr, rows, threads=threads)
         vals.append((v, dt))
     value = sorted(v for v, _ in vals)[len(vals) // 2] / 1e12
@@ -517,7 +521,7 @@ def main():
     ap.add_argument("--threshold", type=float, default=None)
     ap.add_argument("--ref-rows", type=int, default=None,
                     help="row slab of the CPU samples (default 16 for cpu_baseline, 64 for --impl reference)")
-    ap.add_argument("--ref-steps", type=int, default=3)
+    ap.add_argument("--ref-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     ap.add_argument("--no-accuracy", action="store_true", help="skip the FP64-GEMM error report")
