@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kThreads)
             }
             fv[u] = f;
         }
+        double rsv[kBatch];
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
             const int r = r0 + rb + u;
@@ -64,9 +65,7 @@ __global__ void __launch_bounds__(kThreads)
                 cs1 = __dadd_rn(cs1, a1);
                 cs2 = __dadd_rn(cs2, a2);
                 cs3 = __dadd_rn(cs3, a3);
-                double rs = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
-                rs = warp_sumd(rs);
-                if (lane == 0 && r < rows) atomicAdd(row_sum + r, rs);
+                rsv[u] = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
             } else {
                 const bool in0 = c < cols, in1 = c + 1 < cols, in2 = c + 2 < cols, in3 = c + 3 < cols;
                 const bool rin = r < rows;
@@ -81,6 +80,29 @@ __global__ void __launch_bounds__(kThreads)
                 for (int o = 16; o > 0; o >>= 1) rm = fminf(rm, __shfl_xor_sync(0xffffffffu, rm, o));
                 if (lane == 0 && rin) atomicMin(row_min + r, fbits(rm));
             }
+        }
+        if (POLICY == kAvg) {
+            // the 8 row partials of the warp reduced together: each exchange halves
+            // the rows a lane keeps (9 double shuffles instead of 8 x 5); any order of
+            // the fp64 additions is covered by the verified-mean bound
+            static_assert(kBatch == 8, "transposed reduction of 8 rows");
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+            double k4[4], k2[2];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double send = b4 ? rsv[k] : rsv[k + 4];
+                k4[k] = __dadd_rn(b4 ? rsv[k + 4] : rsv[k], __shfl_xor_sync(0xffffffffu, send, 16));
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const double send = b3 ? k4[k] : k4[k + 2];
+                k2[k] = __dadd_rn(b3 ? k4[k + 2] : k4[k], __shfl_xor_sync(0xffffffffu, send, 8));
+            }
+            double v = __dadd_rn(b2 ? k2[1] : k2[0], __shfl_xor_sync(0xffffffffu, b2 ? k2[0] : k2[1], 4));
+            v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 2));
+            v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 1));
+            const int r = r0 + rb + (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+            if ((lane & 3) == 0 && r < rows) atomicAdd(row_sum + r, v);
         }
     }
     if (c < cols) {
