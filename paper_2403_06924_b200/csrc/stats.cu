@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kThreads)
             fv[u] = f;
         }
         double rsv[kBatch];
+        float rmv[kBatch];
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
             const int r = r0 + rb + u;
@@ -75,11 +76,23 @@ __global__ void __launch_bounds__(kThreads)
                 cm1 = fminf(cm1, a1);
                 cm2 = fminf(cm2, a2);
                 cm3 = fminf(cm3, a3);
-                float rm = fminf(fminf(a0, a1), fminf(a2, a3));
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) rm = fminf(rm, __shfl_xor_sync(0xffffffffu, rm, o));
-                if (lane == 0 && rin) atomicMin(row_min + r, fbits(rm));
+                rmv[u] = fminf(fminf(a0, a1), fminf(a2, a3));
             }
+        }
+        if (POLICY != kAvg) {  // the same transposed reduction for the row minima (order-free)
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+            float k4[4], k2[2];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                k4[k] = fminf(b4 ? rmv[k + 4] : rmv[k], __shfl_xor_sync(0xffffffffu, b4 ? rmv[k] : rmv[k + 4], 16));
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                k2[k] = fminf(b3 ? k4[k + 2] : k4[k], __shfl_xor_sync(0xffffffffu, b3 ? k4[k] : k4[k + 2], 8));
+            float v = fminf(b2 ? k2[1] : k2[0], __shfl_xor_sync(0xffffffffu, b2 ? k2[0] : k2[1], 4));
+            v = fminf(v, __shfl_xor_sync(0xffffffffu, v, 2));
+            v = fminf(v, __shfl_xor_sync(0xffffffffu, v, 1));
+            const int r = r0 + rb + (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+            if ((lane & 3) == 0 && r < rows) atomicMin(row_min + r, fbits(v));
         }
         if (POLICY == kAvg) {
             // the 8 row partials of the warp reduced together: each exchange halves
