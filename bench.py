@@ -321,7 +321,7 @@ def run_b200(args, world, rank, local):
     achieved = kops / tk / 1e12
     traffic = None
     try:  # DRAM bytes per launch of that kernel from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r1j_gemm_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1k_gemm_traffic.json")) as f:
             tr = json.load(f)
         pre = "void k_gemm_i8_tc2<1, 4, 1" if t_cp >= t_df else "void k_gemm_i8_tc2<1, 1, 1"
         key = next(kk for kk in tr if kk.startswith(pre))
@@ -329,7 +329,7 @@ def run_b200(args, world, rank, local):
                    # int8 operands in (A'q, RBq, RAq, B'q | Aq, Bq), fp32 D_F in (compensation), fp32 out
                    "algorithmic_bytes_per_launch": (2 * (m * k + k * n) + 8 * m * n) if t_cp >= t_df
                    else (m * k + k * n + 4 * m * n),
-                   "source": "profiles/r1j_gemm_traffic.json (ncu --set full, this kernel, C3)"}
+                   "source": "profiles/r1k_gemm_traffic.json (ncu --set full, this kernel, C3)"}
     except (OSError, KeyError, ValueError, StopIteration):
         pass
     # live reference point for the INT8 denominator (MEASURED_PEAKS.json has
