@@ -105,6 +105,7 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int gro
     const int w = t - g * per_group;
     mb = first + w % gm;
     nb = w / gm;
+    if (g & 1) nb = num_n - 1 - nb;  // serpentine: a group starts on the B panels the previous one ended on
 }
 
 // Column j's scale and its reciprocal live in lane j of the warp (computed once
