@@ -1839,7 +1839,11 @@ bool launch_cols_maxq(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cu
     // K <= 8192 (clusters of <= 4): measured 1-5% faster end to end than the two
     // kernels at C2-C4; 8-CTA clusters (K = 16384) co-schedule worse with the
     // A side and measured ~1% slower, so larger K keeps the two-kernel path
-    if (csize > 4) return false;
+    static const int maxc = [] {  // tuning aid: XG_COLS_FUSED_MAXC (largest cluster used)
+        const char* e = getenv("XG_COLS_FUSED_MAXC");
+        return e ? atoi(e) : 4;
+    }();
+    if (csize > maxc || csize > 8) return false;
     alignas(64) CUtensorMap tm;
     if (!make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) return false;
     constexpr int smem = col_w_smem<WW, SLOTS>();
