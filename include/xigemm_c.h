@@ -38,7 +38,8 @@ typedef enum {
     XG_EINVAL = 1,   /* std::invalid_argument in the reference */
     XG_ECUDA = 2,    /* CUDA runtime / launch failure (no reference equivalent) */
     XG_ENOMEM = 3,
-    XG_EINTERNAL = 4
+    XG_EINTERNAL = 4,
+    XG_EAGAIN = 5    /* row-sharded only: rerun with a larger exchange buffer (xg_shard_finish) */
 } xg_status;
 
 enum { XG_FLOOR = 0, XG_NEAREST = 1 };
@@ -80,6 +81,11 @@ typedef struct {
     float *row_stat; float *col_stat;/* M ; N */
     int8_t *a_red; int8_t *b_red;    /* M*K ; K*N (quantized reduced operands, dense form) */
     double *a_red_scale; double *b_red_scale; /* per-tensor scale of the reduced operands */
+    /* kept-element index sets of reduce_a / reduce_b (sparse.cpp:36-85) as written
+     * by the selection kernels: bit (k % 32) of word [i * ceil(K/32) + k / 32] of
+     * a_keep is set iff a[i][k] is retained; b_keep likewise for b[k][j] at word
+     * [j * ceil(K/32) + k / 32] (one row per column of B).  Zeroed by the call. */
+    uint32_t *a_keep; uint32_t *b_keep;  /* M*ceil(K/32) ; N*ceil(K/32) */
 } xg_dump;
 
 const char *xg_last_error(void);
@@ -204,6 +210,15 @@ xg_status xg_shard_exchange(xg_shard *h, int point, int idx, void **send, void *
                             int64_t *count, int *dtype, int *op);
 xg_status xg_shard_finish(xg_shard *h, xg_report *rep, xg_stream s);
 void xg_shard_destroy(xg_shard *h);
+/* Point 3 all-gathers the D_F columns of the (rare) AvgRule column means that
+ * need the exact sequential sum; the buffer holds xg_shard_remote_cap(h)
+ * columns (8 by default).  When a run flags more, xg_shard_finish returns
+ * XG_EAGAIN (every rank sees the same count) and the results are not valid:
+ * call xg_shard_set_remote_cap(h, xg_shard_remote_needed(h)) on every rank,
+ * re-query the point-3 exchange (its buffers changed) and rerun steps 0-5. */
+int xg_shard_remote_cap(const xg_shard *h);
+int xg_shard_remote_needed(const xg_shard *h);
+xg_status xg_shard_set_remote_cap(xg_shard *h, int cap);
 
 /* ---- host-buffer entry points (what the C++ drop-in binds) --------------- */
 xg_status xg_xigemm_host(const float *a, const float *b, const float *c, float alpha, float beta,

@@ -23,6 +23,15 @@ class InvalidArgument(ValueError):
     """Mirrors the reference's std::invalid_argument."""
 
 
+class ShardRetry(XgError):
+    """XG_EAGAIN from xg_shard_finish: the row-sharded run flagged more exact
+    column means than its exchange buffer holds (`needed`); rerun with more."""
+
+    def __init__(self, msg: str, needed: int = 0):
+        super().__init__(msg)
+        self.needed = needed
+
+
 class XgConfig(C.Structure):
     _fields_ = [("bits", C.c_int), ("threshold", C.c_double), ("density_limit", C.c_double),
                 ("scheme", C.c_int), ("policy", C.c_int), ("rounding", C.c_int)]
@@ -38,7 +47,7 @@ class XgReport(C.Structure):
 
 DUMP_FIELDS = ["aq", "aq_scales", "bq", "bq_scales", "d_f", "raq", "raq_scale", "rbq",
                "rbq_scale", "row_stat", "col_stat", "a_red", "b_red", "a_red_scale",
-               "b_red_scale"]
+               "b_red_scale", "a_keep", "b_keep"]
 
 
 class XgDump(C.Structure):
@@ -88,6 +97,9 @@ _SIGS = {
     "xg_shard_exchange": (_I, [_V, _I, _I, _V, _V, _V, _V, _V]),
     "xg_shard_finish": (_I, [_V, _V, _V]),
     "xg_shard_destroy": (None, [_V]),
+    "xg_shard_remote_cap": (_I, [_V]),
+    "xg_shard_remote_needed": (_I, [_V]),
+    "xg_shard_set_remote_cap": (_I, [_V, _I]),
     "xg_gemm_direct": (_I, [_V, _V, _I, _I, _I, _V, _V, _V]),
     "xg_gemm_direct_q": (_I, [_V, _I, _V, _V, _I, _V, _I, _I, _I, _I, _I, _V, _V]),
     "xg_xigemm_host": (_I, [_V, _V, _V, _F, _F, _I, _I, _I, _V, _I, _V, _V]),
@@ -122,6 +134,8 @@ def check(rc: int) -> None:
     msg = lib().xg_last_error().decode(errors="replace")
     if rc == 1:
         raise InvalidArgument(msg)
+    if rc == 5:
+        raise ShardRetry(msg)
     raise XgError(f"xigemm status {rc}: {msg}")
 
 

@@ -410,6 +410,23 @@ def _fast_dev(x) -> bool:  # already a contiguous fp32 CUDA tensor: used as is
     return isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32 and x.is_contiguous()
 
 
+def _overlaps(x: torch.Tensor, y: torch.Tensor | None) -> bool:
+    if y is None or x.device != y.device:
+        return False
+    x0, y0 = x.data_ptr(), y.data_ptr()
+    return x0 < y0 + y.numel() * y.element_size() and y0 < x0 + x.numel() * x.element_size()
+
+
+def _check_out(out, m: int, n: int, a: torch.Tensor, b: torch.Tensor) -> None:
+    """`out` receives the result and is the pipeline's D_F scratch: a contiguous
+    float32 CUDA tensor of the result's shape, not overlapping A or B."""
+    if not isinstance(out, torch.Tensor) or not out.is_cuda or out.dtype != torch.float32 \
+            or tuple(out.shape) != (m, n) or not out.is_contiguous():
+        raise InvalidArgument("xigemm: out must be a contiguous float32 CUDA tensor of shape (M, N)")
+    if _overlaps(out, a) or _overlaps(out, b):
+        raise InvalidArgument("xigemm: out must not overlap A or B")
+
+
 def _pipeline(a, b, c, alpha, beta, cfg: XigemmConfig, reduce: bool, dump: bool, out=None):
     if _fast_dev(a) and _fast_dev(b):
         x, host, y = a, False, b
@@ -427,6 +444,10 @@ def _pipeline(a, b, c, alpha, beta, cfg: XigemmConfig, reduce: bool, dump: bool,
             raise InvalidArgument("xigemm: C shape does not match the result")
     if out is None:
         out = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    else:
+        _check_out(out, m, n, x, y)
+        if _overlaps(out, cc):  # BLAS-style in place (out is C): D_F lands in out first
+            cc = cc.clone()
     rep = XgReport()
     dmp = None
     bufs = None
@@ -447,7 +468,9 @@ def _pipeline(a, b, c, alpha, beta, cfg: XigemmConfig, reduce: bool, dump: bool,
                     a_red=torch.empty((m, k), dtype=torch.int8, **e),
                     b_red=torch.empty((k, n), dtype=torch.int8, **e),
                     a_red_scale=torch.empty(1, dtype=torch.float64, **e),
-                    b_red_scale=torch.empty(1, dtype=torch.float64, **e))
+                    b_red_scale=torch.empty(1, dtype=torch.float64, **e),
+                    a_keep=torch.empty((m, (k + 31) // 32), dtype=torch.int32, **e),
+                    b_keep=torch.empty((n, (k + 31) // 32), dtype=torch.int32, **e))
         dmp = XgDump(*[bufs[f].data_ptr() for f in DUMP_FIELDS])
     cfgc = cfg.c()
     check(lib().xg_xigemm(_p(x), _p(y), _p(cc), float(alpha), float(beta), m, k, n,
@@ -506,15 +529,24 @@ def xigemm_host(a: np.ndarray, b: np.ndarray, c=None, alpha=1.0, beta=0.0,
     cfg = cfg or XigemmConfig()
     a = np.ascontiguousarray(a, np.float32)
     b = np.ascontiguousarray(b, np.float32)
-    if a.shape[1] != b.shape[0]:
+    if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[0]:
         raise InvalidArgument("xigemm: inner dimensions do not match")
     m, k = a.shape
     n = b.shape[1]
     if out is None:
         out = np.empty((m, n), np.float32)
+    elif not isinstance(out, np.ndarray) or out.dtype != np.float32 or out.shape != (m, n) \
+            or not out.flags.c_contiguous or not out.flags.writeable:
+        raise InvalidArgument("xigemm: out must be a writable C-contiguous float32 array of shape (M, N)")
+    if np.shares_memory(out, a) or np.shares_memory(out, b):
+        raise InvalidArgument("xigemm: out must not overlap A or B")
     cp = None
     if c is not None:
         c = np.ascontiguousarray(c, np.float32)
+        if c.shape != (m, n):  # pipeline.cpp:185-187
+            raise InvalidArgument("xigemm: C shape does not match the result")
+        if np.shares_memory(c, out):
+            c = c.copy()
         cp = c.ctypes.data
     rep = XgReport()
     cfgc = cfg.c()

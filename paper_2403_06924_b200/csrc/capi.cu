@@ -45,6 +45,9 @@ struct InvalidArg : std::runtime_error {
 struct CudaFail : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct Again : std::runtime_error {  // XG_EAGAIN
+    using std::runtime_error::runtime_error;
+};
 
 void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw CudaFail(std::string(what) + ": " + cudaGetErrorString(e));
@@ -68,6 +71,9 @@ xg_status guarded(F&& f) {
     } catch (const CudaFail& e) {
         g_err = e.what();
         return XG_ECUDA;
+    } catch (const Again& e) {
+        g_err = e.what();
+        return XG_EAGAIN;
     } catch (const std::bad_alloc& e) {
         g_err = "out of memory";
         return XG_ENOMEM;
@@ -177,6 +183,7 @@ struct Pipe {
     bool pre_init = false;  // colmax / statistics accumulators already initialised
     unsigned long long *stamp_df = nullptr, *stamp_comp = nullptr;  // DevScalars::ts slots of the GEMMs
     uint32_t* report_dst = nullptr;  // device-mapped pinned report the compensation GEMM writes
+    uint32_t *keepA = nullptr, *keepB = nullptr;  // stage dump: kept-element bitmasks (xg_dump)
 };
 
 // Second stream for the independent A-side / B-side memory-bound kernels of
@@ -187,11 +194,16 @@ struct Aux {
     cudaStream_t s2 = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
 };
-Aux& aux_stream() {
-    thread_local Aux a[16];
+constexpr int kMaxDev = 16;  // per-thread stream slots are indexed by the current device
+int cur_dev() {
     int dev = 0;
-    cudaGetDevice(&dev);
-    Aux& x = a[dev & 15];
+    ck(cudaGetDevice(&dev), "device");
+    req(dev >= 0 && dev < kMaxDev, "xigemm: device ordinal out of range");
+    return dev;
+}
+Aux& aux_stream() {
+    thread_local Aux a[kMaxDev];
+    Aux& x = a[cur_dev()];
     if (!x.s2) {
         ck(cudaStreamCreateWithFlags(&x.s2, cudaStreamNonBlocking), "aux stream");
         for (auto& e : x.ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "aux event");
@@ -363,6 +375,9 @@ void select_operands(Pipe& p, const float* a, const float* b, int reduce, const 
     sb.stat = cstat; sb.other_max = &p.sc->maxA;
     sb.rq = p.rbqT; sb.red = p.bredT;
     sb.nnz = &p.sc->nnzB; sb.retmax = &p.sc->retB;
+    sa.keep = reduce ? p.keepA : nullptr;
+    sb.keep = reduce ? p.keepB : nullptr;
+    sa.keep_ld = sb.keep_ld = (p.K + 31) / 32;
     if (!(phases & 1)) goto fixups;
     {
     const bool co = coschedule_enabled();
@@ -600,6 +615,13 @@ int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* du
                                    &p.sc->nflag, s, dump ? nullptr : &def);
             check_launch("stats", q.cfg.policy == XG_AVG_RULE ? 3 : 1);
         }
+        if (dump && q.reduce) {  // kept-element bitmasks, OR-ed in by the selection kernels
+            const size_t kw = (size_t)(K + 31) / 32;
+            if (dump->a_keep) ck(cudaMemsetAsync(dump->a_keep, 0, 4 * kw * M, s), "dump");
+            if (dump->b_keep) ck(cudaMemsetAsync(dump->b_keep, 0, 4 * kw * N, s), "dump");
+            p.keepA = dump->a_keep;
+            p.keepB = dump->b_keep;
+        }
         select_operands(p, q.a, q.b, q.reduce, w.rstat, w.cstat);
         xg::launch_dispatch(p.sc, q.cfg.bits, (int64_t)M * K, (int64_t)K * N, q.cfg.density_limit, q.reduce, s);
         check_launch("dispatch");
@@ -730,7 +752,8 @@ void make_programmatic(cudaGraph_t g) {
 // device scalars into pinned host memory, so a replay is one graph launch and
 // one stream synchronisation.
 void capture_entry(GraphEntry& e) {
-    static thread_local cudaStream_t cs = nullptr;
+    static thread_local cudaStream_t css[kMaxDev] = {};
+    cudaStream_t& cs = css[cur_dev()];  // the entry's device is current (graph_acquire)
     if (!cs) ck(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
     for (auto& ev : e.ev)
         if (!ev) ck(cudaEventCreate(&ev), "event");
@@ -1440,7 +1463,7 @@ namespace {
 //   point 2  column statistics of D_F: fp64 sums (AvgRule)     fp64 SUM
 //            or float-bit minima (MinRule)                     uint32 MIN
 //   point 3  D_F columns whose AvgRule mean needs the exact sequential sum
-//            (rare; fixed-size buffer)                         ALLGATHER
+//            (rare; `cap` columns, XG_EAGAIN + rerun beyond)   ALLGATHER
 //   point 4  nnz(A') (density / dispatch), retained max|A'|    uint64 SUM, uint32 MAX
 // The caller runs xg_shard_step(h, p) on every rank, then the collectives
 // xg_shard_exchange describes for point p (NCCL / torch.distributed on a
@@ -1448,7 +1471,7 @@ namespace {
 // step p + 1.  Every reduction is exact (max, min, integer sums) except the
 // fp64 column sums, whose rounding the verified-mean test covers for any
 // summation order; results equal the single-GPU pipeline bit for bit.
-constexpr int kRemoteCap = 8;
+constexpr int kRemoteCap = 8;  // default exchange capacity (columns)
 
 struct ShardState {
     PipeCall q;  // q.a / q.c / q.out: this rank's rows; q.M: this rank's row count
@@ -1459,13 +1482,30 @@ struct ShardState {
     uint32_t* x1 = nullptr;             // [4] maxA, maxRA, nonfinite, -
     unsigned long long* x4n = nullptr;  // [1] nnz(A')
     uint32_t* x4r = nullptr;            // [1] retained max|A'|
-    int* remote = nullptr;              // [kRemoteCap] column indices
     int* n_remote = nullptr;
-    float* pack = nullptr;              // [kRemoteCap][mpad]
-    float* gath = nullptr;              // [g][kRemoteCap][mpad]
     int* rank_rows_d = nullptr;
+    // point-3 exchange (separate allocation, resized by xg_shard_set_remote_cap)
+    int cap = kRemoteCap;
+    int needed = 0;                     // columns the last run flagged (xg_shard_finish)
+    void* rbase = nullptr;
+    int* remote = nullptr;              // [cap] column indices
+    float* pack = nullptr;              // [cap][mpad]
+    float* gath = nullptr;              // [g][cap][mpad]
+    void alloc_remote(int c) {
+        if (rbase) cudaFree(rbase), rbase = nullptr;
+        cap = c;
+        const size_t a0 = ((size_t)cap * sizeof(int) + 255) / 256 * 256;
+        const size_t a1 = (size_t)cap * mpad * sizeof(float);
+        const size_t a2 = (size_t)g * cap * mpad * sizeof(float);
+        ck(cudaMalloc(&rbase, a0 + a1 + a2), "shard exchange buffer");
+        remote = static_cast<int*>(rbase);
+        pack = reinterpret_cast<float*>(static_cast<char*>(rbase) + a0);
+        gath = reinterpret_cast<float*>(static_cast<char*>(rbase) + a0 + a1);
+        ck(cudaMemset(gath, 0, a2), "memset");
+    }
     ~ShardState() {
         if (base) cudaFree(base);
+        if (rbase) cudaFree(rbase);
     }
 };
 
@@ -1534,17 +1574,17 @@ void shard_step(ShardState& h, int step, cudaStream_t s) {
                     const char* e = getenv("XG_STATS_WIDEN");  // test hook (see enqueue_stage)
                     return e ? atoi(e) : 0;
                 }();
-                xg::StatsDefer def{q.a, K, q.b, N, K, q.cfg.threshold, widen, h.remote, h.n_remote, kRemoteCap};
+                xg::StatsDefer def{q.a, K, q.b, N, K, q.cfg.threshold, widen, h.remote, h.n_remote, h.cap};
                 xg::launch_stats_final(q.out, M, N, h.m_total, q.cfg.policy, h.w.rstat, h.w.cstat, h.w.rsum,
                                        h.w.csum, h.w.flags, &p.sc->nflag, s, &def);
                 check_launch("stats final", q.cfg.policy == XG_AVG_RULE ? 2 : 0);
-                xg::launch_pack_remote_cols(q.out, M, N, h.remote, h.n_remote, kRemoteCap, h.mpad, h.pack, s);
+                xg::launch_pack_remote_cols(q.out, M, N, h.remote, h.n_remote, h.cap, h.mpad, h.pack, s);
                 check_launch("pack columns");
             }
             break;
         case 4:
             if (q.reduce && q.cfg.policy == XG_AVG_RULE) {
-                xg::launch_remote_col_means(h.gath, h.g, h.rank_rows_d, h.mpad, kRemoteCap, h.remote, h.n_remote,
+                xg::launch_remote_col_means(h.gath, h.g, h.rank_rows_d, h.mpad, h.cap, h.remote, h.n_remote,
                                             h.m_total, h.w.cstat, s);
                 check_launch("remote column means");
             }
@@ -1605,10 +1645,7 @@ xg_status xg_shard_create(const float* a_rows, const float* b, const float* c_ro
             S.x1 = get((uint32_t*)nullptr, 4);
             S.x4n = get((unsigned long long*)nullptr, 1);
             S.x4r = get((uint32_t*)nullptr, 1);
-            S.remote = get((int*)nullptr, kRemoteCap);
             S.n_remote = get((int*)nullptr, 1);
-            S.pack = get((float*)nullptr, (int64_t)kRemoteCap * S.mpad);
-            S.gath = get((float*)nullptr, (int64_t)nranks * kRemoteCap * S.mpad);
             S.rank_rows_d = get((int*)nullptr, nranks);
         };
         int64_t total = 0;
@@ -1627,7 +1664,7 @@ xg_status xg_shard_create(const float* a_rows, const float* b, const float* c_ro
             return p;
         });
         ck(cudaMemcpy(S.rank_rows_d, rank_rows, sizeof(int) * nranks, cudaMemcpyHostToDevice), "rank rows");
-        ck(cudaMemset(S.gath, 0, sizeof(float) * (size_t)nranks * kRemoteCap * S.mpad), "memset");
+        S.alloc_remote(kRemoteCap);
         *h = x.release();
     });
 }
@@ -1661,7 +1698,7 @@ xg_status xg_shard_exchange(xg_shard* h, int point, int idx, void** send, void**
             if (S.q.cfg.policy == XG_AVG_RULE) set(S.w.csum, S.w.csum, S.q.N, 2, 1);
             else set(S.w.cstat, S.w.cstat, S.q.N, 0, 2);
         } else if (point == 3 && idx == 0 && S.q.reduce && S.q.cfg.policy == XG_AVG_RULE) {
-            set(S.pack, S.gath, (int64_t)kRemoteCap * S.mpad, 3, 3);
+            set(S.pack, S.gath, (int64_t)S.cap * S.mpad, 3, 3);
         } else if (point == 4 && idx == 0) set(S.x4n, S.x4n, 1, 1, 1);
         else if (point == 4 && idx == 1) set(S.x4r, S.x4r, 1, 0, 0);
     });
@@ -1676,8 +1713,11 @@ xg_status xg_shard_finish(xg_shard* h, xg_report* rep, xg_stream s) {
         ck(cudaMemcpyAsync(&d, S.w.sc, sizeof d, cudaMemcpyDeviceToHost, st(s)), "report");
         ck(cudaMemcpyAsync(&nrem, S.n_remote, sizeof nrem, cudaMemcpyDeviceToHost, st(s)), "report");
         ck(cudaStreamSynchronize(st(s)), "pipeline");
-        if (nrem > kRemoteCap) throw std::runtime_error("xg_shard: too many ambiguous column statistics");
         req(!d.nonfinite, "xigemm: inputs must be finite");
+        S.needed = nrem;
+        if (nrem > S.cap)  // the same count on every rank (identical global column sums)
+            throw Again("xg_shard: " + std::to_string(nrem) + " column means need the exact sum, the exchange holds " +
+                        std::to_string(S.cap) + ": set the capacity and rerun");
         if (rep) {
             std::memset(rep, 0, sizeof *rep);
             rep->density_a = d.densA;
@@ -1692,6 +1732,18 @@ xg_status xg_shard_finish(xg_shard* h, xg_report* rep, xg_stream s) {
 
 void xg_shard_destroy(xg_shard* h) { delete h; }
 
+int xg_shard_remote_cap(const xg_shard* h) { return h ? h->st.cap : 0; }
+int xg_shard_remote_needed(const xg_shard* h) { return h ? h->st.needed : 0; }
+
+xg_status xg_shard_set_remote_cap(xg_shard* h, int cap) {
+    return guarded([&] {
+        req(h != nullptr, "xg_shard_set_remote_cap: null handle");
+        req(cap >= 1 && cap <= h->st.q.N, "xg_shard_set_remote_cap: capacity must be in [1, N]");
+        ck(cudaDeviceSynchronize(), "shard sync");  // the old buffer may still be in use
+        h->st.alloc_remote(cap);
+    });
+}
+
 xg_status xg_xigemm(const float* a, const float* b, const float* c, float alpha, float beta,
                     int m, int k, int n, const xg_config* cfg, int reduce, float* out,
                     xg_report* rep, xg_dump* dump, xg_stream s) {
@@ -1705,10 +1757,19 @@ xg_status xg_gemm_direct(const float* a, const float* b, int m, int k, int n,
 
 // ---------------------------------------------------------------- host API
 namespace {
-thread_local cudaStream_t t_stream = nullptr;
+// per thread and per device: a stream belongs to the device current at its creation
+struct HostStreams {
+    cudaStream_t s = nullptr, s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev[24] = {};
+};
+HostStreams& host_streams() {
+    thread_local HostStreams h[kMaxDev];
+    return h[cur_dev()];
+}
 cudaStream_t host_stream() {
-    if (!t_stream) ck(cudaStreamCreateWithFlags(&t_stream, cudaStreamNonBlocking), "stream");
-    return t_stream;
+    HostStreams& h = host_streams();
+    if (!h.s) ck(cudaStreamCreateWithFlags(&h.s, cudaStreamNonBlocking), "stream");
+    return h.s;
 }
 }  // namespace
 
@@ -1724,13 +1785,14 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
                        int K, int N, const xg_config* cfg, int reduce, float* out_h, xg_report* rep) {
     req(K <= xg::gemm_max_inner(cfg->bits), "gemm_int: inner dimension permits 32-bit overflow");
     cudaStream_t s = host_stream();
-    thread_local cudaStream_t s_in = nullptr, s_out = nullptr;
-    thread_local cudaEvent_t ev[24];
-    if (!s_in) {
-        ck(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "stream");
-        ck(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "stream");
-        for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    HostStreams& hs = host_streams();
+    if (!hs.s_in) {
+        ck(cudaStreamCreateWithFlags(&hs.s_in, cudaStreamNonBlocking), "stream");
+        ck(cudaStreamCreateWithFlags(&hs.s_out, cudaStreamNonBlocking), "stream");
+        for (auto& e : hs.ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     }
+    cudaStream_t s_in = hs.s_in, s_out = hs.s_out;
+    cudaEvent_t* ev = hs.ev;
     const int64_t ldk = pad16(K);
     Scratch S(s);
     float* da = S.get<float>((int64_t)M * K);

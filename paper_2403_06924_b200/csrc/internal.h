@@ -94,6 +94,11 @@ struct SelectArgs {
     // (pipeline.cpp:50-52), so the table-driven kernels exit instead of
     // indexing their dequant tables with NaN bit patterns
     const int* nonfinite;
+    // stage dump only (null otherwise): kept-element bitmask, bit (c % 32) of
+    // word [r * keep_ld + c / 32] for row r of the operand as laid out above
+    // (A: row i over k; B: row j of B^T over k), OR-ed in by the kernel
+    uint32_t* keep;
+    int64_t keep_ld;
 };
 
 void launch_absmax_global(const float* x, int64_t n, uint32_t* gmax, int* nonfinite,

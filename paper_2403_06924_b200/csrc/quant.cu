@@ -439,6 +439,15 @@ __device__ __forceinline__ double threshold_of(int policy, double thr_m, float s
     return __ddiv_rn(__dmul_rn(__dmul_rn(thr_m, scale_other), (double)stat), (double)inner);
 }
 
+// Stage dump: OR the kept bits of the quad at columns c..c+3 (c % 4 == 0) of
+// row r into the bitmask (sparse.cpp:61-71 keep test, |x| > t  <=>  |x| >= tf).
+__device__ __forceinline__ void dump_keep4(const SelectArgs& a, int r, int c, const float (&x)[4], float tf) {
+    uint32_t nib = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) nib |= (fabsf(x[e]) >= tf ? 1u : 0u) << e;
+    if (nib) atomicOr(&a.keep[(int64_t)r * a.keep_ld + (c >> 5)], nib << (c & 31));
+}
+
 // One quad of the selection: q (main scale), rq (residual scale), red (kept q).
 template <int RND>
 __device__ __forceinline__ void select_quad(const float (&x)[4], const float* lutp, int lstride,
@@ -512,6 +521,7 @@ __global__ void __launch_bounds__(kThreads) k_select_rows(const SelectArgs a) {
                                  cnt, ret);
                 *reinterpret_cast<uint32_t*>(rq_row + c) = pq;
                 if (rd_row) *reinterpret_cast<uint32_t*>(rd_row + c) = pr;
+                if (a.keep) dump_keep4(a, r, c, x, tf);
             }
         } else {
             for (int c = threadIdx.x; c < a.cols; c += kThreads) {
@@ -520,6 +530,7 @@ __global__ void __launch_bounds__(kThreads) k_select_rows(const SelectArgs a) {
                 rq_row[c] = (int8_t)quantize_fast((double)__fsub_rn(v, lut[q + qmax]), lam_r, (double)qmax, RND);
                 const bool keep = fabsf(v) >= tf;
                 if (rd_row) rd_row[c] = (int8_t)(keep ? q : 0);
+                if (a.keep && keep) atomicOr(&a.keep[(int64_t)r * a.keep_ld + (c >> 5)], 1u << (c & 31));
                 cnt += keep && a.do_select;
                 ret = fmaxf(ret, keep ? fabsf(v) : 0.0f);
             }
@@ -633,6 +644,8 @@ __global__ void __launch_bounds__(kThreads) k_select_cols_T(const SelectArgs a) 
                 uint32_t pq, pr;
                 select_quad<RND>(x, &lut[0][32 * c + lane], kTN, lamc[c], l32[c], lam_r, lam_r32, tf[c],
                                  qmaxf, qlim, qmax, pq, pr, cnt, ret);
+                if (a.keep && n0 + 32 * c + lane < a.cols && k0 + 16 * w + 4 * g < a.rows)
+                    dump_keep4(a, n0 + 32 * c + lane, k0 + 16 * w + 4 * g, x, tf[c]);
                 trq[32 * c + lane][4 * w + g] = pq;
                 tred[32 * c + lane][4 * w + g] = pr;
             }
@@ -796,59 +809,6 @@ __device__ __forceinline__ void select_quad_n(const float (&x)[4], uint32_t lut_
     pr = pack4u(d[0], d[1], d[2], d[3]);
 }
 
-__global__ void __launch_bounds__(kThreads) k_select_rows_fast(const SelectArgs a) {
-    XG_PDL_WAIT();
-    XG_EXIT_IF_NONFINITE(a.nonfinite);
-    __shared__ float lut[256];
-    __shared__ float red[kThreads / 32];
-    __shared__ unsigned long long redu[kThreads / 32];
-    const int qmax = quant_max(a.bits);
-    const float qmaxf = (float)qmax;
-    const uint32_t adj = smem_u32(lut) + 4u * (uint32_t)qmax - 4u * 0x4B400000u;
-    const double lam_r = compute_scale((double)__uint_as_float(*a.rmax), a.bits);
-    const float lam_r32 = __double2float_rn(lam_r);
-    const double lam_t = a.vec ? 0.0 : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
-    const double scale_other =
-        a.do_select && a.policy == kMin ? compute_scale((double)__uint_as_float(*a.other_max), a.bits)
-                                        : 1.0;
-    unsigned cnt = 0;
-    float ret = 0.0f;
-    for (int r = blockIdx.x; r < a.rows; r += gridDim.x) {
-        const float* row = a.x + (int64_t)r * a.ld;
-        int8_t* rq_row = a.rq + (int64_t)r * a.ldq;
-        int8_t* rd_row = a.red + (int64_t)r * a.ldq;
-        const double lam = a.vec ? a.lam[r] : lam_t;
-        const float lam32 = __double2float_rn(lam);
-        const bool exact = !(lam32 <= FLT_MAX) || !(lam_r32 <= FLT_MAX);
-        const float tf = a.do_select
-                             ? float_above(threshold_of(a.policy, a.thr_m, a.stat[r], scale_other, a.cols))
-                             : __int_as_float(0x7f800000);
-        if (threadIdx.x <= 2 * qmax) lut[threadIdx.x] = dequant_value((int)threadIdx.x - qmax, lam);
-        __syncthreads();
-        float lmax = 0.0f;
-#pragma unroll 4
-        for (int c = threadIdx.x * 4; c < a.cols; c += kThreads * 4) {
-            const float4 f = __ldg(reinterpret_cast<const float4*>(row + c));
-            const float x[4] = {f.x, f.y, f.z, f.w};
-            uint32_t pq, pr;
-            select_quad_n<2>(x, adj, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, pq, pr, cnt, lmax);
-            *reinterpret_cast<uint32_t*>(rq_row + c) = pq;
-            if (a.do_select) *reinterpret_cast<uint32_t*>(rd_row + c) = pr;
-        }
-        // kept max of this thread's part of the row: its max if that is kept
-        ret = fmaxf(ret, lmax >= tf ? lmax : 0.0f);
-        __syncthreads();
-    }
-    if (a.do_select) {
-        const unsigned long long c64 = block_sum_u64(cnt, redu);
-        ret = block_max(ret, red);
-        if (threadIdx.x == 0) {
-            if (c64) atomicAdd(a.nnz, c64);
-            atomicMax(a.retmax, fbits(ret));
-        }
-    }
-}
-
 __global__ void __launch_bounds__(kThreads) k_quant_cols_T_fast(const QuantColsArgs a) {
     XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
@@ -914,85 +874,6 @@ __global__ void __launch_bounds__(kThreads) k_quant_cols_T_fast(const QuantColsA
     }
     rm = block_max(rm, red);
     if (threadIdx.x == 0 && a.rmax) atomicMax(a.rmax, fbits(rm));
-}
-
-__global__ void __launch_bounds__(kThreads) k_select_cols_T_fast(const SelectArgs a) {
-    XG_PDL_WAIT();
-    XG_EXIT_IF_NONFINITE(a.nonfinite);
-    extern __shared__ float4 dyn_smem[];
-    float(*lut)[kTN] = reinterpret_cast<float(*)[kTN]>(dyn_smem);
-    __shared__ uint32_t trq[kTN][kTW];
-    __shared__ uint32_t tred[kTN][kTW];
-    __shared__ double lam_s[kTN];
-    __shared__ float red[kThreads / 32];
-    __shared__ unsigned long long redu[kThreads / 32];
-    const int n0 = blockIdx.x * kTN;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qmax = quant_max(a.bits);
-    const float qmaxf = (float)qmax;
-    const double lam_r = compute_scale((double)__uint_as_float(*a.rmax), a.bits);
-    const float lam_r32 = __double2float_rn(lam_r);
-    const double lam_t = a.vec ? 0.0 : compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
-    const double so = a.do_select && a.policy == kMin
-                          ? compute_scale((double)__uint_as_float(*a.other_max), a.bits)
-                          : 1.0;
-    if (threadIdx.x < kTN) {
-        const int n = min(n0 + (int)threadIdx.x, a.cols - 1);
-        lam_s[threadIdx.x] = a.vec ? a.lam[n] : lam_t;
-    }
-    __syncthreads();
-    build_col_luts(lut, lam_s, qmax);
-    double lamc[2];
-    float l32[2], tf[2];
-    uint32_t adj[2];
-    bool exact[2];
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-        const int nraw = n0 + 32 * c + lane;
-        const int n = min(nraw, a.cols - 1);
-        lamc[c] = lam_s[32 * c + lane];
-        l32[c] = __double2float_rn(lamc[c]);
-        exact[c] = !(l32[c] <= FLT_MAX) || !(lam_r32 <= FLT_MAX);
-        adj[c] = smem_u32(lut) + 4u * (32 * c + lane) + 256u * (uint32_t)qmax - 256u * 0x4B400000u;
-        tf[c] = (a.do_select && nraw < a.cols)
-                    ? float_above(threshold_of(a.policy, a.thr_m, a.stat[n], so, a.rows))
-                    : __int_as_float(0x7f800000);
-    }
-    __syncthreads();
-    unsigned cnt = 0;
-    float ret = 0.0f;
-    for (int sub = 0; sub < kColSub; ++sub) {
-        const int k0 = blockIdx.y * kColTileRows + sub * kTK;
-        if (k0 >= a.rows) break;  // uniform
-        float v[2][16];
-        load_col_tile(a.x, a.rows, a.cols, a.ld, n0, k0, v);  // rows past K load as 0: never kept
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            float lmax = 0.0f;
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                const float x[4] = {v[c][4 * g], v[c][4 * g + 1], v[c][4 * g + 2], v[c][4 * g + 3]};
-                uint32_t pq, pr;
-                select_quad_n<8>(x, adj[c], lamc[c], l32[c], lam_r, lam_r32, tf[c], qmaxf, exact[c], pq, pr,
-                                 cnt, lmax);
-                trq[32 * c + lane][4 * w + g] = pq;
-                tred[32 * c + lane][4 * w + g] = pr;
-            }
-            ret = fmaxf(ret, lmax >= tf[c] ? lmax : 0.0f);
-        }
-        __syncthreads();
-        store_T_tile(trq, a.rq, a.ldq, n0, k0, a.cols, a.rows);
-        if (a.do_select) store_T_tile(tred, a.red, a.ldq, n0, k0, a.cols, a.rows);
-        __syncthreads();
-    }
-    if (a.do_select) {
-        const unsigned long long c64 = block_sum_u64(cnt, redu);
-        ret = block_max(ret, red);
-        if (threadIdx.x == 0) {
-            if (c64) atomicAdd(a.nnz, c64);
-            atomicMax(a.retmax, fbits(ret));
-        }
-    }
 }
 
 
@@ -1174,6 +1055,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_select_rows_r4(const SelectArgs a
                     select_quad_n<2>(x, adj, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, pq, pr, cnt, lmax);
                     *reinterpret_cast<uint32_t*>(rq_row + c) = pq;
                     if (a.do_select) *reinterpret_cast<uint32_t*>(rd_row + c) = pr;
+                    if (a.keep) dump_keep4(a, r, c, x, tf);
                 }
             }
         }
@@ -1394,6 +1276,7 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
                 if (SELECT) {
                     select_quad_n<7>(xq, adj_base, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, w0[q], w1[q],
                                      cnt, lmax);
+                    if (sa.keep && n < cols && k0 + 4 * q < rows) dump_keep4(sa, n, k0 + 4 * q, xq, tf);
                 } else {
                     uint32_t u[4];
                     float dmax = 0.0f;
@@ -1930,9 +1813,6 @@ void launch_select_rows(const SelectArgs& a, cudaStream_t s) {
         return;
     }
     if (a.fix_mode) k_fix_rows<<<grid_rows(a.rows), kThreads, 0, s>>>(a);
-    else if (a.rounding == kNearest && (a.ld % 4 == 0) && (a.ldq % 4 == 0) && (a.cols % 4 == 0) &&
-             ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0))
-        k_select_rows_fast<<<grid_rows(a.rows), kThreads, 0, s>>>(a);
     else if (a.rounding == kNearest) k_select_rows<kNearest><<<grid_rows(a.rows), kThreads, 0, s>>>(a);
     else k_select_rows<kFloor><<<grid_rows(a.rows), kThreads, 0, s>>>(a);
 }
@@ -1951,8 +1831,8 @@ void launch_select_cols_T(const SelectArgs& a, cudaStream_t s) {
     }
     dim3 grid((a.cols + kTN - 1) / kTN, (a.rows + kColTileRows - 1) / kColTileRows);
     if (a.rounding == kNearest) {
-        set_dyn_smem(k_select_cols_T_fast, kLutBytes);
-        k_select_cols_T_fast<<<grid, kThreads, kLutBytes, s>>>(a);
+        set_dyn_smem(k_select_cols_T<kNearest>, kLutBytes);
+        k_select_cols_T<kNearest><<<grid, kThreads, kLutBytes, s>>>(a);
     } else {
         set_dyn_smem(k_select_cols_T<kFloor>, kLutBytes);
         k_select_cols_T<kFloor><<<grid, kThreads, kLutBytes, s>>>(a);

@@ -11,6 +11,8 @@ reference's algorithm has (pipeline.cpp:50-111):
     point 2  column statistics of D_F   (AvgRule sums / MinRule min) SUM / MIN
     point 3  D_F columns of the rare AvgRule means that need the exact
              sequential sum across ranks                            ALLGATHER
+             (a fixed number of columns; a run that flags more raises
+             ShardRetry on every rank and is rerun with a larger buffer)
     point 4  nnz(A'), retained max|A'|  (density, dispatch, scale)   SUM, MAX
 
 All reductions are exact (max/min/integer sums) except the fp64 column sums,
@@ -29,7 +31,7 @@ import ctypes as C
 
 import torch
 
-from ._lib import XgReport, check, lib
+from ._lib import ShardRetry, XgReport, check, lib
 from .api import GemmPath, GemmReport, InvalidArgument, XigemmConfig, _dev, _p, _s
 
 NSTEPS = 6
@@ -107,10 +109,22 @@ class Shard:
 
     def finish(self) -> XgReport:
         """Synchronises and returns the global report; the handle (and its
-        workspace) stays valid for the next run of the same problem."""
+        workspace) stays valid for the next run of the same problem.  Raises
+        ShardRetry (on every rank alike) when the run flagged more exact column
+        means than the point-3 exchange holds: grow_remote(), then rerun."""
         rep = XgReport()
-        check(lib().xg_shard_finish(self.h, C.byref(rep), _s()))
+        try:
+            check(lib().xg_shard_finish(self.h, C.byref(rep), _s()))
+        except ShardRetry as e:
+            e.needed = int(lib().xg_shard_remote_needed(self.h))
+            raise
         return rep
+
+    def grow_remote(self, needed: int) -> None:
+        """Point-3 exchange buffer for `needed` columns (new buffers: re-queried)."""
+        check(lib().xg_shard_set_remote_cap(self.h, int(needed)))
+        self._ex.clear()
+        self._graph = None
 
     def close(self):
         if self.h:
@@ -200,8 +214,14 @@ def xigemm_sharded_local(a, b, c=None, alpha: float = 1.0, beta: float = 0.0,
                             reduce, out[r0:r0 + m]))
         r0 += m
     try:
-        run_protocol(shards, LocalComm(), nranks)
-        reps = [sh.finish() for sh in shards]
+        while True:
+            run_protocol(shards, LocalComm(), nranks)
+            try:
+                reps = [sh.finish() for sh in shards]
+                break
+            except ShardRetry as e:  # rare: more exact column means than the exchange holds
+                for sh in shards:
+                    sh.grow_remote(e.needed)
     finally:
         for sh in shards:
             sh.close()
@@ -252,11 +272,14 @@ def xigemm_sharded(a_rows, b, c_rows=None, alpha: float = 1.0, beta: float = 0.0
         allm = [torch.zeros_like(mine) for _ in range(world)]
         dist.all_gather(allm, mine, group=group)
         rank_rows = [int(t) for t in torch.cat(allm).tolist()]
-    if out is None:
-        out = torch.empty((x.shape[0], y.shape[1]), dtype=torch.float32, device="cuda")
+    if out is not None and (not isinstance(out, torch.Tensor) or not out.is_cuda or out.dtype != torch.float32
+                            or tuple(out.shape) != (x.shape[0], y.shape[1]) or not out.is_contiguous()):
+        raise InvalidArgument("xigemm: out must be a contiguous float32 CUDA tensor of the result's shape")
     c = cfg.c()
+    # out=None: the cached shard's own result buffer is reused (and returned), so
+    # a repeated call hits the cache (and its CUDA graph) instead of a new handle
     key = (x.data_ptr(), tuple(x.shape), y.data_ptr(), tuple(y.shape), 0 if cc is None else cc.data_ptr(),
-           out.data_ptr(), float(alpha), float(beta), bool(reduce), rank, tuple(rank_rows),
+           None if out is None else out.data_ptr(), float(alpha), float(beta), bool(reduce), rank, tuple(rank_rows),
            (c.bits, c.threshold, c.density_limit, c.scheme, c.policy, c.rounding), id(group))
     sh = _cached_shard(key, lambda: Shard(x, y, cc, alpha, beta, rank, rank_rows, cfg, reduce, out))
     runs = getattr(sh, "_runs", 0)
@@ -272,4 +295,9 @@ def xigemm_sharded(a_rows, b, c_rows=None, alpha: float = 1.0, beta: float = 0.0
     else:
         run_protocol([sh], DistComm(group), world)
     sh._runs = runs + 1
-    return _report(sh.finish(), sh.out)
+    while True:
+        try:
+            return _report(sh.finish(), sh.out)
+        except ShardRetry as e:  # every rank raises alike: grow the exchange, rerun eagerly
+            sh.grow_remote(e.needed)
+            run_protocol([sh], DistComm(group), world)

@@ -320,3 +320,13 @@ def reference() -> Oracle | None:
     if not os.path.exists(REF_SO):
         return None
     return Oracle(REF_SO, "xr")
+
+
+def keep_mask(words, rows: int, k: int) -> np.ndarray:
+    """Unpacks an xg_dump keep bitmask (rows x ceil(k/32) uint32 words, bit k % 32
+    of word k / 32) into a rows x k bool array."""
+    w = np.ascontiguousarray(np.asarray(words.cpu() if hasattr(words, "cpu") else words)).view(np.uint32)
+    w = w.reshape(rows, -1)
+    bits = np.unpackbits(w.view(np.uint8).reshape(rows, -1), axis=1, bitorder="little")
+    return bits[:, :k].astype(bool)
+

@@ -137,8 +137,12 @@ def test_stage_golden():
                      "col_stat", "a_red", "b_red"):
             assert beq(d[name], g[pre + name]), (pre, name)
         assert beq(d["raq_scale"], g[pre + "raq_scale"]) and beq(d["rbq_scale"], g[pre + "rbq_scale"])
-        # retained index sets: nnz counts equal the reference's (density is
-        # nnz / size and bit-equal), values equal on every retained entry
+        # retained index sets (reduce_a / reduce_b, sparse.cpp:36-85) exactly as the
+        # selection kernels wrote them, against the reference's masks
+        m, k = g[pre + "a"].shape
+        n = g[pre + "b"].shape[1]
+        assert np.array_equal(ol.keep_mask(d["a_keep"], m, k), g[pre + "a_mask"].astype(bool)), pre
+        assert np.array_equal(ol.keep_mask(d["b_keep"], n, k).T, g[pre + "b_mask"].astype(bool)), pre
         assert rep.nnz_a == int(g[pre + "a_mask"].sum()) and rep.nnz_b == int(g[pre + "b_mask"].sum())
 
 
@@ -539,3 +543,33 @@ def test_graph_cache_alternating_shapes_reports():
                    (f.density_a, f.density_b, int(f.path), f.nnz_a, f.nnz_b)
             assert all(v >= 0 for v in r.timings.values())
             assert r.timings["xxmm"] > 0
+
+
+def test_out_argument_contract(oracle):
+    """xigemm(out=...) (api.py): out must be a contiguous float32 CUDA (M, N)
+    tensor not overlapping A or B; out aliasing C (BLAS-style in place) gives
+    the same result as a separate buffer; the host entry checks C's shape."""
+    m, k, n = 96, 160, 72
+    a = torch.from_numpy(ol.random_dense(m, k, 3, -2, 2)).cuda()
+    b = torch.from_numpy(ol.random_dense(k, n, 4, -2, 2)).cuda()
+    c = torch.from_numpy(ol.random_dense(m, n, 5, -1, 1)).cuda()
+    cfg = xg.XigemmConfig(threshold=0.2, scheme=xg.QuantScheme.VectorWise, policy=xg.ReductionPolicy.AvgRule)
+    want = xg.xigemm(a, b, c, 1.5, -0.75, cfg).result.clone()
+    for bad in (torch.empty((m, n + 1), device="cuda"), torch.empty((m, n), dtype=torch.float64, device="cuda"),
+                torch.empty((n, m), device="cuda").t(), torch.empty((m, n)),
+                a.view(-1)[: m * n].view(m, n)):
+        with pytest.raises(xg.InvalidArgument):
+            xg.xigemm(a, b, c, 1.5, -0.75, cfg, out=bad)
+    inplace = c.clone()
+    got = xg.xigemm(a, b, inplace, 1.5, -0.75, cfg, out=inplace)
+    assert got.result.data_ptr() == inplace.data_ptr() and beq(inplace, want)
+    an, bn = a.cpu().numpy(), b.cpu().numpy()
+    with pytest.raises(xg.InvalidArgument):
+        xg.xigemm_host(an, bn, np.zeros((m, n + 2), np.float32), cfg=cfg)
+    with pytest.raises(xg.InvalidArgument):
+        xg.xigemm_host(an, bn, cfg=cfg, out=np.zeros((m, n), np.float64))
+    with pytest.raises(xg.InvalidArgument):
+        xg.xigemm_host(an[0], bn, cfg=cfg)
+    cn = c.cpu().numpy()
+    out, _ = xg.xigemm_host(an, bn, cn, 1.5, -0.75, cfg=cfg, out=cn)  # in place on the host too
+    assert beq(out, want)

@@ -98,7 +98,23 @@ for seed in range(6):
                                        density_limit=0.5, scheme=1, policy=0, rounding=1))
     got = sharded.xigemm_sharded_local(a, b, cfg=cfg, nranks=3)
     assert np.array_equal(got.result.cpu().numpy().view(np.uint32), ref.view(np.uint32)), seed
-print("ok")
+# more flagged columns than the default 8-column exchange: XG_EAGAIN on every
+# shard, the exchange grows to the reported count and the run is redone
+grown = []
+orig = sharded.Shard.grow_remote
+def spy(self, needed):
+    grown.append(needed)
+    return orig(self, needed)
+sharded.Shard.grow_remote = spy
+m, k, n = 301, 512, 96
+a = torch.from_numpy(ol.random_dense(m, k, 7, -3, 3)).cuda()
+b = torch.from_numpy(ol.random_dense(k, n, 8, -3, 3)).cuda()
+rc, ref, orep = ol.oracle().xigemm(a.cpu().numpy(), b.cpu().numpy(), config=ol.cfg(threshold=0.05,
+                                   density_limit=0.5, scheme=1, policy=0, rounding=1))
+got = sharded.xigemm_sharded_local(a, b, cfg=cfg, nranks=3)
+assert np.array_equal(got.result.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+assert grown and max(grown) > 8, grown
+print("ok", grown)
 """
 
 
