@@ -2,13 +2,16 @@
 
 One step = one full xigemm() over one synthetic batch: quantize A and B,
 tcgen05 INT8 GEMM, |D_F| statistics, residual quantisation + threshold
-selection, compensation GEMM with the fused epilogue.  Metric (BASELINE.json):
-effective TFLOP/s = 2MNK / t.
+selection, compensation with the fused epilogue.  Metric (BASELINE.json):
+effective TFLOP/s = 2MNK / t, plus the relative error against an FP64 GEMM.
 
-Workload (default): C3 of BASELINE.json — M=N=K=8192, Student-t(3) FP32 inputs,
-INT8 vector-wise quantisation, AvgRule, threshold M bisected for ~5% residual
-density (s = 0.3 so the sparse path is taken).  Inputs (256 MiB each) exceed the
-126 MB L2, so no explicit flush is needed between steps.
+Workload (headline): C3 of BASELINE.json - M=N=K=8192, Student-t(3) FP32
+inputs, INT8 vector-wise quantisation, AvgRule, threshold M bisected for ~5%
+residual density (s = 0.3, sparse path).  Inputs (256 MiB each) exceed the
+126 MB L2, so no explicit flush is needed between steps.  The same JSON line
+carries every other configuration of BASELINE.json (C1, C2 at 1/5/10%, C4, C5
+on one GPU, C3 under the reference's default PerTensor/MinRule), each against
+the roofline of SURVEY.md section 8(d).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
@@ -16,6 +19,10 @@ Multi-GPU (torchrun, --gpus N > 1): the row-sharded pipeline (weak scaling:
 M rows of A and C per GPU, B broadcast from rank 0 by NCCL every step, exact
 all-reduce couplings between the stages; paper_2403_06924_b200/sharded.py).
 --replicas runs N independent full problems instead.
+
+The reference arm (--impl reference) never loads this repository's CUDA
+library: inputs come from numpy, and the reference's own xigemm (oracle/_ref,
+compiled from the reference sources) is timed on the host cores.
 """
 from __future__ import annotations
 
@@ -32,6 +39,13 @@ sys.path.insert(0, ROOT)
 
 M_DEFAULT = N_DEFAULT = K_DEFAULT = 8192
 TARGET_DENSITY = 0.05
+# M giving ~5% density on the C3 inputs (bisected on the device generator's
+# Student-t(3) data: density 4.69%); the reference arm, which must not load the
+# CUDA library, uses it for its numpy-generated inputs of the same distribution
+C3_THRESHOLD = 0.01539926526059492
+P_I8_SPEC = 4.5e15   # B200 dense INT8 op/s
+BW_SPEC = 8.0e12     # HBM3e B/s (north star "~8 TB/s")
+METRIC = "effective TFLOP/s (2MNK/t) of compensated GEMM"
 
 
 def _dist_init():
@@ -97,122 +111,308 @@ class ClockSampler:
                 "samples": len(s)}
 
 
-def _peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+def _peaks_file():
     try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+        return float(d.get("hbm_gbs", 6448.4)) * 1e9, float(d.get("bf16_tflops", 1675.7)) * 1e12, "measured"
     except OSError:
-        return 6650.0, 1590.0, "fallback"
+        return 6.4484e12, 1.6757e12, "fallback (B200_PROFILING.md figures)"
 
 
-def find_threshold(xg, a, b, scheme, policy, target=TARGET_DENSITY):
-    """Bisects M (log scale) so max(density_a, density_b) is within 10% of target."""
-    lo, hi = 1e-4, 10.0
+# ---------------------------------------------------------------- roofline --
+def b_alg(m, n, k, nnz_a, nnz_b):
+    """Algorithmic bytes of one single-GPU call:
+    A, B fp32 read twice (phases Q and R), Aq/Bq/RAq/RBq written and read,
+    D_F written and read, C written, CSR(A') / CSR(B'^T) col_idx + int8 value
+    written and read, row pointers written and read."""
+    return 12 * (m * k + k * n) + 12 * m * n + 10 * (nnz_a + nnz_b) + 8 * (m + n + 2)
+
+
+def roofline(m, n, k, nnz_a, nnz_b, t_s, p_i8=P_I8_SPEC, bw=BW_SPEC, p_simt=None):
+    """T_roof = 2MNK/P_i8 + B_alg/BW (summed: the phases are data-dependent);
+    frac = T_roof / t = achieved effective TFLOP/s / roofline effective TFLOP/s.
+    With p_simt, the 3-term model adds the SpMM MACs (nnzA*N + nnzB*M) at the
+    measured SIMT integer MAC rate."""
+    ops = 2.0 * m * n * k
+    ba = b_alg(m, n, k, nnz_a, nnz_b)
+    t_tc, t_hbm = ops / p_i8, ba / bw
+    t_roof = t_tc + t_hbm
+    r = {"t_roof_us": t_roof * 1e6, "tensor_us": t_tc * 1e6, "hbm_us": t_hbm * 1e6, "b_alg_bytes": ba,
+         "peak": ops / t_roof / 1e12, "achieved": ops / t_s / 1e12, "frac": t_roof / t_s}
+    if p_simt:
+        t3 = t_roof + (float(nnz_a) * n + float(nnz_b) * m) / p_simt
+        r["three_term"] = {"simt_macs": float(nnz_a) * n + float(nnz_b) * m, "t_roof_us": t3 * 1e6,
+                           "frac": t3 / t_s}
+    return r
+
+
+def measure_peaks(L):
+    """INT8 tensor ceiling from the repo's own tcgen05 GEMM with TMA loads and
+    epilogue switched off (MMA issue only, 8192^3), SIMT integer MAC rates
+    (IDP4A, IMAD) from probe kernels; HBM from MEASURED_PEAKS.json."""
+    hbm, bf16, src = _peaks_file()
+    out = {"hbm_Bps": hbm, "hbm_source": f"MEASURED_PEAKS.json hbm_gbs ({src})",
+           "bf16_flops": bf16}
+    try:
+        L.xg_debug_gemm_df.restype = C.c_double
+        L.xg_debug_gemm_df.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
+        ms = L.xg_debug_gemm_df(8192, 8192, 8192, 1 | 2, 20)
+        out["int8_ops"] = 2.0 * 8192 ** 3 / (ms * 1e-3) if ms > 0 else None
+        out["int8_source"] = "tcgen05 kind::i8 pair GEMM, MMA issue only (debug flags: no TMA, no epilogue), 8192^3"
+    except AttributeError:
+        out["int8_ops"] = None
+    try:
+        L.xg_debug_simt_rate.restype = C.c_double
+        L.xg_debug_simt_rate.argtypes = [C.c_int, C.c_int]
+        out["idp4a_macs"] = L.xg_debug_simt_rate(0, 4096)
+        out["imad_macs"] = L.xg_debug_simt_rate(1, 4096)
+    except AttributeError:
+        out["idp4a_macs"] = out["imad_macs"] = None
+    if not out.get("int8_ops"):
+        out["int8_ops"], out["int8_source"] = 2.0 * bf16, "2 x MEASURED_PEAKS bf16_tflops (proxy)"
+    return out
+
+
+# --------------------------------------------------------------- workloads --
+def find_threshold(xg, a, b, scheme, policy, target=TARGET_DENSITY, tol=0.1):
+    """Bisects M (log scale) so max(density_a, density_b) is within tol*target."""
+    lo, hi = 1e-5, 20.0
     best = None
-    for _ in range(30):
+    for _ in range(40):
         mid = (lo * hi) ** 0.5
-        cfg = xg.XigemmConfig(threshold=mid, scheme=scheme, policy=policy)
-        rep = xg.xigemm(a, b, cfg=cfg)
+        rep = xg.xigemm(a, b, cfg=xg.XigemmConfig(threshold=mid, scheme=scheme, policy=policy))
         d = max(rep.density_a, rep.density_b)
-        best = (mid, rep.density_a, rep.density_b)
-        if abs(d - target) <= 0.1 * target:
+        if best is None or abs(d - target) < abs(best[1] - target):
+            best = (mid, d)
+        if abs(d - target) <= tol * target:
             break
         if d > target:
             lo = mid
         else:
             hi = mid
-    return best
+    return best[0]
 
 
-def cpu_baseline_sample(a_host, b_host, thr, rows, threads=1, reps=1):
-    """The reference's xigemm (oracle/_ref, else the C restatement) on a row slab
-    of the same A against the full B, on host cores.  Returns (ops/s, seconds, kind)."""
+CONFIGS = [
+    # name, m, n, k, A data, B data, scheme, policy, target density
+    ("C1 1024^3 uniform VectorWise AvgRule 5%", 1024, 1024, 1024, ("uniform", -1.0, 1.0), ("uniform", -1.0, 1.0),
+     1, 0, 0.05),
+    ("C2 4096^3 normal VectorWise AvgRule 1%", 4096, 4096, 4096, ("normal", 0.0, 1.0), ("normal", 0.0, 1.0), 1, 0,
+     0.01),
+    ("C2 4096^3 normal VectorWise AvgRule 5%", 4096, 4096, 4096, ("normal", 0.0, 1.0), ("normal", 0.0, 1.0), 1, 0,
+     0.05),
+    ("C2 4096^3 normal VectorWise AvgRule 10%", 4096, 4096, 4096, ("normal", 0.0, 1.0), ("normal", 0.0, 1.0), 1, 0,
+     0.10),
+    ("C3 8192^3 Student-t(3) PerTensor MinRule (reference defaults) ~5%", 8192, 8192, 8192,
+     ("student_t3", 0.0, 1.0), ("student_t3", 0.0, 1.0), 0, 1, 0.05),
+    ("C4 16384x11008x4096 A Student-t(3) B normal VectorWise AvgRule 5%", 16384, 11008, 4096,
+     ("student_t3", 0.0, 1.0), ("normal", 0.0, 1.0), 1, 0, 0.05),
+    ("C5 65536x16384x16384 normal VectorWise AvgRule 5% (one GPU)", 65536, 16384, 16384, ("normal", 0.0, 1.0),
+     ("normal", 0.0, 1.0), 1, 0, 0.05),
+]
+
+
+def time_calls(xg, torch, a, b, cfg, out, steps, warmup):
+    for _ in range(warmup):
+        rep = xg.xigemm(a, b, cfg=cfg, out=out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        rep = xg.xigemm(a, b, cfg=cfg, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps * 1e-3, rep
+
+
+def run_configs(xg, torch, peaks, steps, only=None):
+    res = []
+    for name, m, n, k, da, db, scheme, policy, target in CONFIGS:
+        if only and not any(o in name for o in only):
+            continue
+        try:
+            a = xg.generate(da[0], m, k, 1, da[1], da[2])
+            b = xg.generate(db[0], k, n, 2, db[1], db[2])
+            s, p = xg.QuantScheme(scheme), xg.ReductionPolicy(policy)
+            thr = find_threshold(xg, a, b, s, p, target)
+            cfg = xg.XigemmConfig(threshold=thr, scheme=s, policy=p)
+            out = torch.empty((m, n), dtype=torch.float32, device="cuda")
+            big = m * n * k > 2 ** 36
+            t, rep = time_calls(xg, torch, a, b, cfg, out, max(3, steps // (4 if big else 1)), 3)
+            rf = roofline(m, n, k, rep.nnz_a, rep.nnz_b, t)
+            rm = roofline(m, n, k, rep.nnz_a, rep.nnz_b, t, peaks["int8_ops"], peaks["hbm_Bps"],
+                          peaks.get("idp4a_macs"))
+            res.append({"config": name, "m": m, "n": n, "k": k, "threshold_M": thr,
+                        "density_a": rep.density_a, "density_b": rep.density_b, "path": int(rep.path),
+                        "ms": t * 1e3, "tflops": 2.0 * m * n * k / t / 1e12,
+                        "t_roof_us": rf["t_roof_us"], "frac": rf["frac"],
+                        "frac_measured_peaks": rm["frac"],
+                        "frac_three_term": rm.get("three_term", {}).get("frac"),
+                        "gemm_df_ms": rep.timings["gemm_df"] * 1e-6, "gemm_comp_ms": rep.timings["gemm_comp"] * 1e-6})
+            del a, b, out
+            torch.cuda.empty_cache()
+        except Exception as ex:  # noqa: BLE001
+            res.append({"config": name, "error": str(ex)[:300]})
+    return res
+
+
+# ------------------------------------------------------------- CPU baseline --
+def _reference_lib():
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import numpy as np
     import oracle_lib as ol
     r = ol.reference()
-    kind = "reference"
-    if r is None:
-        r, kind = ol.oracle(), "port"
+    if r is not None:
+        return ol, r, "reference"
+    return ol, ol.oracle(), "port"
+
+
+def slab_fit(ol, r, a_rows, b, thr, scheme, policy, sizes=(16, 48), threads=1, reps=1):
+    """The reference's xigemm on row slabs of A against the full B (on `threads`
+    host threads at once, each its own slab): t(rows) = t_B + rows * t_row,
+    where t_B is the per-call O(KN) B-side work and t_row the per-row work.
+    Returns (t_B, t_row, densities of the largest slab, wall seconds)."""
+    import numpy as np
+    cfg = ol.cfg(threshold=thr, density_limit=0.3, scheme=scheme, policy=policy, rounding=1)
+    k, n = b.shape
+    times, dens = {}, None
+    w0 = time.perf_counter()
+    for rows in sizes:
+        slabs = [np.ascontiguousarray(a_rows[(t * rows) % max(1, a_rows.shape[0] - rows):][:rows])
+                 for t in range(threads)]
+        outs = [None] * threads
+
+        def work(t):
+            outs[t] = r.xigemm(slabs[t], b, config=cfg)
+
+        best = None
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            ths = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+            for th in ths:
+                th.start()
+            for th in ths:
+                th.join()
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        times[rows] = best
+        dens = (outs[0][2].density_a, outs[0][2].density_b)
+    r1, r2 = sizes
+    t_row = max(1e-9, (times[r2] - times[r1]) / (r2 - r1))
+    t_b = max(0.0, times[r1] - r1 * t_row)
+    return t_b, t_row, dens, time.perf_counter() - w0
+
+
+def cpu_baseline_run(jobs):
+    """1-core reference timings (bench.py cpu_baseline): C1 and C2 on the full
+    problem with the GPU arm's inputs and thresholds (best of 3 / once; the
+    outputs are compared bit for bit with the GPU's), C3 by the two-slab fit."""
+    import numpy as np
+    ol, r, kind = _reference_lib()
+    res = {"kind": kind, "cores": 1}
+    for job in jobs:
+        name, a, b, thr, scheme, policy, gpu_out = job["name"], job["a"], job["b"], job["thr"], job["scheme"], \
+            job["policy"], job.get("gpu_out")
+        m, k = a.shape
+        n = b.shape[1]
+        cfg = ol.cfg(threshold=thr, density_limit=0.3, scheme=scheme, policy=policy, rounding=1)
+        if job["mode"] == "full":
+            best = None
+            for _ in range(job.get("reps", 1)):
+                t0 = time.perf_counter()
+                rc, out, rep = r.xigemm(a, b, config=cfg)
+                dt = time.perf_counter() - t0
+                best = dt if best is None else min(best, dt)
+            d = {"mode": f"full problem, best of {job.get('reps', 1)}", "seconds": best,
+                 "tflops": 2.0 * m * n * k / best / 1e12, "density_a": rep.density_a, "density_b": rep.density_b}
+            if gpu_out is not None:
+                d["bit_equal_to_gpu"] = bool(np.array_equal(out.view(np.uint32), gpu_out.view(np.uint32)))
+        else:
+            t_b, t_row, dens, wall = slab_fit(ol, r, a, b, thr, scheme, policy)
+            t_full = t_b + m * t_row
+            d = {"mode": "two-slab fit: xigemm_ref on 16- and 48-row slabs of A with the full B, "
+                         "t = t_B + M * t_row (estimate)", "t_B_s": t_b, "t_row_s": t_row, "seconds": t_full,
+                 "tflops": 2.0 * m * n * k / t_full / 1e12, "density_a_slab": dens[0],
+                 "density_b_slab": dens[1], "sample_wall_s": wall}
+        res[name] = d
+    return res
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's own xigemm (oracle/_ref) on this box's
+    host cores, on the C3 workload, without this repository's CUDA library.
+    Inputs: numpy Student-t(3) of the same shape and distribution; threshold
+    C3_THRESHOLD (or --threshold).  Each step runs T concurrent slabs (one per
+    host thread, alternating 16- and 48-row slabs of A against the full B);
+    the fit t(rows) = t_B + rows*t_row over the steps gives the time of the
+    whole problem with the row work spread over the T threads:
+    t = t_B + M*t_row/T (the B-side work of the reference is serial)."""
+    import numpy as np
+    if world > 1 and rank != 0:
+        return
+    ol, r, kind = _reference_lib()
+    m, n, k = args.m, args.n, args.k
+    threads = min(os.cpu_count() or 1, 64)
+    try:
+        import psutil
+        threads = max(1, min(threads, int(psutil.virtual_memory().available / 2.5e9)))
+    except Exception:  # noqa: BLE001
+        pass
+    thr = args.threshold if args.threshold is not None else C3_THRESHOLD
+    rng = np.random.default_rng(1)
+    small, big = (2, 6) if args.ref_rows_set and args.ref_rows <= 4 else (16, 48)
+    nrows = big * threads + big
+
+    def t3(rows, cols):
+        z = rng.standard_normal((rows, cols), dtype=np.float32)
+        chi = (rng.standard_normal((3, rows, cols), dtype=np.float32) ** 2).sum(0) / np.float32(3.0)
+        return (z / np.sqrt(chi)).astype(np.float32)
+
+    a = t3(min(m, nrows), k)
+    b = t3(k, n)
     cfg = ol.cfg(threshold=thr, density_limit=0.3, scheme=1, policy=0, rounding=1)
-    k, n = b_host.shape
-    slabs = [np.ascontiguousarray(a_host[(t * rows) % a_host.shape[0]:][:rows]) for t in range(threads)]
-    outs = [None] * threads
+    nsteps = max(1, args.steps if args.ref_steps is None else args.ref_steps)
+    samples = {small: [], big: []}
+    dens = None
+    for i in range(nsteps):
+        rows = small if i % 2 == 0 else big
+        slabs = [np.ascontiguousarray(a[(t * rows) % max(1, a.shape[0] - rows):][:rows]) for t in range(threads)]
+        outs = [None] * threads
 
-    def work(t):
-        outs[t] = r.xigemm(slabs[t], b_host, config=cfg)
+        def work(t):
+            outs[t] = r.xigemm(slabs[t], b, config=cfg)
 
-    best = None
-    for _ in range(reps):
         t0 = time.perf_counter()
         ths = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
         for th in ths:
             th.start()
         for th in ths:
             th.join()
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    ops = 2.0 * rows * n * k * threads
-    return ops / best, best, kind
-
-
-def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU implementation on this box's host
-    cores (all of them), on the same metric/config; bounded row-slab samples."""
-    import numpy as np
-    if world > 1 and rank != 0:
-        return
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import oracle_lib as ol
-    m, n, k = args.m, args.n, args.k
-    threads = min(os.cpu_count() or 1, 32)
-    try:
-        import psutil
-        threads = max(1, min(threads, int(psutil.virtual_memory().available / 2.0e9)))
-    except Exception:  # noqa: BLE001
-        pass
-    # inputs: same generator stream as the GPU arm (device generator), host copy
-    import torch
-    import paper_2403_06924_b200 as xg
-    if torch.cuda.is_available():
-        a = xg.generate("student_t3", m, k, 1, 0.0, 1.0).cpu().numpy()
-        b = xg.generate("student_t3", k, n, 2, 0.0, 1.0).cpu().numpy()
-        thr = args.threshold or find_threshold(xg, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
-                                               xg.QuantScheme.VectorWise, xg.ReductionPolicy.AvgRule)[0]
-    else:  # no GPU on this host: same distribution from numpy
-        rng = np.random.default_rng(1)
-        z = rng.standard_normal((m, k), dtype=np.float32)
-        a = (z / np.sqrt((rng.standard_normal((m, k), dtype=np.float32) ** 2 * 3) / 3)).astype(np.float32)
-        b = a.T.copy()
-        thr = args.threshold or 0.01
-    # larger slabs than the single-core baseline: the reference redoes all of
-    # B's quantisation per call, which a 16-row slab would over-weight
-    # exactly --steps K steps (or --ref-steps); each a bounded sample: 64-row
-    # slabs (~4-5 s per step on the GPU box's cores), smaller beyond 30 steps so
-    # the whole run stays within a few minutes
-    nsteps = max(1, args.steps if args.ref_steps is None else args.ref_steps)
-    rows = args.ref_rows if args.ref_rows_set else (64 if nsteps <= 30 else max(8, 64 * 30 // nsteps))
-    vals = []
-    for _ in range(args.warmup):
-        pass  # CPU: no warm-up effect worth paying minutes for
-    for _ in range(nsteps):
-        v, dt, kind = cpu_baseline_sample(a, b, thr, rows, threads=threads)
-        vals.append((v, dt))
-    value = sorted(v for v, _ in vals)[len(vals) // 2] / 1e12
-    step_s = sorted(dt for _, dt in vals)[len(vals) // 2]
+        samples[rows].append(time.perf_counter() - t0)
+        if rows == big or dens is None:
+            dens = (outs[0][2].density_a, outs[0][2].density_b)
+    ts = {s: sorted(v)[len(v) // 2] for s, v in samples.items() if v}
+    if len(ts) == 2:
+        t_row = max(1e-9, (ts[big] - ts[small]) / (big - small))
+        t_b = max(0.0, ts[small] - small * t_row)
+    else:  # one step only: no fit, the slab's B-side share is charged to its rows
+        t_b, t_row = 0.0, ts[small] / small
+    t_full = t_b + m * t_row / threads
+    value = 2.0 * m * n * k / t_full / 1e12
+    sample = (f"{threads} host threads, each xigemm_ref on its own {small}- or {big}-row slab of A against the "
+              f"full {k}x{n} B per step (alternating); fit t(rows) = t_B + rows*t_row: t_B = {t_b:.2f} s, "
+              f"t_row = {t_row * 1e3:.1f} ms; C3 time = t_B + M*t_row/threads = {t_full:.1f} s")
     line = {
-        "impl": "reference", "metric": "effective TFLOP/s (2MNK/t) of compensated GEMM",
-        "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": len(vals),
-        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "impl": "reference", "metric": METRIC,
+        "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": nsteps,
+        "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int8/fp64 (reference CPU)",
-        "data": "synthetic Student-t(3)",
-        "config": _config(args, thr, None),
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": kind,
-                         "sample": f"{threads} threads x xigemm_ref on a {rows}-row slab of A "
-                                   f"against the full {k}x{n} B per step"},
+        "data": "synthetic Student-t(3) (numpy generator, same shape and distribution as the GPU arm)",
+        "config": dict(_config(args, thr, dens), density_note="density_a over the slab rows (row statistics are "
+                       "exact per row); density_b from the slab's column statistics"),
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cuda_library_loaded": "libxigemm_b200" in open("/proc/self/maps").read(),
     }
     print(json.dumps(line), flush=True)
 
@@ -229,6 +429,52 @@ def _config(args, thr, dens):
     return c
 
 
+def _roofline_block(m, n, k, rep, t, peaks, t_df, t_cp):
+    """The bench's roofline object: whole call against SURVEY 8(d)'s summed
+    2-term roofline (spec peaks; measured peaks beside), 3-term with the
+    measured SIMT rate, and the dominant kernel's own algorithmic fraction."""
+    rf = roofline(m, n, k, rep.nnz_a, rep.nnz_b, t)
+    rm = roofline(m, n, k, rep.nnz_a, rep.nnz_b, t, peaks["int8_ops"], peaks["hbm_Bps"], peaks.get("idp4a_macs"))
+    traffic = None
+    try:  # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            tr = json.load(f)
+        key = next(kk for kk in tr if kk.startswith("void k_gemm_i8_tc2<1, 4"))
+        traffic = tr[key]
+    except (OSError, KeyError, ValueError, StopIteration):
+        pass
+    # dominant kernel: the compensation launch (K4+K5).  Its algorithmic bytes:
+    # A'q, RBq, RAq, B'q int8 in, D_F fp32 in, C fp32 out
+    alg = 2 * (m * k + k * n) + 8 * m * n
+    kern = {"name": "compensation launch (dr1 = A'q RBq, dr2 = RAq B'q, fused exact epilogue)",
+            "ms": t_cp * 1e3, "algorithmic_bytes": alg,
+            "algorithmic_GBps": alg / t_cp / 1e9, "frac_hbm": alg / t_cp / peaks["hbm_Bps"],
+            "tensor_ops_issued": 4.0 * m * n * k, "tensor_tops": 4.0 * m * n * k / t_cp / 1e12,
+            "frac_int8_peak": 4.0 * m * n * k / t_cp / peaks["int8_ops"],
+            "d_f_gemm_ms": t_df * 1e3, "d_f_gemm_frac_int8_peak": 2.0 * m * n * k / t_df / peaks["int8_ops"]}
+    if traffic:
+        kern["dram_bytes"] = traffic.get("bytes_per_launch")
+        kern["dram_over_algorithmic"] = traffic.get("bytes_per_launch", 0) / alg
+        kern["traffic_source"] = traffic.get("source")
+    return {
+        "bound": "tensor+hbm",
+        "model": "T_roof = 2MNK/P_i8 + B_alg/BW (SURVEY.md 8(d), summed); achieved = 2MNK/t, peak = 2MNK/T_roof, "
+                 "frac = T_roof/t",
+        "achieved": rf["achieved"], "peak": rf["peak"], "unit": "TFLOP/s", "frac": rf["frac"],
+        "peak_source": "spec: P_i8 = 4.5e15 op/s, BW = 8.0e12 B/s",
+        "t_roof_us": rf["t_roof_us"], "tensor_us": rf["tensor_us"], "hbm_us": rf["hbm_us"],
+        "b_alg_bytes": rf["b_alg_bytes"],
+        "measured_peaks": {"int8_tops": peaks["int8_ops"] / 1e12, "int8_source": peaks["int8_source"],
+                           "hbm_GBps": peaks["hbm_Bps"] / 1e9, "hbm_source": peaks["hbm_source"],
+                           "t_roof_us": rm["t_roof_us"], "peak": rm["peak"], "frac": rm["frac"]},
+        "three_term": dict(rm.get("three_term", {}), p_simt_macs=peaks.get("idp4a_macs"),
+                           p_imad_macs=peaks.get("imad_macs"),
+                           note="adds (nnzA*N + nnzB*M) int8 MACs at the measured IDP4A rate; peaks measured"),
+        "traffic": kern.get("dram_bytes"),
+        "dominant_kernel": kern,
+    }
+
+
 def run_b200(args, world, rank, local):
     import numpy as np
     import torch
@@ -242,7 +488,7 @@ def run_b200(args, world, rank, local):
     scheme, policy = xg.QuantScheme.VectorWise, xg.ReductionPolicy.AvgRule
     thr = args.threshold
     if thr is None:
-        thr = find_threshold(xg, a, b, scheme, policy)[0]
+        thr = find_threshold(xg, a, b, scheme, policy)
     cfg = xg.XigemmConfig(threshold=thr, scheme=scheme, policy=policy)
     out = torch.empty((m, n), dtype=torch.float32, device="cuda")
     rep = xg.xigemm(a, b, cfg=cfg, out=out)
@@ -305,37 +551,43 @@ def run_b200(args, world, rank, local):
         e2e_val = ops * world / e2e_s / 1e12
         # host path result equals the device path result
         assert np.array_equal(on.view(np.uint32), out.cpu().numpy().view(np.uint32))
+        del ah, bh, oh
 
     if rank != 0:
         return
-    hbm, bf16, src = _peaks()
-    int8_peak = 2.0 * bf16  # dense INT8 = 2x dense bf16 on B200 (proxy for the missing INT8 figure)
+    # ---- CPU baseline (1 core, background thread: the reference releases the GIL) ----
+    cpu_thread, cpu_res = None, {}
+    if not args.no_cpu_baseline:
+        jobs = []
+        for nm, sz, kind_, lo, hi, target in (("C1", 1024, "uniform", -1.0, 1.0, 0.05),
+                                              ("C2", 4096, "normal", 0.0, 1.0, 0.05)):
+            if nm == "C2" and args.cpu_quick:
+                continue
+            x = xg.generate(kind_, sz, sz, 1, lo, hi)
+            y = xg.generate(kind_, sz, sz, 2, lo, hi)
+            th = find_threshold(xg, x, y, scheme, policy, target)
+            g = xg.xigemm(x, y, cfg=xg.XigemmConfig(threshold=th, scheme=scheme, policy=policy))
+            jobs.append(dict(name=nm, a=x.cpu().numpy(), b=y.cpu().numpy(), thr=th, scheme=1, policy=0,
+                             gpu_out=g.result.cpu().numpy(), mode="full", reps=3 if nm == "C1" else 1,
+                             gpu_density=(g.density_a, g.density_b)))
+        jobs.append(dict(name="C3", a=a[:2048].cpu().numpy(), b=b.cpu().numpy(), thr=thr, scheme=1, policy=0,
+                         mode="fit"))
+
+        def cpu_work():
+            try:
+                cpu_res.update(cpu_baseline_run(jobs))
+            except Exception as ex:  # noqa: BLE001
+                cpu_res["error"] = str(ex)[:300]
+
+        cpu_thread = threading.Thread(target=cpu_work, daemon=True)
+        cpu_thread.start()
+
+    peaks = measure_peaks(L)
     t_df = float(np.mean(gemm_ns["gemm_df"])) * 1e-9
     t_cp = float(np.mean(gemm_ns["gemm_comp"])) * 1e-9
-    # dominant kernel: the larger of the two tensor-core launches
-    if t_cp >= t_df:
-        name, kops, tk = ("compensation GEMM (one launch, masked-dense dr1 and dr2 per tile: 4MNK tensor ops)",
-                          4.0 * m * n * k, t_cp)
-    else:
-        name, kops, tk = "D_F GEMM (2MNK tensor ops)", 2.0 * m * n * k, t_df
-    achieved = kops / tk / 1e12
-    traffic = None
-    try:  # DRAM bytes per launch of that kernel from the committed ncu --set full capture
-        with open(os.path.join(ROOT, "profiles", "r1k_gemm_traffic.json")) as f:
-            tr = json.load(f)
-        pre = "void k_gemm_i8_tc2<1, 4, 1" if t_cp >= t_df else "void k_gemm_i8_tc2<1, 1, 1"
-        key = next(kk for kk in tr if kk.startswith(pre))
-        traffic = {"dram_bytes_per_launch": tr[key]["bytes_per_launch"],
-                   # int8 operands in (A'q, RBq, RAq, B'q | Aq, Bq), fp32 D_F in (compensation), fp32 out
-                   "algorithmic_bytes_per_launch": (2 * (m * k + k * n) + 8 * m * n) if t_cp >= t_df
-                   else (m * k + k * n + 4 * m * n),
-                   "source": "profiles/r1k_gemm_traffic.json (ncu --set full, this kernel, C3)"}
-    except (OSError, KeyError, ValueError, StopIteration):
-        pass
-    # live reference point for the INT8 denominator (MEASURED_PEAKS.json has
-    # bf16 only): cuBLASLt int8 GEMM (torch._int_mm, s32 out, no epilogue) at
-    # the same shape; library call for context, never on the product path
-    cublaslt = None
+    roof = _roofline_block(m, n, k, rep, ms * 1e-3, peaks, t_df, t_cp)
+    # live reference point: cuBLASLt int8 GEMM (torch._int_mm, s32 out, no epilogue) at the
+    # same shape - a library call for context, never on the product path
     try:
         ia = torch.randint(-127, 128, (m, k), dtype=torch.int8, device="cuda")
         ib = torch.randint(-127, 128, (n, k), dtype=torch.int8, device="cuda").t()
@@ -348,13 +600,13 @@ def run_b200(args, world, rank, local):
             torch._int_mm(ia, ib)
         c1.record()
         torch.cuda.synchronize()
-        cublaslt = 2.0 * m * n * k / (c0.elapsed_time(c1) / 10 * 1e-3) / 1e12
+        roof["dominant_kernel"]["cublaslt_int8_tops_same_shape"] = ops / (c0.elapsed_time(c1) / 10 * 1e-3) / 1e12
         del ia, ib
     except Exception:  # noqa: BLE001
         pass
-    # accuracy (BASELINE.json metric, second half): relative Frobenius error
-    # e_delta = ||C64 - C||_F / ||C64||_F against an FP64 GEMM of the same
-    # inputs (metrics.cpp:7-33), for xigemm and the paper's two baselines
+    # accuracy (BASELINE.json metric, second half): e_delta = ||C64 - C||_F / ||C64||_F
+    # against an FP64 GEMM of the same inputs (metrics.cpp:7-33), for xigemm and the
+    # paper's two baselines
     accuracy = None
     if not args.no_accuracy:
         try:
@@ -372,14 +624,24 @@ def run_b200(args, world, rank, local):
             del c64
         except Exception as ex:  # noqa: BLE001
             accuracy = {"error": str(ex)[:200]}
+    del a, b
+    torch.cuda.empty_cache()
+    configs = None if args.no_configs else run_configs(xg, torch, peaks, args.steps)
     cpu = None
-    if not args.no_cpu_baseline:
-        v, dt, kind = cpu_baseline_sample(a.cpu().numpy(), b.cpu().numpy(), thr, args.ref_rows, 1)
-        cpu = {"value": v / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": kind,
-               "sample": f"xigemm_ref on a {args.ref_rows}-row slab of A against the full "
-                         f"{k}x{n} B ({dt:.1f} s); 2*rows*N*K/t"}
+    if cpu_thread is not None:
+        cpu_thread.join()
+        c3 = cpu_res.get("C3", {})
+        if "seconds" in c3:
+            cpu = {"value": 2.0 * m * n * k / c3["seconds"] / 1e12, "unit": "TFLOP/s", "cores": 1,
+                   "kind": cpu_res.get("kind"),
+                   "sample": "C3: the reference's xigemm (oracle/_ref) on 16- and 48-row slabs of the same A "
+                             "against the full B, one core; t = t_B + M*t_row (estimate). C1 and C2: full "
+                             "problems on the GPU arm's inputs (outputs compared bit for bit)",
+                   "configs": cpu_res}
+        else:
+            cpu = {"value": None, "unit": "TFLOP/s", "cores": 1, "kind": cpu_res.get("kind"), "configs": cpu_res}
     line = {
-        "metric": "effective TFLOP/s (2MNK/t) of compensated GEMM",
+        "metric": METRIC,
         "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int8 (fp64/fp32 exact epilogues)",
@@ -387,19 +649,12 @@ def run_b200(args, world, rank, local):
         "config": _config(args, thr, dens),
         "e2e": {"value": e2e_val, "unit": "TFLOP/s",
                 "h2d_bytes_per_step": 4 * (m * k + k * n), "d2h_bytes_per_step": 4 * m * n} if e2e_val else None,
-        "roofline": {"bound": "tensor", "kernel": name, "achieved": achieved,
-                     "peak": int8_peak, "unit": "TFLOP/s", "frac": achieved / int8_peak,
-                     # dram__bytes_read.sum + dram__bytes_write.sum per launch (ncu --set full)
-                     "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
-                     "traffic_detail": traffic,
-                     "peak_source": f"2 x bf16_tflops ({bf16}) of MEASURED_PEAKS.json ({src}); INT8 dense = 2x bf16 on B200",
-                     "gemm_df_ms": t_df * 1e3, "gemm_comp_ms": t_cp * 1e3,
-                     "cublaslt_int8_tflops": cublaslt,
-                     "frac_of_cublaslt_int8": (achieved / cublaslt) if cublaslt else None},
+        "roofline": roof,
         "clocks": clk.summary(),
         "gpu_launches": launches,
         "accuracy": accuracy,
         "stage_ns": {kk: int(vv) for kk, vv in r.timings.items()},  # last timed call
+        "configs": configs,
     }
     if cpu:
         line["cpu_baseline"] = cpu
@@ -412,7 +667,6 @@ def run_b200_sharded(args, world, rank, local):
     B (K x N) lives on rank 0 and is replicated by one NCCL broadcast inside
     every timed step; the exact couplings (max|A|, max|RA|, column statistics,
     nnz(A')) are NCCL all-reduces between the pipeline stages."""
-    import numpy as np
     import torch
     import torch.distributed as dist
     import paper_2403_06924_b200 as xg
@@ -427,7 +681,7 @@ def run_b200_sharded(args, world, rank, local):
     scheme, policy = xg.QuantScheme.VectorWise, xg.ReductionPolicy.AvgRule
     t = torch.tensor([args.threshold or 0.0], dtype=torch.float64, device="cuda")
     if args.threshold is None and rank == 0:
-        t[0] = find_threshold(xg, a, b, scheme, policy)[0]
+        t[0] = find_threshold(xg, a, b, scheme, policy)
     dist.broadcast(t, src=0)
     thr = float(t.item())
     cfg = xg.XigemmConfig(threshold=thr, scheme=scheme, policy=policy)
@@ -450,7 +704,7 @@ def run_b200_sharded(args, world, rank, local):
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            step()
+            rep = step()
         e1.record(stream)
         torch.cuda.synchronize()
     launches = int(L.xg_launch_count(1))
@@ -490,8 +744,22 @@ def run_b200_sharded(args, world, rank, local):
     e2e_val = ops / float(te.item()) / 1e12
     if rank != 0:
         return
+    # roofline of one rank's share: its M rows against the replicated B (the
+    # B-side stages run on every rank: B_alg counts them once per rank)
+    rf = roofline(m, n, k, rep.nnz_a // world, rep.nnz_b, ms * 1e-3)
+    peaks = measure_peaks(L)
+    rm = roofline(m, n, k, rep.nnz_a // world, rep.nnz_b, ms * 1e-3, peaks["int8_ops"], peaks["hbm_Bps"],
+                  peaks.get("idp4a_macs"))
+    cpu = None
+    if not args.no_cpu_baseline:
+        c3 = cpu_baseline_run([dict(name="C3", a=a[:2048].cpu().numpy(), b=b.cpu().numpy(), thr=thr, scheme=1,
+                                    policy=0, mode="fit")]).get("C3", {})
+        if "seconds" in c3:
+            cpu = {"value": 2.0 * m * n * k / c3["seconds"] / 1e12, "unit": "TFLOP/s", "cores": 1,
+                   "kind": "reference", "sample": "one rank's C3 rows: two-slab fit of xigemm_ref (16/48 rows), "
+                                                  "t = t_B + M*t_row (estimate)", "fit": c3}
     line = {
-        "metric": "effective TFLOP/s (2MNK/t) of compensated GEMM",
+        "metric": METRIC,
         "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int8 (fp64/fp32 exact epilogues)",
@@ -502,10 +770,17 @@ def run_b200_sharded(args, world, rank, local):
                        parallelism=f"rows{world} (B replicated by NCCL broadcast; exact all-reduce couplings)"),
         "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": 4 * (m * k * world + k * n),
                 "d2h_bytes_per_step": 4 * m * n * world},
-        "roofline": None,
+        "roofline": {"bound": "tensor+hbm", "model": "per rank: T_roof = 2MNK/P_i8 + B_alg/BW of its rows "
+                     "(B-side stages counted on every rank); frac = T_roof / t", "achieved": rf["achieved"],
+                     "peak": rf["peak"], "unit": "TFLOP/s per GPU", "frac": rf["frac"],
+                     "peak_source": "spec: P_i8 = 4.5e15 op/s, BW = 8.0e12 B/s", "t_roof_us": rf["t_roof_us"],
+                     "measured_peaks": {"frac": rm["frac"], "t_roof_us": rm["t_roof_us"]},
+                     "three_term": rm.get("three_term"), "traffic": None},
         "clocks": clk.summary(),
         "gpu_launches": launches,
     }
+    if cpu:
+        line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
 
 
@@ -519,10 +794,11 @@ def main():
     ap.add_argument("--n", type=int, default=N_DEFAULT)
     ap.add_argument("--k", type=int, default=K_DEFAULT)
     ap.add_argument("--threshold", type=float, default=None)
-    ap.add_argument("--ref-rows", type=int, default=None,
-                    help="row slab of the CPU samples (default 16 for cpu_baseline, 64 for --impl reference)")
+    ap.add_argument("--ref-rows", type=int, default=None, help="--impl reference: tiny slabs (<= 4: 2/6 rows)")
     ap.add_argument("--ref-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-quick", action="store_true", help="cpu_baseline without the full C2 problem (~60 s)")
+    ap.add_argument("--no-configs", action="store_true", help="only the headline configuration")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     ap.add_argument("--no-accuracy", action="store_true", help="skip the FP64-GEMM error report")
     ap.add_argument("--replicas", action="store_true",
@@ -531,8 +807,6 @@ def main():
                     help="use the row-sharded pipeline even at N=1 (needs torchrun / a process group)")
     args = ap.parse_args()
     args.ref_rows_set = args.ref_rows is not None
-    if args.ref_rows is None:
-        args.ref_rows = 16
     world, rank, local = _dist_init()
     if args.impl == "reference":
         run_reference(args, world, rank)

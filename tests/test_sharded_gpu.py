@@ -119,12 +119,12 @@ print("ok", grown)
 
 
 def test_sharded_remote_exact_means_widened():
-    """XG_STATS_WIDEN=20 flags every AvgRule mean; column means whose kept set
+    """XG_STATS_WIDEN=40 flags every AvgRule mean (and widens the candidate interval to ~15%); column means whose kept set
     could change are recomputed from the all-gathered D_F columns in global row
     order (collective point 3).  Must still match the reference oracle."""
     here = os.path.dirname(os.path.abspath(__file__))
     code = _WIDEN_SCRIPT.format(root=os.path.dirname(here), tests=here)
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, XG_STATS_WIDEN="20"),
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, XG_STATS_WIDEN="40"),
                        capture_output=True, text=True)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
 
