@@ -68,6 +68,8 @@ typedef struct {
     int stats_fallbacks; /* AvgRule statistics recomputed in exact order */
     double ns_gemm_df;   /* device time of the D_F GEMM launch (K2) */
     double ns_gemm_comp; /* device time of the compensation GEMM launch (K4+K5) */
+    int comp_kernel;     /* the sparse terms ran on: 0 tcgen05 masked-dense launch,
+                            1 CUDA-core quad-packed CSR SpMM (same result, bit for bit) */
 } xg_report;
 
 /* Device pointers (reference row-major layouts) receiving pipeline
@@ -158,6 +160,22 @@ xg_status xg_csr_transpose_f32(int rows, int cols, const int32_t *row_ptr, const
 xg_status xg_spmm_i8(int rows, int cols, const int32_t *row_ptr, const int32_t *col_idx,
                      const int8_t *values, const int8_t *d, int d_cols, int d_bits, int32_t *out,
                      xg_stream s);
+/* Compensation kernel choice of the SparseResidual branch (no reference
+ * equivalent: the reference always runs spmm_int there, pipeline.cpp:118-124).
+ * The device picks the tcgen05 masked-dense launch or the CUDA-core CSR SpMM
+ * from t_dense = 4MNK/p_tc against t_csr = max((nnzA N + nnzB M)/p_sp,
+ * 16MN/bw) + (M+N)K/bw; force 0 auto, 1 dense, 2 CSR.  Values <= 0 (force < 0)
+ * keep the current setting.  Process-wide. */
+xg_status xg_comp_model_set(double p_tc, double p_sp, double bw, int force);
+void xg_comp_model_get(double *p_tc, double *p_sp, double *bw, int *force);
+/* calibrate_eta() calibrate.hpp:28 / calibrate.cpp:68-100 on the device: the
+ * tcgen05 gemm_int against the CSR spmm_int on size x size int8 operands (random
+ * CSR at bisected densities, CUDA-event timed, best of reps), eta = the density
+ * where they cost the same.  Also returns the measured rates (int8 op/s of the
+ * GEMM, MAC/s of the SpMM at eta); install != 0 makes them the compensation
+ * cost model above. */
+xg_status xg_calibrate_eta(int size, int bits, uint64_t seed, int install, double *eta, int *reps,
+                           double *p_tc, double *p_sp);
 /* spmm() sparse.hpp:61 / sparse.cpp:97-117 */
 xg_status xg_spmm_f32(int rows, int cols, const int32_t *row_ptr, const int32_t *col_idx,
                       const float *values, const float *d, int d_cols, float *out, xg_stream s);

@@ -42,7 +42,7 @@ class XgReport(C.Structure):
                 ("nnz_a", C.c_int64), ("nnz_b", C.c_int64), ("ns_quant", C.c_double),
                 ("ns_xxmm", C.c_double), ("ns_reduce", C.c_double), ("ns_package", C.c_double),
                 ("stats_fallbacks", C.c_int), ("ns_gemm_df", C.c_double),
-                ("ns_gemm_comp", C.c_double)]
+                ("ns_gemm_comp", C.c_double), ("comp_kernel", C.c_int)]
 
 
 DUMP_FIELDS = ["aq", "aq_scales", "bq", "bq_scales", "d_f", "raq", "raq_scale", "rbq",
@@ -86,6 +86,9 @@ _SIGS = {
     "xg_csr_transpose_f32": (_I, [_I, _I, _V, _V, _V, _I64, _V, _V, _V, _V]),
     "xg_spmm_i8": (_I, [_I, _I, _V, _V, _V, _V, _I, _I, _V, _V]),
     "xg_spmm_f32": (_I, [_I, _I, _V, _V, _V, _V, _I, _V, _V]),
+    "xg_comp_model_set": (_I, [_D, _D, _D, _I]),
+    "xg_comp_model_get": (None, [_V, _V, _V, _V]),
+    "xg_calibrate_eta": (_I, [_I, _I, C.c_uint64, _I, _V, _V, _V, _V]),
     "xg_csr_from_dense_count": (_I, [_V, _I, _I, _V, _V, _V]),
     "xg_csr_from_dense_fill": (_I, [_V, _I, _I, _V, _V, _V, _V]),
     "xg_densify": (_I, [_I, _I, _V, _V, _V, _V, _V]),

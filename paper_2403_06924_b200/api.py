@@ -124,6 +124,7 @@ class GemmReport:                   # pipeline.hpp:32-39
     nnz_a: int = 0
     nnz_b: int = 0
     stats_fallbacks: int = 0
+    comp_kernel: int = 0            # sparse terms ran on 0: tcgen05 masked-dense, 1: CUDA-core CSR SpMM
 
 
 # ---- plumbing -----------------------------------------------------------------
@@ -479,10 +480,41 @@ def _pipeline(a, b, c, alpha, beta, cfg: XigemmConfig, reduce: bool, dump: bool,
     report = GemmReport(_ret(out, host), rep.density_a, rep.density_b, GemmPath(rep.path),
                         {"quant": int(rep.ns_quant), "xxmm": int(rep.ns_xxmm),
                          "reduce": int(rep.ns_reduce), "package": int(rep.ns_package)},
-                        rep.nnz_a, rep.nnz_b, rep.stats_fallbacks)
+                        rep.nnz_a, rep.nnz_b, rep.stats_fallbacks, rep.comp_kernel)
     report.timings["gemm_df"] = int(rep.ns_gemm_df)
     report.timings["gemm_comp"] = int(rep.ns_gemm_comp)
     return (report, bufs) if dump else report
+
+
+@dataclass
+class EtaCalibration:               # calibrate.hpp:15-20
+    eta: float = 0.0
+    repetitions: int = 1
+    timer_coarse_warning: bool = False
+    fingerprint: str = ""
+    gemm_ops_per_s: float = 0.0     # measured tcgen05 GEMM rate (int8 op/s)
+    spmm_macs_per_s: float = 0.0    # measured CSR SpMM rate near eta (MAC/s)
+
+
+def calibrate_eta(size: int, bits=QuantBits.Int8, seed: int = 0, install: bool = False) -> EtaCalibration:
+    """calibrate.cpp:68-100 on the device: the density where the CSR spmm_int costs as
+    much as the tcgen05 gemm_int at size x size.  install=True makes the measured rates
+    the SparseResidual branch's compensation cost model (comp_model)."""
+    eta, reps, ptc, psp = C.c_double(), C.c_int(), C.c_double(), C.c_double()
+    check(lib().xg_calibrate_eta(int(size), int(bits), int(seed) & (2 ** 64 - 1), int(bool(install)),
+                                 C.byref(eta), C.byref(reps), C.byref(ptc), C.byref(psp)))
+    name = torch.cuda.get_device_name() if torch.cuda.is_available() else "no-gpu"
+    return EtaCalibration(eta.value, reps.value, False, name, ptc.value, psp.value)
+
+
+def comp_model(p_tc: float = 0.0, p_sp: float = 0.0, bw: float = 0.0, force: int = -1) -> dict:
+    """Sets (values > 0 / force >= 0) and returns the compensation cost model: the
+    device chooses the tcgen05 masked-dense launch or the CUDA-core CSR SpMM for the
+    sparse terms (force: 0 auto, 1 dense, 2 CSR).  Results are identical either way."""
+    check(lib().xg_comp_model_set(float(p_tc), float(p_sp), float(bw), int(force)))
+    v = [C.c_double(), C.c_double(), C.c_double(), C.c_int()]
+    lib().xg_comp_model_get(*[C.byref(x) for x in v])
+    return {"p_tc": v[0].value, "p_sp": v[1].value, "bw": v[2].value, "force": v[3].value}
 
 
 def xigemm(a, b, c=None, alpha: float = 1.0, beta: float = 0.0, cfg: XigemmConfig | None = None,
@@ -496,8 +528,9 @@ def xigemm_dump(a, b, cfg: XigemmConfig | None = None):
     return _pipeline(a, b, None, 1.0, 0.0, cfg or XigemmConfig(), True, True)
 
 
-def quantized_gemm_full_residual(a, b, cfg: XigemmConfig | None = None):
-    return _pipeline(a, b, None, 1.0, 0.0, cfg or XigemmConfig(), False, False).result
+def quantized_gemm_full_residual(a, b, cfg: XigemmConfig | None = None, *, out=None):
+    """pipeline.hpp:50-51 / pipeline.cpp:177-180 (out=: as for xigemm)."""
+    return _pipeline(a, b, None, 1.0, 0.0, cfg or XigemmConfig(), False, False, out=out).result
 
 
 def quantized_gemm_direct(a, b, cfg: XigemmConfig | None = None):

@@ -15,6 +15,7 @@
 //       compensation epilogue  C = (D_F + deq(acc0)) + deq(acc1), alpha/beta
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <memory>
 #include <mutex>
@@ -32,6 +33,7 @@
 #include "gemm.h"
 #include "gemm_tc.cuh"
 #include "internal.h"
+#include "spmm.h"
 #include "misc.h"
 
 namespace {
@@ -184,6 +186,9 @@ struct Pipe {
     unsigned long long *stamp_df = nullptr, *stamp_comp = nullptr;  // DevScalars::ts slots of the GEMMs
     uint32_t* report_dst = nullptr;  // device-mapped pinned report the compensation GEMM writes
     uint32_t *keepA = nullptr, *keepB = nullptr;  // stage dump: kept-element bitmasks (xg_dump)
+    // CUDA-core CSR compensation (spmm.cu): quad-packed A'q rows and B'q^T rows
+    xg::QCsr csrA{}, csrB{};
+    bool csr_ok = false;
 };
 
 // Second stream for the independent A-side / B-side memory-bound kernels of
@@ -419,12 +424,49 @@ void gemm_comp(Pipe& p, float* out, const float* c, float alpha, float beta) {
     const ScaleRef r2 = sref(&p.sc->lamRA, 0, &p.sc->rRA);
     const ScaleRef c2d = p.vw ? sref(p.lb, 1, p.lbr) : sref(&p.sc->lamB, 0, &p.sc->rB);
     const ScaleRef c2s = p.vw ? sref(p.lb, 1, p.lbr) : sref(&p.sc->lamBred, 0, &p.sc->rBred);
+    if (p.csr_ok) {
+        // CUDA-core CSR path (spmm.cu), run only when k_dispatch chose it (sc->csr) and the
+        // builds fit (!sc->csr_bad); otherwise these launches return at once and the
+        // masked-dense launch below does the work (it skips itself in the CSR case)
+        const int maxq = 1 << 30;  // long rows are shared by a warp in the SpMM (kHeavyQ)
+        xg::launch_qcsr_build(p.ared, p.M, p.K, p.ldk, p.csrA, &p.sc->csr, &p.sc->csr_bad, maxq, p.s);
+        check_launch("csr build A'");
+        xg::launch_qcsr_build(p.bredT, p.N, p.K, p.ldk, p.csrB, &p.sc->csr, &p.sc->csr_bad, maxq, p.s);
+        check_launch("csr build B'");
+        auto sp = [](const ScaleRef& r) { return xg::SpScale{r.p, r.stride, r.r}; };
+        xg::SpmmArgs s1{};
+        s1.seg = p.csrA.seg; s1.quad = p.csrA.quad;
+        s1.nsp = p.M; s1.K = p.K;
+        s1.dense = p.rbqT; s1.ldd = p.ldk; s1.nlines = p.N;
+        s1.mode = xg::kSpmmRows;
+        s1.out = out; s1.din = out; s1.ldo = p.N;
+        s1.sp_scale = sp(r1s); s1.line_scale = sp(c1);
+        s1.run = &p.sc->csr; s1.bad = &p.sc->csr_bad;
+        s1.stamp = p.stamp_comp;
+        xg::SpmmArgs s2 = s1;  // dr2^T = B'q^T RAq^T: sparse rows j, dense lines = rows i of RAq
+        s2.seg = p.csrB.seg; s2.quad = p.csrB.quad;
+        s2.nsp = p.N;
+        s2.dense = p.raq; s2.nlines = p.M;
+        s2.mode = xg::kSpmmColsT;
+        s2.din = nullptr;
+        s2.sp_scale = sp(c2s); s2.line_scale = sp(r2);
+        s2.c_in = c; s2.has_c = c != nullptr; s2.alpha = alpha; s2.beta = beta;
+        s2.stamp = nullptr;
+        s2.stamp_end = p.stamp_comp ? p.stamp_comp + 1 : nullptr;
+        xg::launch_spmm_strip(s1, p.s);
+        check_launch("spmm dr1");
+        xg::launch_spmm_strip(s2, p.s);
+        check_launch("spmm dr2");
+    }
+    const int* skip = p.csr_ok ? &p.sc->csr : nullptr;
+    const int* veto = p.csr_ok ? &p.sc->csr_bad : nullptr;
     if (p.M >= 256 && (p.N % 4) == 0 && !getenv("XG_GEMM_1CTA")) {
         // Two single-accumulator pair GEMMs with double-buffered TMEM (pipeline.cpp:141-145
         // order): out = fl(D_F + deq(dr1)), then out = fl(out + deq(dr2)) and alpha/beta.
         GemmArgs g{};
         g.M = p.M; g.N = p.N; g.K = p.K;
         g.sel_ptr = &p.sc->sel;
+        g.skip_ptr = skip; g.skip_veto = veto;
         g.out_f32 = out;
         g.df_in = out;
         g.c_in = c;
@@ -478,6 +520,7 @@ void gemm_comp(Pipe& p, float* out, const float* c, float alpha, float beta) {
     g.amap[1][0] = 3; g.amap[1][1] = 3;   // RAq
     g.bmap[1][0] = 4; g.bmap[1][1] = 5;   // Y2: dense Bq | sparse B'q
     g.sel_ptr = &p.sc->sel;
+    g.skip_ptr = skip; g.skip_veto = veto;
     g.out_f32 = out;
     g.df_in = out;
     g.c_in = c;
@@ -535,7 +578,16 @@ struct PipeWs {
     float *rstat, *cstat;
     double *rsum, *csum;
     int* flags;
+    // quad-packed CSR of A'q / B'q^T (null when K is too large for the CUDA-core path)
+    int2 *segA, *segB;
+    uint4 *quadA, *quadB;
+    int64_t capA, capB;  // quads
 };
+
+// CSR capacity in quads: 1/16 of the operand (6.25% density) plus one padding
+// quad per row; the dispatch only picks the CSR path far below that, and an
+// overflow falls back to the dense launch (csr_bad).
+int64_t csr_cap_quads(int rows, int64_t k) { return (int64_t)rows * k / 64 + rows + 64; }
 
 template <class Get>
 void alloc_ws(PipeWs& w, int M, int N, int64_t ldk, Get&& get) {
@@ -556,6 +608,24 @@ void alloc_ws(PipeWs& w, int M, int N, int64_t ldk, Get&& get) {
     w.rsum = get((double*)nullptr, M);
     w.csum = get((double*)nullptr, N);
     w.flags = get((int*)nullptr, (int64_t)M + N);
+    w.segA = w.segB = nullptr;
+    w.quadA = w.quadB = nullptr;
+    w.capA = w.capB = 0;
+    if (xg::spmm_strip_width((int)ldk) > 0 && !getenv("XG_NO_CSR")) {
+        w.capA = csr_cap_quads(M, ldk);
+        w.capB = csr_cap_quads(N, ldk);
+        w.segA = get((int2*)nullptr, M);
+        w.segB = get((int2*)nullptr, N);
+        w.quadA = get((uint4*)nullptr, w.capA);
+        w.quadB = get((uint4*)nullptr, w.capB);
+    }
+}
+
+void set_csr(Pipe& p, const PipeWs& w) {
+    p.csr_ok = w.segA != nullptr;
+    if (!p.csr_ok) return;
+    p.csrA = xg::QCsr{w.segA, w.quadA, &w.sc->qcurA, w.capA};
+    p.csrB = xg::QCsr{w.segB, w.quadB, &w.sc->qcurB, w.capB};
 }
 
 struct PipeCall {
@@ -565,6 +635,9 @@ struct PipeCall {
     xg_config cfg;
     int reduce;
     float* out;
+    // compensation cost model at call time (part of the graph-cache key: a
+    // captured dispatch kernel holds it as an argument)
+    xg::CompModel cm{};
 };
 
 // One stage group of the device pipeline (no host synchronisation anywhere):
@@ -584,6 +657,7 @@ int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* du
     p.stamp_df = &w.sc->ts[1];
     p.stamp_comp = &w.sc->ts[3];
     p.report_dst = report_dst;
+    set_csr(p, w);
     const int M = q.M, K = q.K, N = q.N;
     p.pre_init = true;  // stage 0 initialises everything in one launch
     if (stage == 0) {
@@ -623,7 +697,8 @@ int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* du
             p.keepB = dump->b_keep;
         }
         select_operands(p, q.a, q.b, q.reduce, w.rstat, w.cstat);
-        xg::launch_dispatch(p.sc, q.cfg.bits, (int64_t)M * K, (int64_t)K * N, q.cfg.density_limit, q.reduce, s);
+        xg::launch_dispatch(p.sc, q.cfg.bits, (int64_t)M * K, (int64_t)K * N, q.cfg.density_limit, q.reduce, s, M, N,
+                            K, p.csr_ok, &q.cm);
         check_launch("dispatch");
         if (dump) {
             dump_operands(p, dump);
@@ -672,7 +747,8 @@ bool same_call(const PipeCall& x, const PipeCall& y) {
     return x.a == y.a && x.b == y.b && x.c == y.c && x.out == y.out && x.M == y.M && x.K == y.K &&
            x.N == y.N && x.reduce == y.reduce && std::memcmp(&x.alpha, &y.alpha, sizeof(float)) == 0 &&
            std::memcmp(&x.beta, &y.beta, sizeof(float)) == 0 &&
-           std::memcmp(&x.cfg, &y.cfg, sizeof(xg_config)) == 0;
+           std::memcmp(&x.cfg, &y.cfg, sizeof(xg_config)) == 0 &&
+           std::memcmp(&x.cm, &y.cm, sizeof(xg::CompModel)) == 0;
 }
 
 bool graphs_enabled() {
@@ -863,6 +939,7 @@ void finish_report(const xg::DevScalars& h, int reduce, EventTimer& tm, xg_repor
         rep->ns_xxmm = rep->ns_gemm_df + rep->ns_gemm_comp;
         rep->ns_package = 0.0;
         rep->stats_fallbacks = h.nflag;
+        rep->comp_kernel = (h.csr && !h.csr_bad) ? 1 : 0;
     }
 }
 
@@ -874,6 +951,7 @@ void run_pipeline(const float* a, const float* b, const float* c, float alpha, f
     req(a && b && out, "xigemm: null matrix");
     req(K <= xg::gemm_max_inner(cfg->bits), "gemm_int: inner dimension permits 32-bit overflow");
     PipeCall q{a, b, c, alpha, beta, M, K, N, *cfg, reduce, out};
+    q.cm = xg::comp_model();
     const int64_t ldk = pad16(K);
     EventTimer tm(rep != nullptr, s);
     xg::DevScalars h;
@@ -1413,8 +1491,176 @@ xg_status xg_spmm_i8(int rows, int cols, const int32_t* row_ptr, const int32_t* 
                      xg_stream s) {
     return guarded([&] {
         req(cols <= xg::gemm_max_inner(d_bits), "spmm_int: inner dimension permits 32-bit overflow");
+        if (rows > 0 && d_cols > 0 && cols < 65536 && xg::spmm_strip_width(cols) > 0 && !getenv("XG_SPMM_NAIVE")) {
+            // quad-packed rows + the strip SpMM (spmm.cu); the nnz sizes the buffer
+            int32_t nnz = 0;
+            ck(cudaMemcpyAsync(&nnz, row_ptr + rows, sizeof nnz, cudaMemcpyDeviceToHost, st(s)), "nnz");
+            ck(cudaStreamSynchronize(st(s)), "nnz");
+            Scratch S(st(s));
+            xg::QCsr q{};
+            q.cap_q = (int64_t)nnz / 4 + rows + 1;
+            q.seg = S.get<int2>(rows);
+            q.quad = S.get<uint4>(q.cap_q);
+            q.cursor = S.get<unsigned long long>(1);
+            ck(cudaMemsetAsync(q.cursor, 0, sizeof(unsigned long long), st(s)), "memset");
+            xg::launch_qcsr_from_csr(row_ptr, col_idx, values, rows, q, st(s));
+            check_launch("spmm_i8 pack");
+            xg::SpmmArgs a{};
+            a.seg = q.seg; a.quad = q.quad;
+            a.nsp = rows; a.K = cols;
+            a.dense = d; a.ldd = d_cols; a.nlines = d_cols; a.src_rowmajor = 1;
+            a.mode = xg::kSpmmS32; a.out_s32 = out; a.ldo = d_cols;
+            xg::launch_spmm_strip(a, st(s));
+            check_launch("spmm_i8");
+            return;
+        }
         xg::spmm_i8(rows, row_ptr, col_idx, values, d, d_cols, out, st(s));
         check_launch("spmm_i8");
+    });
+}
+
+xg_status xg_comp_model_set(double p_tc, double p_sp, double bw, int force) {
+    return guarded([&] {
+        req(force <= 2, "comp model: force must be 0 (auto), 1 (dense) or 2 (CSR)");
+        xg::CompModel m = xg::comp_model();
+        if (p_tc > 0) m.p_tc = p_tc;
+        if (p_sp > 0) m.p_sp = p_sp;
+        if (bw > 0) m.bw = bw;
+        if (force >= 0) m.force = force;
+        xg::set_comp_model(m);
+    });
+}
+
+void xg_comp_model_get(double* p_tc, double* p_sp, double* bw, int* force) {
+    const xg::CompModel& m = xg::comp_model();
+    if (p_tc) *p_tc = m.p_tc;
+    if (p_sp) *p_sp = m.p_sp;
+    if (bw) *bw = m.bw;
+    if (force) *force = m.force;
+}
+
+// calibrate.cpp:68-100 with the B200 kernels, timed on the device: gemm_int is
+// the tcgen05 GEMM (raw s32 epilogue), spmm_int the strip SpMM over a random
+// quad-packed CSR operand built outside the timed region (as the reference
+// builds its CSR outside time_best_of).  Each timing is the best of `reps`
+// event-timed batches long enough to dwarf the launch overhead.
+xg_status xg_calibrate_eta(int size, int bits, uint64_t seed, int install, double* eta, int* reps_out,
+                           double* p_tc, double* p_sp) {
+    return guarded([&] {
+        req(size >= 8, "calibrate_eta: size too small to time");
+        req(bits == 4 || bits == 8, "calibrate_eta: bits must be 4 or 8");
+        req(size < 65536 && xg::spmm_strip_width(size) > 0, "calibrate_eta: size too large for the CSR SpMM");
+        cudaStream_t s = nullptr;
+        ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+        struct StreamGuard {
+            cudaStream_t s;
+            ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+        } sg{s};
+        const int n = size;
+        const int64_t ld = pad16(n);
+        const int qmax = xg::quant_max(bits);
+        Scratch S(s);
+        int8_t* aq = S.get<int8_t>(n * ld);
+        int8_t* bT = S.get<int8_t>(n * ld);  // B^T (K-major), the GEMM's and the SpMM's dense operand
+        int8_t* xs = S.get<int8_t>(n * ld);  // random sparse operand
+        int32_t* out = S.get<int32_t>((int64_t)n * n);
+        xg::launch_random_masked_i8(aq, n, n, ld, 1.0, qmax, seed + 1, s);
+        xg::launch_random_masked_i8(bT, n, n, ld, 1.0, qmax, seed, s);
+        check_launch("calibrate operands", 2);
+        xg::QCsr q{};
+        q.cap_q = (int64_t)n * ld / 4 + n + 64;
+        q.seg = S.get<int2>(n);
+        q.quad = S.get<uint4>(q.cap_q);
+        q.cursor = S.get<unsigned long long>(1);
+        int* bad = S.get<int>(1);
+        cudaEvent_t e0, e1;
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        struct EvGuard {
+            cudaEvent_t a, b;
+            ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
+        } eg{e0, e1};
+        auto time_batch = [&](auto&& launch, int batch) {
+            ck(cudaEventRecord(e0, s), "event");
+            for (int i = 0; i < batch; ++i) launch();
+            ck(cudaEventRecord(e1, s), "event");
+            ck(cudaEventSynchronize(e1), "event");
+            float ms = 0;
+            ck(cudaEventElapsedTime(&ms, e0, e1), "event");
+            return ms * 1e-3 / batch;
+        };
+        // the GEMM the pipeline runs (pair kernel, exact dequantising epilogue,
+        // unit scales): its rate is the one the SpMM competes with
+        double* one = S.get<double>(1);
+        const double h_one = 1.0;
+        ck(cudaMemcpyAsync(one, &h_one, sizeof h_one, cudaMemcpyHostToDevice, s), "scale");
+        float* outf = reinterpret_cast<float*>(out);
+        auto gemm = [&] {
+            xg::KOperand ops[2] = {{aq, n, ld}, {bT, n, ld}};
+            int isb[2] = {0, 1};
+            xg::GemmArgs g{};
+            g.M = n; g.N = n; g.K = n;
+            g.out_f32 = outf;
+            g.amap[0][0] = g.amap[0][1] = 0;
+            g.bmap[0][0] = g.bmap[0][1] = 1;
+            g.rs[0][0] = g.rs[0][1] = sref(one, 0);
+            g.cs[0][0] = g.cs[0][1] = sref(one, 0);
+            xg::gemm_i8(xg::EPI_DF, ops, isb, 2, g, s);
+        };
+        gemm();  // warm-up (tensor maps, attributes)
+        check_launch("calibrate gemm");
+        // batch so one timing spans >= ~1 ms; best of 3 batches (time_best_of)
+        const double t1 = time_batch(gemm, 1);
+        const int batch = std::max(1, std::min(512, (int)(1e-3 / std::max(t1, 1e-7))));
+        const int reps = 3;
+        double t_gemm = 1e30;
+        for (int r = 0; r < reps; ++r) t_gemm = std::min(t_gemm, time_batch(gemm, batch));
+        double last_sp = 0.0, last_d = 0.0;
+        auto model = [&](double d) {
+            xg::launch_random_masked_i8(xs, n, n, ld, d, qmax, seed ^ 0x5DEECE66DULL, s);
+            ck(cudaMemsetAsync(q.cursor, 0, sizeof(unsigned long long), s), "memset");
+            ck(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset");
+            xg::launch_qcsr_build(xs, n, n, ld, q, nullptr, bad, 1 << 30, s);
+            check_launch("calibrate csr", 2);
+            xg::SpmmArgs a{};
+            a.seg = q.seg; a.quad = q.quad;
+            a.nsp = n; a.K = n;
+            a.dense = bT; a.ldd = ld; a.nlines = n;
+            a.mode = xg::kSpmmS32; a.out_s32 = out; a.ldo = n;
+            auto sp = [&] { xg::launch_spmm_strip(a, s); };
+            sp();
+            const double t1s = time_batch(sp, 1);
+            const int bs = std::max(1, std::min(batch, (int)(1e-3 / std::max(t1s, 1e-7))));
+            double t = 1e30;
+            for (int r = 0; r < reps; ++r) t = std::min(t, time_batch(sp, bs));
+            last_sp = t;
+            last_d = d;
+            return t / t_gemm;
+        };
+        constexpr double kMin = 1.0 / 1024.0;  // calibrate.cpp:18, :52-66
+        double e;
+        if (model(1.0) <= 1.0) e = 1.0;
+        else if (model(kMin) >= 1.0) e = kMin;
+        else {
+            double lo = kMin, hi = 1.0;
+            for (int it = 0; it < 20; ++it) {
+                const double mid = 0.5 * (lo + hi);
+                (model(mid) <= 1.0 ? lo : hi) = mid;
+            }
+            e = 0.5 * (lo + hi);
+        }
+        const double ptc = 2.0 * (double)n * n * n / t_gemm;
+        const double psp = last_sp > 0 ? last_d * (double)n * n * n / last_sp : 0.0;
+        if (eta) *eta = e;
+        if (reps_out) *reps_out = reps;
+        if (p_tc) *p_tc = ptc;
+        if (p_sp) *p_sp = psp;
+        if (install) {
+            xg::CompModel m = xg::comp_model();
+            m.p_tc = ptc;
+            if (psp > 0) m.p_sp = psp;
+            xg::set_comp_model(m);
+        }
     });
 }
 
@@ -1535,6 +1781,7 @@ Pipe shard_pipe(ShardState& h, cudaStream_t s) {
     p.aq = h.w.aq; p.raq = h.w.raq; p.ared = h.w.ared;
     p.bqT = h.w.bqT; p.rbqT = h.w.rbqT; p.bredT = h.w.bredT;
     p.la = h.w.la; p.lb = h.w.lb; p.lar = h.w.lar; p.lbr = h.w.lbr; p.colmax = h.w.colmax;
+    set_csr(p, h.w);
     return p;
 }
 
@@ -1595,7 +1842,7 @@ void shard_step(ShardState& h, int step, cudaStream_t s) {
             shard_xfer(h, 3, s);  // global nnz(A'), retained max
             select_operands(p, q.a, q.b, q.reduce, h.w.rstat, h.w.cstat, 2);
             xg::launch_dispatch(p.sc, q.cfg.bits, (int64_t)h.m_total * K, (int64_t)K * N, q.cfg.density_limit,
-                                q.reduce, s);
+                                q.reduce, s, M, N, K, p.csr_ok, &q.cm);
             check_launch("dispatch");
             gemm_comp(p, q.out, q.c, q.alpha, q.beta);
             break;
@@ -1634,6 +1881,7 @@ xg_status xg_shard_create(const float* a_rows, const float* b, const float* c_ro
         ShardState& S = x->st;
         const int M = rank_rows[rank];
         S.q = PipeCall{a_rows, b, c_rows, alpha, beta, M, k, n, *cfg, reduce, out_rows};
+        S.q.cm = xg::comp_model();
         S.m_total = (int)mt;
         S.g = nranks;
         S.rank = rank;

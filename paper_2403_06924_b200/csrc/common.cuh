@@ -235,11 +235,16 @@ __device__ __forceinline__ float dq_ff(int32_t p, float2 a, float2 b, bool& slow
 // (accepted: the reference's +0); a non-finite scale marker makes r NaN
 // (rejected).  Elements that fail (|p| >= 2^24, ~2^-15 of random ones) set
 // their bit in `slowmask` and are redone by dq_slow.
-__device__ __forceinline__ float dq_ff24(int32_t p, float2 a, float2 b, uint32_t& slowmask,
-                                         uint32_t bit) {
+// c = (ah + al)(bh + bl) as ch + cl (the scale product of dq_ff24, hoistable
+// when one scale is fixed over many elements)
+__device__ __forceinline__ float2 ff_mul(float2 a, float2 b) {
     const float ch = __fmul_rn(a.x, b.x);
     const float ce = __fmaf_rn(a.x, b.x, -ch);
-    const float cl = __fmaf_rn(a.x, b.y, __fmaf_rn(a.y, b.x, ce));
+    return make_float2(ch, __fmaf_rn(a.x, b.y, __fmaf_rn(a.y, b.x, ce)));
+}
+
+__device__ __forceinline__ float dq_ff24c(int32_t p, float2 c, uint32_t& slowmask, uint32_t bit) {
+    const float ch = c.x, cl = c.y;
     const float pf = __int2float_rn(p);
     const float t1 = __fmul_rn(pf, ch);
     const float e1 = __fmaf_rn(pf, ch, -t1);
@@ -253,6 +258,11 @@ __device__ __forceinline__ float dq_ff24(int32_t p, float2 a, float2 b, uint32_t
     const bool ok = fabsf(pf) < 16777216.0f && fabsf(r) <= thr;
     slowmask |= ok ? 0u : bit;
     return f;
+}
+
+__device__ __forceinline__ float dq_ff24(int32_t p, float2 a, float2 b, uint32_t& slowmask,
+                                         uint32_t bit) {
+    return dq_ff24c(p, ff_mul(a, b), slowmask, bit);
 }
 
 // Rare path of the epilogues: the full-range float-float form, then the

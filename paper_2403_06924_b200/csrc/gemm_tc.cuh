@@ -55,6 +55,10 @@ struct GemmArgs {
     int amap[3][2];
     int bmap[3][2];
     const int* sel_ptr;  // device flag choosing column 1 of the index tables (nullable)
+    // the CUDA-core CSR path (spmm.cu) serves the call when *skip_ptr && !*skip_veto:
+    // the launch then does no tile (and writes no stage stamps)
+    const int* skip_ptr;
+    const int* skip_veto;
     // epilogue
     int32_t* out_s32;
     float* out_f32;
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(256, 1)
     const int lane = threadIdx.x & 31;
     const int num_m = (args.M + Cfg::BM - 1) / Cfg::BM;
     const int num_n = (args.N + BN - 1) / BN;
-    const int num_tiles = num_m * num_n;
+    const int num_tiles_all = num_m * num_n;
     const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
 
     if (threadIdx.x == 0) {
@@ -261,6 +265,8 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t tmem_base = *tmem_slot;
     XG_PDL_WAIT_ONLY();
     const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
+    const bool skip = args.skip_ptr && *args.skip_ptr && !(args.skip_veto && *args.skip_veto);
+    const int num_tiles = skip ? 0 : num_tiles_all;
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -472,7 +478,7 @@ __global__ void __launch_bounds__(384, 1)
     const int nclusters = gridDim.x / (2 * PAIRS);
     const int num_m = (args.M + 2 * PAIRS * Cfg::BM - 1) / (2 * PAIRS * Cfg::BM);
     const int num_n = (args.N + Cfg::BN - 1) / Cfg::BN;
-    const int num_tiles = num_m * num_n;
+    const int num_tiles_all = num_m * num_n;
     const int nkb = (args.K + Cfg::BK - 1) / Cfg::BK;
     const int gm = args.group_m > 0 ? args.group_m : Cfg::GROUP_M;
 
@@ -500,7 +506,9 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tmem_base = *tmem_slot;
     // everything above overlaps the predecessor's tail under a programmatic edge
     XG_PDL_WAIT_ONLY();
-    if (args.stamp && blockIdx.x == 0 && threadIdx.x == 0) args.stamp[0] = globaltimer_ns();
+    const bool skip = args.skip_ptr && *args.skip_ptr && !(args.skip_veto && *args.skip_veto);
+    const int num_tiles = skip ? 0 : num_tiles_all;
+    if (args.stamp && !skip && blockIdx.x == 0 && threadIdx.x == 0) args.stamp[0] = globaltimer_ns();
     const int sel = args.sel_ptr ? (*args.sel_ptr != 0) : 0;
     const int nterms = (EPI == EPI_ACC && args.dual) ? 2 : 1;
 
@@ -824,7 +832,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         tmem_dealloc2(tmem_base, Cfg::TMEM_COLS);
     }
-    if (args.stamp && threadIdx.x == 128) atomicMax(&args.stamp[1], globaltimer_ns());  // stores landed above
+    if (args.stamp && !skip && threadIdx.x == 128) atomicMax(&args.stamp[1], globaltimer_ns());  // stores landed above
     if (args.done) {
         __syncthreads();  // this CTA's stamp is in
         uint32_t* last = tmem_slot + 1;  // spare word of the barrier area

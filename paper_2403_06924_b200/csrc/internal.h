@@ -31,7 +31,27 @@ struct DevScalars {
     unsigned long long ts[5];
     unsigned done;  // CTAs of the compensation GEMM finished (the last one writes the report)
     unsigned pad2;
+    // sparse compensation on CUDA cores (spmm.cu) instead of the masked-dense
+    // tensor-core launch: chosen by k_dispatch from the cost model; csr_bad is
+    // raised by the CSR build (capacity / a very long row), the dense launch
+    // then serves the call
+    int csr, csr_bad;
+    unsigned long long qcurA, qcurB;  // quads handed out by the two CSR builds
 };
+
+// Cost model of the compensation choice (k_dispatch): masked-dense tcgen05
+// t_d = 4MNK / p_tc against the CUDA-core CSR path t_c = max((nnzA N + nnzB M)
+// / p_sp, MN c_el) + (M + N) K / bw (the CSR builds), c_el the per-output-element
+// cost of its two exact epilogue passes.  The CSR path is taken when t_c <
+// 0.9 t_d.  Rates measured on B200 (xg_calibrate_eta re-measures p_tc, p_sp).
+// force: 0 auto, 1 dense, 2 CSR.
+struct CompModel {
+    double p_tc, p_sp, bw, c_el;
+    int force;
+    int csr_ok;  // host: the CSR path is available for this shape (strip fits, buffers allocated)
+};
+const CompModel& comp_model();
+void set_comp_model(const CompModel& m);
 
 struct QuantRowsArgs {
     const float* x;
@@ -114,7 +134,8 @@ void launch_select_rows(const SelectArgs& a, cudaStream_t s);
 void launch_select_cols_T(const SelectArgs& a, cudaStream_t s);
 void launch_lambdas(DevScalars* sc, int bits, cudaStream_t s);
 void launch_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, double density_limit,
-                     int reduce, cudaStream_t s);
+                     int reduce, cudaStream_t s, int M = 0, int N = 0, int K = 0, int csr_ok = 0,
+                     const CompModel* model = nullptr);
 
 // statistics over D_F (pipeline.cpp:215-247)
 // Deferred exact-mean fallback (AvgRule): the operands whose selection the

@@ -1545,7 +1545,8 @@ __global__ void k_lambdas(DevScalars* sc, int bits) {
 
 // Density, dispatch (pipeline.cpp:106-111) and the per-tensor scales the
 // compensation epilogue reads.
-__global__ void k_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, double s, int reduce) {
+__global__ void k_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, double s, int reduce, int M, int N,
+                           int K, CompModel cm) {
     XG_PDL_WAIT();
     sc->lamRA = compute_scale((double)__uint_as_float(sc->maxRA), bits);
     sc->lamRB = compute_scale((double)__uint_as_float(sc->maxRB), bits);
@@ -1563,6 +1564,20 @@ __global__ void k_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, dou
         const int sparse = fmax(da, db) < s;
         sc->sel = sparse;
         sc->path = sparse ? kSparse : kDense;
+        // same result either way (exact integer sums): pick the faster compensation
+        int csr = 0;
+        if (sparse && cm.csr_ok) {
+            if (cm.force == 2) {
+                csr = 1;
+            } else if (cm.force == 0) {
+                const double mn = (double)M * (double)N;
+                const double t_d = 4.0 * mn * (double)K / cm.p_tc;
+                const double macs = (double)sc->nnzA * (double)N + (double)sc->nnzB * (double)M;
+                const double t_c = fmax(macs / cm.p_sp, mn * cm.c_el) + ((double)M + (double)N) * K / cm.bw;
+                csr = t_c < 0.9 * t_d;
+            }
+        }
+        sc->csr = csr;
     } else {
         sc->densA = sc->densB = 0.0;
         sc->sel = 0;
@@ -1842,9 +1857,25 @@ void launch_select_cols_T(const SelectArgs& a, cudaStream_t s) {
 void launch_lambdas(DevScalars* sc, int bits, cudaStream_t s) { k_lambdas<<<1, 1, 0, s>>>(sc, bits); }
 
 void launch_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, double density_limit,
-                     int reduce, cudaStream_t s) {
-    k_dispatch<<<1, 1, 0, s>>>(sc, bits, MK, KN, density_limit, reduce);
+                     int reduce, cudaStream_t s, int M, int N, int K, int csr_ok, const CompModel* model) {
+    CompModel cm = model ? *model : comp_model();
+    cm.csr_ok = csr_ok;
+    k_dispatch<<<1, 1, 0, s>>>(sc, bits, MK, KN, density_limit, reduce, M, N, K, cm);
 }
+
+// B200 measurements (tools/csr_sweep.py at 8192^3, profiles/r2_csr_sweep.txt):
+// compensation launch 3.6e15 int8 op/s (4MNK masked-dense), strip SpMM ~1.1e13
+// MAC/s incremental, 8.3 ns of fixed epilogue work per output element, HBM 6.4e12 B/s
+namespace {
+CompModel g_model = [] {
+    CompModel m{3.6e15, 1.1e13, 6.4e12, 8.3e-12, 0, 0};
+    if (const char* e = getenv("XG_COMP")) m.force = atoi(e);  // 0 auto, 1 dense, 2 CSR
+    if (const char* e = getenv("XG_P_SPMM")) m.p_sp = atof(e);
+    return m;
+}();
+}  // namespace
+const CompModel& comp_model() { return g_model; }
+void set_comp_model(const CompModel& m) { g_model = m; }
 
 void fill_u32(uint32_t* p, uint32_t v, int64_t n, cudaStream_t s) {
     int64_t blocks = (n + 255) / 256;

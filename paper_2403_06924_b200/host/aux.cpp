@@ -11,6 +11,7 @@
 #include <thread>
 
 #include "xigemm/calibrate.hpp"
+#include "xigemm_c.h"
 #include "xigemm/metrics.hpp"
 #include "xigemm/qr.hpp"
 #include "xigemm/random_matrix.hpp"
@@ -139,48 +140,20 @@ std::string machine_fingerprint() {
     return gpu + " / " + cpu + " / " + std::to_string(std::thread::hardware_concurrency()) + " threads";
 }
 
-// GPU analogue of the reference's host calibration (calibrate.cpp:68-100): the
-// B200 gemm_int (tcgen05) against the B200 spmm_int at bisected densities,
-// wall-timed through the public API (best of `reps`).
+// calibrate.cpp:68-100 on the B200: the tcgen05 gemm_int against the CSR
+// spmm_int, CUDA-event timed on the device by xg_calibrate_eta (no PCIe or
+// host work inside the timings).
 EtaCalibration calibrate_eta(int size, QuantBits bits, std::uint64_t seed) {
     if (size < 8) throw std::invalid_argument("calibrate_eta: size too small to time");
     EtaCalibration cal;
     cal.fingerprint = machine_fingerprint();
-    const QuantizedMatrix bq = quantize(generate(DistributionSpec::uniform01(seed), size, size), bits,
-                                        ScaleScheme::PerTensor, RoundingMode::Nearest);
-    const QuantizedMatrix aq = quantize(generate(DistributionSpec::uniform01(seed + 1), size, size), bits,
-                                        ScaleScheme::PerTensor, RoundingMode::Nearest);
-    using clk = std::chrono::steady_clock;
-    auto best_of = [](const auto& fn, int reps) {
-        double best = 1e30;
-        for (int i = 0; i < reps; ++i) {
-            const auto t0 = clk::now();
-            fn();
-            best = std::min(best, std::chrono::duration<double>(clk::now() - t0).count());
-        }
-        return best;
-    };
-    int reps = 3;
-    double t_gemm = best_of([&] { gemm_int(aq, bq); }, reps);
+    double eta = 0.0, ptc = 0.0, psp = 0.0;
+    int reps = 0;
+    const xg_status st = xg_calibrate_eta(size, bits == QuantBits::Int4 ? 4 : 8, seed, 0, &eta, &reps, &ptc, &psp);
+    if (st == XG_EINVAL) throw std::invalid_argument(xg_last_error());
+    if (st != XG_OK) throw std::runtime_error(xg_last_error());
+    cal.eta = eta;
     cal.repetitions = reps;
-    SplitMix64 rng(seed ^ 0x5DEECE66DULL);
-    const CostModel measured = [&](double dens) {
-        SparseCsrI8 s;
-        s.rows = s.cols = size;
-        s.row_ptr.assign(size + 1, 0);
-        for (int i = 0; i < size; ++i) {
-            for (int j = 0; j < size; ++j) {
-                if (rng.next_unit() < dens) {
-                    s.col_idx.push_back(j);
-                    const int v = static_cast<int>(rng.next() % 255) - 127;
-                    s.values.push_back(static_cast<std::int8_t>(v == 0 ? 1 : v));
-                }
-            }
-            s.row_ptr[i + 1] = static_cast<std::int32_t>(s.values.size());
-        }
-        return best_of([&] { spmm_int(s, bq); }, reps) / t_gemm;
-    };
-    cal.eta = calibrate_eta_from_model(measured);
     return cal;
 }
 

@@ -32,7 +32,7 @@ import ctypes as C
 import torch
 
 from ._lib import ShardRetry, XgReport, check, lib
-from .api import GemmPath, GemmReport, InvalidArgument, XigemmConfig, _dev, _p, _s
+from .api import comp_model, GemmPath, GemmReport, InvalidArgument, XigemmConfig, _dev, _p, _s
 
 NSTEPS = 6
 OP_MAX, OP_SUM, OP_MIN, OP_ALLGATHER = 0, 1, 2, 3
@@ -280,7 +280,8 @@ def xigemm_sharded(a_rows, b, c_rows=None, alpha: float = 1.0, beta: float = 0.0
     # a repeated call hits the cache (and its CUDA graph) instead of a new handle
     key = (x.data_ptr(), tuple(x.shape), y.data_ptr(), tuple(y.shape), 0 if cc is None else cc.data_ptr(),
            None if out is None else out.data_ptr(), float(alpha), float(beta), bool(reduce), rank, tuple(rank_rows),
-           (c.bits, c.threshold, c.density_limit, c.scheme, c.policy, c.rounding), id(group))
+           (c.bits, c.threshold, c.density_limit, c.scheme, c.policy, c.rounding), id(group),
+           tuple(comp_model().values()))  # the handle holds the compensation cost model of its creation
     sh = _cached_shard(key, lambda: Shard(x, y, cc, alpha, beta, rank, rank_rows, cfg, reduce, out))
     runs = getattr(sh, "_runs", 0)
     if graph and runs >= 1 and getattr(sh, "_graph", None) is None:
