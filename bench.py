@@ -528,7 +528,7 @@ def run_b200(args, world, rank, local):
     value = ops * world / (ms * 1e-3) / 1e12
 
     # ---- e2e through the host-buffer C-ABI call (pinned host buffers) ----
-    e2e_val = None
+    e2e_val = e2e_pageable = None
     if not args.no_e2e:
         ah = torch.empty((m, k), dtype=torch.float32, pin_memory=True)
         bh = torch.empty((k, n), dtype=torch.float32, pin_memory=True)
@@ -551,7 +551,23 @@ def run_b200(args, world, rank, local):
         e2e_val = ops * world / e2e_s / 1e12
         # host path result equals the device path result
         assert np.array_equal(on.view(np.uint32), out.cpu().numpy().view(np.uint32))
+        # the same call on pageable buffers (plain numpy, like the C++ drop-in's
+        # std::vector memory): xg_xigemm_host stages them through pinned slots
+        ap, bp, op = an.copy(), bn.copy(), np.empty_like(on)
         del ah, bh, oh
+        xg.xigemm_host(ap, bp, cfg=cfg, out=op)
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            xg.xigemm_host(ap, bp, cfg=cfg, out=op)
+        pg_s = (time.perf_counter() - t0) / e2e_steps
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([pg_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pg_s = float(t.item())
+        e2e_pageable = ops * world / pg_s / 1e12
+        assert np.array_equal(op.view(np.uint32), out.cpu().numpy().view(np.uint32))
+        del ap, bp, op
 
     if rank != 0:
         return
@@ -648,7 +664,11 @@ def run_b200(args, world, rank, local):
         "data": "synthetic Student-t(3) (device SplitMix64 generator), seeds A=1 B=2",
         "config": _config(args, thr, dens),
         "e2e": {"value": e2e_val, "unit": "TFLOP/s",
-                "h2d_bytes_per_step": 4 * (m * k + k * n), "d2h_bytes_per_step": 4 * m * n} if e2e_val else None,
+                "h2d_bytes_per_step": 4 * (m * k + k * n), "d2h_bytes_per_step": 4 * m * n,
+                "buffers": "pinned host memory (torch pin_memory), xg_xigemm_host",
+                "pageable": {"value": e2e_pageable, "unit": "TFLOP/s",
+                             "buffers": "pageable numpy arrays - the C++ drop-in's std::vector memory - staged "
+                                        "through pinned slots inside xg_xigemm_host"}} if e2e_val else None,
         "roofline": roof,
         "clocks": clk.summary(),
         "gpu_launches": launches,

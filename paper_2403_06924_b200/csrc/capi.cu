@@ -17,6 +17,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <thread>
 #include <memory>
 #include <mutex>
 #include <type_traits>
@@ -590,7 +592,7 @@ struct PipeWs {
 int64_t csr_cap_quads(int rows, int64_t k) { return (int64_t)rows * k / 64 + rows + 64; }
 
 template <class Get>
-void alloc_ws(PipeWs& w, int M, int N, int64_t ldk, Get&& get) {
+void alloc_ws(PipeWs& w, int M, int N, int64_t ldk, Get&& get, bool csr = true) {
     w.sc = get((xg::DevScalars*)nullptr, 1);
     w.aq = get((int8_t*)nullptr, M * ldk);
     w.raq = get((int8_t*)nullptr, M * ldk);
@@ -611,7 +613,7 @@ void alloc_ws(PipeWs& w, int M, int N, int64_t ldk, Get&& get) {
     w.segA = w.segB = nullptr;
     w.quadA = w.quadB = nullptr;
     w.capA = w.capB = 0;
-    if (xg::spmm_strip_width((int)ldk) > 0 && !getenv("XG_NO_CSR")) {
+    if (csr && xg::spmm_strip_width((int)ldk) > 0 && !getenv("XG_NO_CSR")) {
         w.capA = csr_cap_quads(M, ldk);
         w.capB = csr_cap_quads(N, ldk);
         w.segA = get((int2*)nullptr, M);
@@ -2029,6 +2031,144 @@ cudaStream_t host_stream() {
 //   D2H stream: each chunk of the result as soon as its compensation is done.
 // Only H2D(A, B) + the non-overlappable middle + D2H remain on the critical
 // path (the PCIe link is full-duplex, ~52 GB/s each way on this box).
+
+// ---- pageable host buffers ------------------------------------------------------
+// The C++ drop-in hands xg_xigemm_host std::vector memory (pageable).  A
+// cudaMemcpyAsync from pageable memory is staged by the driver before it
+// returns, so neither the copies nor the compute would overlap.  Pageable
+// inputs are instead fed by a host thread through pinned slots (a parallel
+// memcpy into a slot, then an async H2D out of it) while the caller's thread
+// enqueues each compute step as soon as its input piece has been issued; the
+// outputs drain through two pinned slots chunk by chunk.
+bool host_pinned(const void* p) {
+    static const bool off = getenv("XG_NO_STAGING") != nullptr;  // A/B aid: the driver's own pageable copies
+    if (off) return true;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// Persistent workers for large host memcpys (one job at a time, the caller joins).
+class MemcpyPool {
+  public:
+    static MemcpyPool& get() {
+        static MemcpyPool p;
+        return p;
+    }
+    void copy(void* dst, const void* src, size_t n) {
+        if (nw_ == 0 || n < ((size_t)1 << 20)) {
+            std::memcpy(dst, src, n);
+            return;
+        }
+        std::lock_guard<std::mutex> one(call_mu_);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = static_cast<char*>(dst);
+            src_ = static_cast<const char*>(src);
+            n_ = n;
+            parts_ = nw_ + 1;
+            next_.store(0);
+            left_ = parts_;
+            ++gen_;
+        }
+        cv_.notify_all();
+        run();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return left_ == 0; });
+    }
+    ~MemcpyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+
+  private:
+    MemcpyPool() {
+        const unsigned hc = std::thread::hardware_concurrency();
+        nw_ = (int)std::min(7u, hc > 1 ? hc - 1 : 0u);
+        if (const char* e = getenv("XG_COPY_THREADS")) nw_ = std::max(0, std::min(63, atoi(e) - 1));
+        for (int i = 0; i < nw_; ++i) th_.emplace_back([this] { worker(); });
+    }
+    void run() {
+        for (;;) {
+            const int i = next_.fetch_add(1);
+            if (i >= parts_) return;
+            const size_t a = n_ * (size_t)i / parts_, b = n_ * (size_t)(i + 1) / parts_;
+            std::memcpy(dst_ + a, src_ + a, b - a);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--left_ == 0) done_.notify_all();
+        }
+    }
+    void worker() {
+        int seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            run();
+        }
+    }
+    int nw_ = 0;
+    std::vector<std::thread> th_;
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, done_;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t n_ = 0;
+    int parts_ = 0, left_ = 0, gen_ = 0;
+    std::atomic<int> next_{0};
+    bool stop_ = false;
+};
+
+// Pinned slots per device: 4 for inputs, 2 for outputs (32 MiB each).
+struct Staging {
+    static constexpr int kIn = 4, kOut = 2;
+    static constexpr size_t kSlot = (size_t)32 << 20;
+    std::mutex mu;  // one pageable call per device at a time
+    void* in[kIn] = {};
+    void* out[kOut] = {};
+    cudaEvent_t in_ev[kIn] = {}, out_ev[kOut] = {};
+    int next_in = 0;
+    bool ready = false;
+    void init() {
+        if (ready) return;
+        for (int i = 0; i < kIn; ++i) {
+            ck(cudaMallocHost(&in[i], kSlot), "pinned staging");
+            ck(cudaEventCreateWithFlags(&in_ev[i], cudaEventDisableTiming), "event");
+        }
+        for (int i = 0; i < kOut; ++i) {
+            ck(cudaMallocHost(&out[i], kSlot), "pinned staging");
+            ck(cudaEventCreateWithFlags(&out_ev[i], cudaEventDisableTiming), "event");
+        }
+        ready = true;
+    }
+    // host -> device through the input slots, async on s (the caller records its own event after)
+    void h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
+        for (size_t off = 0; off < bytes; off += kSlot) {
+            const size_t n = std::min(kSlot, bytes - off);
+            const int k = next_in++ % kIn;
+            ck(cudaEventSynchronize(in_ev[k]), "staging");  // the slot's previous H2D is done
+            MemcpyPool::get().copy(in[k], static_cast<const char*>(h) + off, n);
+            ck(cudaMemcpyAsync(static_cast<char*>(d) + off, in[k], n, cudaMemcpyHostToDevice, s), "h2d");
+            ck(cudaEventRecord(in_ev[k], s), "event");
+        }
+    }
+};
+
+Staging& staging(int dev) {
+    static Staging st[kMaxDev];
+    return st[dev % kMaxDev];
+}
+
 void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, float alpha, float beta, int M,
                        int K, int N, const xg_config* cfg, int reduce, float* out_h, xg_report* rep) {
     req(K <= xg::gemm_max_inner(cfg->bits), "gemm_int: inner dimension permits 32-bit overflow");
@@ -2048,7 +2188,8 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
     float* dc = c_h ? S.get<float>((int64_t)M * N) : nullptr;
     float* dout = S.get<float>((int64_t)M * N);
     PipeWs w;
-    alloc_ws(w, M, N, ldk, [&](auto* tag, int64_t cnt) { return S.get<std::remove_pointer_t<decltype(tag)>>(cnt); });
+    alloc_ws(w, M, N, ldk, [&](auto* tag, int64_t cnt) { return S.get<std::remove_pointer_t<decltype(tag)>>(cnt); },
+             false);  // row-chunked compensation: masked-dense launches only
     // the workspace comes from the stream-ordered pool of `s`: the copy streams wait for it
     ck(cudaEventRecord(ev[0], s), "event");
     ck(cudaStreamWaitEvent(s_in, ev[0], 0), "wait");
@@ -2062,18 +2203,89 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
     int r0s[9], nchk = 0;
     for (int r = 0; r < M && nchk < nch; r += rc) r0s[nchk++] = r;
     r0s[nchk] = M;
-    // H2D: B, A chunks, C
-    ck(cudaMemcpyAsync(db, b_h, sizeof(float) * (size_t)K * N, cudaMemcpyHostToDevice, s_in), "h2d");
-    ck(cudaEventRecord(ev[1], s_in), "event");
+    // H2D pieces in order: B (ev[1]), the A row chunks (ev[2 + i]), C (ev[10])
+    struct Piece {
+        void* d;
+        const void* h;
+        size_t bytes;
+        cudaEvent_t e;
+    };
+    std::vector<Piece> pieces;
+    pieces.push_back({db, b_h, sizeof(float) * (size_t)K * N, ev[1]});
     for (int i = 0; i < nchk; ++i) {
         const size_t off = (size_t)r0s[i] * K, cnt = (size_t)(r0s[i + 1] - r0s[i]) * K;
-        ck(cudaMemcpyAsync(da + off, a_h + off, sizeof(float) * cnt, cudaMemcpyHostToDevice, s_in), "h2d");
-        ck(cudaEventRecord(ev[2 + i], s_in), "event");
+        pieces.push_back({da + off, a_h + off, sizeof(float) * cnt, ev[2 + i]});
     }
-    if (c_h) {
-        ck(cudaMemcpyAsync(dc, c_h, sizeof(float) * (size_t)M * N, cudaMemcpyHostToDevice, s_in), "h2d");
-        ck(cudaEventRecord(ev[10], s_in), "event");
+    if (c_h) pieces.push_back({dc, c_h, sizeof(float) * (size_t)M * N, ev[10]});
+    const bool pageable_in = !host_pinned(a_h) || !host_pinned(b_h) || (c_h && !host_pinned(c_h));
+    const bool pageable_out = !host_pinned(out_h);
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "device");
+    Staging* stg = nullptr;
+    std::unique_lock<std::mutex> stg_lock;
+    if (pageable_in || pageable_out) {
+        stg = &staging(dev);
+        stg_lock = std::unique_lock<std::mutex>(stg->mu);
+        stg->init();
     }
+    auto issue = [&](const Piece& pc) {
+        if (host_pinned(pc.h)) ck(cudaMemcpyAsync(pc.d, pc.h, pc.bytes, cudaMemcpyHostToDevice, s_in), "h2d");
+        else stg->h2d(pc.d, pc.h, pc.bytes, s_in);
+        ck(cudaEventRecord(pc.e, s_in), "event");
+    };
+    // pageable inputs: a feeder thread issues the pieces (the main thread waits for
+    // piece j before it enqueues the stream wait on piece j's event)
+    std::mutex fm;
+    std::condition_variable fcv;
+    int issued = 0;
+    bool ffail = false, fstop = false;
+    std::string ferr;
+    std::thread feeder;
+    struct Joiner {
+        std::thread& t;
+        std::mutex& m;
+        bool& stop;
+        ~Joiner() {
+            if (t.joinable()) {
+                {
+                    std::lock_guard<std::mutex> lk(m);
+                    stop = true;
+                }
+                t.join();
+            }
+        }
+    } joiner{feeder, fm, fstop};
+    if (pageable_in) {
+        feeder = std::thread([&, dev] {
+            try {
+                ck(cudaSetDevice(dev), "device");
+                for (size_t j = 0; j < pieces.size(); ++j) {
+                    {
+                        std::lock_guard<std::mutex> lk(fm);
+                        if (fstop) return;
+                    }
+                    issue(pieces[j]);
+                    std::lock_guard<std::mutex> lk(fm);
+                    issued = (int)j + 1;
+                    fcv.notify_all();
+                }
+            } catch (const std::exception& ex) {
+                std::lock_guard<std::mutex> lk(fm);
+                ffail = true;
+                ferr = ex.what();
+                fcv.notify_all();
+            }
+        });
+    } else {
+        for (const Piece& pc : pieces) issue(pc);
+        issued = (int)pieces.size();
+    }
+    auto wait_piece = [&](int j) {
+        if (!pageable_in) return;
+        std::unique_lock<std::mutex> lk(fm);
+        fcv.wait(lk, [&] { return issued > j || ffail; });
+        if (ffail) throw CudaFail(ferr);
+    };
     // compute
     PipeCall q{da, db, dc, alpha, beta, M, K, N, *cfg, reduce, dout};
     Pipe p;
@@ -2085,6 +2297,7 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
     p.bqT = w.bqT; p.rbqT = w.rbqT; p.bredT = w.bredT;
     p.la = w.la; p.lb = w.lb; p.lar = w.lar; p.lbr = w.lbr; p.colmax = w.colmax;
     ck(cudaMemsetAsync(p.sc, 0, sizeof(xg::DevScalars), s), "memset");
+    wait_piece(0);
     ck(cudaStreamWaitEvent(s, ev[1], 0), "wait");
     quantize_b_vw(p, db);
     if (reduce)
@@ -2093,6 +2306,7 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
     // contribution to the row / column statistics
     for (int i = 0; i < nchk; ++i) {
         const int r0 = r0s[i], rows = r0s[i + 1] - r0s[i];
+        wait_piece(1 + i);
         ck(cudaStreamWaitEvent(s, ev[2 + i], 0), "wait");
         quantize_a_rows(p, da, r0, rows);
         Pipe pi = p;
@@ -2108,6 +2322,7 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
         }
     }
     if (c_h) {
+        wait_piece(1 + nchk);
         ck(cudaStreamWaitEvent(s, ev[10], 0), "wait");
         xg::finite_max(dc, (int64_t)M * N, &p.sc->retB /*scratch, reset below*/, &p.sc->nonfinite, s);
         check_launch("finite C");
@@ -2131,9 +2346,44 @@ void run_pipeline_host(const float* a_h, const float* b_h, const float* c_h, flo
         pi.lar = p.lar ? p.lar + r0 : nullptr;
         gemm_comp(pi, dout + (int64_t)r0 * N, dc ? dc + (int64_t)r0 * N : nullptr, alpha, beta);
         ck(cudaEventRecord(ev[11 + i], s), "event");
+        if (pageable_out) continue;  // drained through the pinned slots below
         ck(cudaStreamWaitEvent(s_out, ev[11 + i], 0), "wait");
         ck(cudaMemcpyAsync(out_h + (int64_t)r0 * N, dout + (int64_t)r0 * N, sizeof(float) * (size_t)rows * N,
                            cudaMemcpyDeviceToHost, s_out), "d2h");
+    }
+    if (pageable_out) {
+        // blocks of <= one slot, alternating two slots: block k's D2H overlaps the
+        // host copy of block k - 1 out of the other slot
+        struct Blk {
+            size_t off, bytes;
+        };
+        std::vector<Blk> blks;
+        std::vector<int> chunk_of;
+        for (int i = 0; i < nchk; ++i) {
+            const size_t b0 = (size_t)r0s[i] * N * sizeof(float), b1 = (size_t)r0s[i + 1] * N * sizeof(float);
+            for (size_t o = b0; o < b1; o += Staging::kSlot) {
+                blks.push_back({o, std::min(Staging::kSlot, b1 - o)});
+                chunk_of.push_back(i);
+            }
+        }
+        auto drain = [&](size_t k) {
+            const int sl = (int)(k % Staging::kOut);
+            ck(cudaEventSynchronize(stg->out_ev[sl]), "d2h");
+            MemcpyPool::get().copy(reinterpret_cast<char*>(out_h) + blks[k].off, stg->out[sl], blks[k].bytes);
+        };
+        int waited = -1;
+        for (size_t k = 0; k < blks.size(); ++k) {
+            const int sl = (int)(k % Staging::kOut);
+            if (chunk_of[k] != waited) {
+                ck(cudaStreamWaitEvent(s_out, ev[11 + chunk_of[k]], 0), "wait");
+                waited = chunk_of[k];
+            }
+            ck(cudaMemcpyAsync(stg->out[sl], reinterpret_cast<const char*>(dout) + blks[k].off, blks[k].bytes,
+                               cudaMemcpyDeviceToHost, s_out), "d2h");
+            ck(cudaEventRecord(stg->out_ev[sl], s_out), "event");
+            if (k >= 1) drain(k - 1);
+        }
+        if (!blks.empty()) drain(blks.size() - 1);
     }
     xg::DevScalars h;
     ck(cudaMemcpyAsync(&h, w.sc, sizeof h, cudaMemcpyDeviceToHost, s), "report");

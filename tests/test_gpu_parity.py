@@ -441,6 +441,32 @@ def test_host_entry_overlapped_equals_device(shape):
         xg.xigemm_host(bad, b, cfg=cfg)
 
 
+def _pinned(x):
+    t = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+    t.numpy()[...] = x
+    return t.numpy()
+
+
+@pytest.mark.parametrize("shape", [(2600, 4096, 3100), (700, 1500, 333)])
+def test_host_entry_pageable_equals_pinned(shape):
+    """Pageable host buffers (the C++ drop-in's std::vector memory) go through the
+    pinned staging slots (32 MiB: A, B, C and the result span several slots and
+    ragged last blocks); every mix of pinned / pageable buffers gives the same bits."""
+    m, k, n = shape
+    a = ol.random_dense(m, k, 5, -3, 3)
+    b = ol.random_dense(k, n, 6, -3, 3)
+    c = ol.random_dense(m, n, 7, -1, 1)
+    cfg = xg.XigemmConfig(threshold=0.05, density_limit=0.5, scheme=xg.QuantScheme.VectorWise,
+                          policy=xg.ReductionPolicy.AvgRule)
+    ref = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda(), 1.5, -0.25,
+                    cfg).result.cpu().numpy()
+    pa, pb, pc = _pinned(a), _pinned(b), _pinned(c)
+    for aa, bb, cc, pinned_out in ((a, b, c, False), (pa, pb, pc, True), (pa, b, pc, False), (a, pb, c, True)):
+        out = _pinned(np.zeros((m, n), np.float32)) if pinned_out else np.zeros((m, n), np.float32)
+        res, _ = xg.xigemm_host(aa, bb, cc, 1.5, -0.25, cfg=cfg, out=out)
+        assert beq(res, ref)
+
+
 @pytest.mark.parametrize("k,n", [(256, 33), (300, 100), (2047, 64), (2049, 96), (5000, 1000), (8192, 200),
                                  (4100, 31)])
 def test_fused_column_quantisation(oracle, k, n):

@@ -37,22 +37,25 @@ def _driver():
     return DRIVER
 
 
-def _run(tool):
+def _run(tool, env=None):
     r = subprocess.run([SAN, "--tool", tool, "--print-limit", "50", _driver()], capture_output=True, text=True,
-                       timeout=1500)
+                       timeout=1500, env=dict(os.environ, **(env or {})))
     out = r.stdout + r.stderr
     assert "sanitize driver ok" in out, out[-4000:]
     return r.returncode, out
 
 
+# XG_COMP=2 forces the sparse terms onto the CUDA-core CSR path (csrc/spmm.cu)
+@pytest.mark.parametrize("comp", ["auto", "csr"])
 @pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
-def test_sanitizer_clean(tool):
-    rc, out = _run(tool)
+def test_sanitizer_clean(tool, comp):
+    rc, out = _run(tool, {"XG_COMP": "2"} if comp == "csr" else None)
     assert rc == 0 and re.search(r"ERROR SUMMARY: 0 errors", out), out[-4000:]
 
 
-def test_racecheck_only_tmem_alloc_slot():
-    rc, out = _run("racecheck")
+@pytest.mark.parametrize("comp", ["auto", "csr"])
+def test_racecheck_only_tmem_alloc_slot(comp):
+    rc, out = _run("racecheck", {"XG_COMP": "2"} if comp == "csr" else None)
     races = [ln for ln in out.splitlines() if "Race reported" in ln or "Access at" in ln or "access at" in ln]
     bad = []
     block = []
