@@ -623,8 +623,18 @@ void alloc_ws(PipeWs& w, int M, int N, int64_t ldk, Get&& get, bool csr = true) 
     }
 }
 
-void set_csr(Pipe& p, const PipeWs& w) {
-    p.csr_ok = w.segA != nullptr;
+// The CSR path can win only where its density-independent cost (the builds and
+// the two epilogue passes) is below the masked-dense launch's (comp model of
+// k_dispatch): otherwise its kernels are not even enqueued.
+bool csr_possible(const xg::CompModel& m, int M, int N, int K) {
+    if (m.force == 2) return true;
+    if (m.force == 1) return false;
+    const double mn = (double)M * N;
+    return mn * m.c_el + ((double)M + N) * K / m.bw < 0.9 * 4.0 * mn * K / m.p_tc;
+}
+
+void set_csr(Pipe& p, const PipeWs& w, const xg::CompModel& m) {
+    p.csr_ok = w.segA != nullptr && csr_possible(m, p.M, p.N, p.K);
     if (!p.csr_ok) return;
     p.csrA = xg::QCsr{w.segA, w.quadA, &w.sc->qcurA, w.capA};
     p.csrB = xg::QCsr{w.segB, w.quadB, &w.sc->qcurB, w.capB};
@@ -659,7 +669,7 @@ int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* du
     p.stamp_df = &w.sc->ts[1];
     p.stamp_comp = &w.sc->ts[3];
     p.report_dst = report_dst;
-    set_csr(p, w);
+    set_csr(p, w, q.cm);
     const int M = q.M, K = q.K, N = q.N;
     p.pre_init = true;  // stage 0 initialises everything in one launch
     if (stage == 0) {
@@ -1783,7 +1793,7 @@ Pipe shard_pipe(ShardState& h, cudaStream_t s) {
     p.aq = h.w.aq; p.raq = h.w.raq; p.ared = h.w.ared;
     p.bqT = h.w.bqT; p.rbqT = h.w.rbqT; p.bredT = h.w.bredT;
     p.la = h.w.la; p.lb = h.w.lb; p.lar = h.w.lar; p.lbr = h.w.lbr; p.colmax = h.w.colmax;
-    set_csr(p, h.w);
+    set_csr(p, h.w, h.q.cm);
     return p;
 }
 

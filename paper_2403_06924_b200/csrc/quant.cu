@@ -1196,7 +1196,10 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
     const int nstrips = (cols + kWC - 1) / kWC;
     const int nchunks = (rows + kWItemRows - 1) / kWItemRows;
     const int nitems = nstrips * nchunks;
-    const int my_items = nitems > (int)blockIdx.x ? (nitems - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    // a contiguous range of items in strip-major order: consecutive items share a
+    // strip, so its scales, thresholds and dequant table are built once per strip
+    const int it0 = (int)((int64_t)nitems * blockIdx.x / gridDim.x);
+    const int my_items = (int)((int64_t)nitems * (blockIdx.x + 1) / gridDim.x) - it0;
     const int nsub = my_items * kWSub;  // sub-tiles this warp will consume
     double lam_r = 0.0, lam_t = 0.0, so = 1.0;
     if (SELECT) {
@@ -1209,8 +1212,8 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
     const float lam_r32 = __double2float_rn(lam_r);
     float* wring = ring + w * kWSlots * kWC * kWR;
     auto issue = [&](int g) {  // sub-tile g of this warp's sequence into slot g % kWSlots
-        const int item = (int)blockIdx.x + (g / kWSub) * (int)gridDim.x;
-        const int strip = item % nstrips, chunk = item / nstrips;
+        const int item = it0 + g / kWSub;
+        const int strip = item / nchunks, chunk = item % nchunks;
         const int slot = g % kWSlots;
         mbar_expect_tx(&full[w][slot], kWC * kWR * 4);
         tma_load_2d(wring + slot * kWC * kWR, &tmap, &full[w][slot], strip * kWC,
@@ -1229,21 +1232,25 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
     float rm = 0.0f, ret = 0.0f;
     unsigned cnt = 0;
     int g = 0;
+    int cur_strip = -1;
+    double lam = 0.0;
+    float lam32 = 0.0f, tf = 0.0f;
+    bool exact = false;
     for (int i = 0; i < my_items; ++i) {
-        const int item = (int)blockIdx.x + i * (int)gridDim.x;
-        const int strip = item % nstrips, chunk = item / nstrips;
+        const int item = it0 + i;
+        const int strip = item / nchunks, chunk = item % nchunks;
         const int n = strip * kWC + lane;
         const int nc = min(n, cols - 1);
-        double lam;
+        if (strip != cur_strip) {
         if (SELECT) lam = sa.vec ? sa.lam[nc] : lam_t;
         else lam = qa.per_col ? compute_scale((double)__uint_as_float(qa.colmax[nc]), bits) : lam_t;
         if (!SELECT && qa.per_col && qa.lam_out && chunk == 0 && w == 0 && n < cols) qa.lam_out[n] = lam;
         if (!SELECT && qa.per_col && qa.rcp_out && chunk == 0 && w == 0 && n < cols) qa.rcp_out[n] = ff_recip(lam);
-        const float lam32 = __double2float_rn(lam);
-        const bool exact = !(lam32 <= FLT_MAX) || (SELECT && !(lam_r32 <= FLT_MAX));
-        float tf = __int_as_float(0x7f800000);
+        lam32 = __double2float_rn(lam);
+        exact = !(lam32 <= FLT_MAX) || (SELECT && !(lam_r32 <= FLT_MAX));
+        tf = __int_as_float(0x7f800000);
         if (SELECT && sa.do_select && n < cols) tf = float_above(threshold_of(sa.policy, sa.thr_m, sa.stat[nc], so, rows));
-        __syncthreads();  // previous item's table readers are done
+        __syncthreads();  // previous strip's table readers are done
         {
             const double inv = __ddiv_rn(1.0, lam);
             constexpr int per = (128 + kWW - 1) / kWW;  // q in [0, qmax], mirrored (see build_row_lut)
@@ -1255,6 +1262,8 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
                 }
         }
         __syncthreads();
+        cur_strip = strip;
+        }
         float lmax = 0.0f;
         for (int j = 0; j < kWSub; ++j, ++g) {
             const int slot = g % kWSlots;
