@@ -662,6 +662,18 @@ __global__ void __launch_bounds__(384, 1)
                 i0 = args.rs[ts][sel].rcp(row);
                 if (NACC > 1) i1 = args.rs[1][sel].rcp(row);
             }
+            // column reciprocals: this term's scale refs hoisted, chunk i+1's values
+            // loaded while chunk i is processed (a global load per chunk otherwise
+            // sits on the epilogue's critical path)
+            const ScaleRef csr0 = args.cs[ts][sel];
+            const ScaleRef csr1 = args.cs[NACC > 1 ? 1 : ts][sel];
+            auto col_rcp = [&](int chunk, float2& r0c, float2& r1c) {
+                const int cl = min(colbase + chunk * CW + lane, args.N - 1);
+                r0c = csr0.rcp(cl);
+                if (NACC > 1) r1c = csr1.rcp(cl);
+            };
+            float2 nrc0 = make_float2(1.0f, 0.0f), nrc1 = nrc0;
+            if (nchunk > 0) col_rcp(rev ? nchunk - 1 : 0, nrc0, nrc1);
             mbar_wait(&tfull[buf], bphase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * Cfg::ACC_COLS +
@@ -685,9 +697,9 @@ __global__ void __launch_bounds__(384, 1)
                     tma_load_2d(stg0 + (cn % NS) * (32 * CW), &emaps.din, &mybar[cn % NS], colbase + cn * CW, rowbase);
                 }
                 // column reciprocals of this chunk, broadcast through shared memory
-                const int mycol = min(col0 + lane, args.N - 1);
-                scw[lane] = args.cs[ts][sel].rcp(mycol);
-                if (NACC > 1) scw[32 + lane] = args.cs[1][sel].rcp(mycol);
+                scw[lane] = nrc0;
+                if (NACC > 1) scw[32 + lane] = nrc1;
+                if (i + 1 < nchunk) col_rcp(rev ? c - 1 : c + 1, nrc0, nrc1);
                 uint32_t acc[NACC][CW];
 #pragma unroll
                 for (int a = 0; a < NACC; ++a) tmem_ld_cols<CW>(tbase + a * Cfg::BN + c * CW, acc[a]);
