@@ -1582,7 +1582,9 @@ __global__ void k_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, dou
                 const double mn = (double)M * (double)N;
                 const double t_d = 4.0 * mn * (double)K / cm.p_tc;
                 const double macs = (double)sc->nnzA * (double)N + (double)sc->nnzB * (double)M;
-                const double t_c = fmax(macs / cm.p_sp, mn * cm.c_el) + ((double)M + (double)N) * K / cm.bw;
+                // K > 8192 runs 8-line strips: twice the strips, half the columns per lane
+                const double wf = K > 8192 ? 1.5 : 1.0;
+                const double t_c = fmax(macs * wf / cm.p_sp, mn * cm.c_el * wf) + ((double)M + (double)N) * K / cm.bw;
                 csr = t_c < 0.9 * t_d;
             }
         }
@@ -1872,12 +1874,13 @@ void launch_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, double de
     k_dispatch<<<1, 1, 0, s>>>(sc, bits, MK, KN, density_limit, reduce, M, N, K, cm);
 }
 
-// B200 measurements (tools/csr_sweep.py at 8192^3, profiles/r2_csr_sweep.txt):
-// compensation launch 3.6e15 int8 op/s (4MNK masked-dense), strip SpMM ~1.1e13
-// MAC/s incremental, 8.3 ns of fixed epilogue work per output element, HBM 6.4e12 B/s
+// B200 measurements (tools/csr_sweep.py, profiles/r2_csr_sweep_*.jsonl): the
+// compensation launch 3.6e15 int8 op/s (4MNK masked-dense); 16-line strips
+// (K <= 8192) ~9.6e12 MAC/s incremental and 7.7 ns of density-independent work
+// per output element (8-line strips: x1.5); HBM 6.4e12 B/s
 namespace {
 CompModel g_model = [] {
-    CompModel m{3.6e15, 1.1e13, 6.4e12, 8.3e-12, 0, 0};
+    CompModel m{3.6e15, 9.6e12, 6.4e12, 7.7e-12, 0, 0};
     if (const char* e = getenv("XG_COMP")) m.force = atoi(e);  // 0 auto, 1 dense, 2 CSR
     if (const char* e = getenv("XG_P_SPMM")) m.p_sp = atof(e);
     return m;
