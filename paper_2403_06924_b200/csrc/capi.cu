@@ -631,7 +631,7 @@ bool csr_possible(const xg::CompModel& m, int M, int N, int K) {
     if (m.force == 1) return false;
     const double mn = (double)M * N;
     const double wf = K > 8192 ? 1.5 : 1.0;  // as k_dispatch
-    return mn * m.c_el * wf + ((double)M + N) * K / m.bw < 0.9 * 4.0 * mn * K / m.p_tc;
+    return mn * m.c_el * wf + 3.0 * ((double)M + N) * K / m.bw < 0.9 * 4.0 * mn * K / m.p_tc;
 }
 
 void set_csr(Pipe& p, const PipeWs& w, const xg::CompModel& m) {

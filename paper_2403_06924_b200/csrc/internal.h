@@ -41,7 +41,7 @@ struct DevScalars {
 
 // Cost model of the compensation choice (k_dispatch): masked-dense tcgen05
 // t_d = 4MNK / p_tc against the CUDA-core CSR path t_c = max((nnzA N + nnzB M)
-// / p_sp, MN c_el) + (M + N) K / bw (the CSR builds), c_el the per-output-element
+// / p_sp, MN c_el) + 3 (M + N) K / bw (the CSR builds), c_el the per-output-element
 // cost of its two exact epilogue passes.  The CSR path is taken when t_c <
 // 0.9 t_d.  Rates measured on B200 (xg_calibrate_eta re-measures p_tc, p_sp).
 // force: 0 auto, 1 dense, 2 CSR.

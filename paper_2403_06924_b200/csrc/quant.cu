@@ -681,6 +681,13 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
     return v;
 }
+// table entry at adj + (u << SHIFT): one IMAD (adj already holds the -(magic << SHIFT) bias)
+template <int SHIFT>
+__device__ __forceinline__ float lut_at(uint32_t u, uint32_t adj) {
+    uint32_t a;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(a) : "r"(u), "n"(1 << SHIFT), "r"(adj));
+    return lds_f32(a);
+}
 // NaN-propagating max (PTX max.NaN): a NaN input makes dmax NaN, which sends
 // the quad to the exact path (quantize.cpp:13-24 maps NaN to -qmax).
 __device__ __forceinline__ float fmax_nan(float a, float b) {
@@ -758,7 +765,7 @@ __global__ void __launch_bounds__(NT) k_quant_rows_fast(const QuantRowsArgs a) {
                 for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(x[4 * v + e], lam, qmaxf, kNearest));
             }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[4 * v + e], lds_f32((u[e] << 2) + adj))));
+            for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[4 * v + e], lut_at<2>(u[e], adj))));
             store_quad(qrow, (v * NT + (int)threadIdx.x) * 4, a.cols, vec, pack4u(u[0], u[1], u[2], u[3]));
         }
         rmax_acc = fmaxf(rmax_acc, rm);
@@ -785,14 +792,14 @@ __device__ __forceinline__ void select_quad_n(const float (&x)[4], uint32_t lut_
     float res[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-        res[e] = __fsub_rn(x[e], lds_f32((u[e] << SHIFT) + lut_adj));
+        res[e] = __fsub_rn(x[e], lut_at<SHIFT>(u[e], lut_adj));
         ur[e] = qn(res[e], lam_r32, dmax);
     }
     if (exact || !(dmax < 0.4999f)) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             u[e] = ubits(qexact(x[e], lam, qmaxf, kNearest));
-            res[e] = __fsub_rn(x[e], lds_f32((u[e] << SHIFT) + lut_adj));
+            res[e] = __fsub_rn(x[e], lut_at<SHIFT>(u[e], lut_adj));
             ur[e] = ubits(qexact(res[e], lam_r, qmaxf, kNearest));
         }
     }
@@ -956,7 +963,7 @@ __global__ void __launch_bounds__(kThreads) k_quant_rows_async(const QuantRowsAr
                 for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(x[e], lam, qmaxf, kNearest));
             }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[e], lds_f32((u[e] << 2) + adj))));
+            for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[e], lut_at<2>(u[e], adj))));
             *reinterpret_cast<uint32_t*>(qrow + c) = pack4u(u[0], u[1], u[2], u[3]);
         }
         rmax_acc = fmaxf(rmax_acc, rm);
@@ -1008,7 +1015,7 @@ __device__ __forceinline__ void build_row_lut(float* lut, double lam, int qmax) 
     }
 }
 
-template <int U, int MINB = kRCtasPerSM>
+template <int U, int MINB = kRCtasPerSM, bool KEEP = true>
 __global__ void __launch_bounds__(kRT, MINB) k_select_rows_r4(const SelectArgs a) {
     XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
@@ -1055,7 +1062,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_select_rows_r4(const SelectArgs a
                     select_quad_n<2>(x, adj, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, pq, pr, cnt, lmax);
                     *reinterpret_cast<uint32_t*>(rq_row + c) = pq;
                     if (a.do_select) *reinterpret_cast<uint32_t*>(rd_row + c) = pr;
-                    if (a.keep) dump_keep4(a, r, c, x, tf);
+                    if (KEEP && a.keep) dump_keep4(a, r, c, x, tf);
                 }
             }
         }
@@ -1146,7 +1153,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_quant_rows_r4(const QuantRowsArgs
                 for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(x[e], lam, qmaxf, kNearest));
             }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[e], lds_f32((u[e] << 2) + adj))));
+            for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[e], lut_at<2>(u[e], adj))));
             if (c < a.cols) *reinterpret_cast<uint32_t*>(qrow + c) = pack4u(u[0], u[1], u[2], u[3]);
         }
         rmax_acc = fmaxf(rmax_acc, rm);
@@ -1176,7 +1183,7 @@ constexpr int kWC = 32, kWR = 32, kWSub = 4;  // strip width, sub-tile rows, sub
 template <int WW, int SLOTS>
 constexpr int col_w_smem() { return WW * SLOTS * kWC * kWR * 4 + 256 * kWC * 4 + 1024; }
 
-template <bool SELECT, int kWW, int kWSlots, int kWCtas>
+template <bool SELECT, int kWW, int kWSlots, int kWCtas, bool KEEP = true>
 __global__ void __launch_bounds__(kWW * 32, kWCtas)
     k_cols_w4(const __grid_constant__ CUtensorMap tmap, const QuantColsArgs qa, const SelectArgs sa) {
     XG_PDL_WAIT();
@@ -1285,7 +1292,7 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
                 if (SELECT) {
                     select_quad_n<7>(xq, adj_base, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, w0[q], w1[q],
                                      cnt, lmax);
-                    if (sa.keep && n < cols && k0 + 4 * q < rows) dump_keep4(sa, n, k0 + 4 * q, xq, tf);
+                    if (KEEP && sa.keep && n < cols && k0 + 4 * q < rows) dump_keep4(sa, n, k0 + 4 * q, xq, tf);
                 } else {
                     uint32_t u[4];
                     float dmax = 0.0f;
@@ -1296,7 +1303,7 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
                         for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(xq[e], lam, qmaxf, kNearest));
                     }
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(xq[e], lds_f32((u[e] << 7) + adj_base))));
+                    for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(xq[e], lut_at<7>(u[e], adj_base))));
                     w0[q] = pack4u(u[0], u[1], u[2], u[3]);
                 }
             }
@@ -1508,7 +1515,7 @@ __global__ void __launch_bounds__(kWW * 32, 1)
                         for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(xq[e], lam, qmaxf, kNearest));
                     }
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(xq[e], lds_f32((u[e] << 7) + adj_base))));
+                    for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(xq[e], lut_at<7>(u[e], adj_base))));
                     w0[q] = pack4u(u[0], u[1], u[2], u[3]);
                 }
                 if (n < cols && k0 < rows) {
@@ -1584,7 +1591,8 @@ __global__ void k_dispatch(DevScalars* sc, int bits, int64_t MK, int64_t KN, dou
                 const double macs = (double)sc->nnzA * (double)N + (double)sc->nnzB * (double)M;
                 // K > 8192 runs 8-line strips: twice the strips, half the columns per lane
                 const double wf = K > 8192 ? 1.5 : 1.0;
-                const double t_c = fmax(macs * wf / cm.p_sp, mn * cm.c_el * wf) + ((double)M + (double)N) * K / cm.bw;
+                // the two CSR builds read A'q / B'q^T at ~1/3 of HBM bandwidth (measured)
+                const double t_c = fmax(macs * wf / cm.p_sp, mn * cm.c_el * wf) + 3.0 * ((double)M + (double)N) * K / cm.bw;
                 csr = t_c < 0.9 * t_d;
             }
         }
@@ -1720,7 +1728,8 @@ template <bool SELECT, int WW, int SLOTS, int CTAS>
 void launch_cols_w(const CUtensorMap& tm, const QuantColsArgs& qa, const SelectArgs& sa, int rows, int cols,
                    int co_share, cudaStream_t s) {
     constexpr int smem = col_w_smem<WW, SLOTS>();
-    auto kern = k_cols_w4<SELECT, WW, SLOTS, CTAS>;
+    // no stage-dump bitmask: the variant without the per-quad check
+    auto kern = (SELECT && !sa.keep) ? k_cols_w4<SELECT, WW, SLOTS, CTAS, false> : k_cols_w4<SELECT, WW, SLOTS, CTAS>;
     set_dyn_smem(kern, smem);
     const int items = ((cols + kWC - 1) / kWC) * ((rows + WW * kWR * kWSub - 1) / (WW * kWR * kWSub));
     const int cap = kNumSMs * (co_share > 0 ? co_share : CTAS);
@@ -1835,7 +1844,8 @@ void launch_select_rows(const SelectArgs& a, cudaStream_t s) {
         if (cfg.x == 2) k_select_rows_r4<2, 8><<<g, kRT, 0, s>>>(a);
         else if (cfg.x == 8) k_select_rows_r4<8, 6><<<g, kRT, 0, s>>>(a);
         else if (cfg.y >= 12) k_select_rows_r4<4, 12><<<g, kRT, 0, s>>>(a);
-        else k_select_rows_r4<4><<<g, kRT, 0, s>>>(a);
+        else if (a.keep) k_select_rows_r4<4><<<g, kRT, 0, s>>>(a);
+        else k_select_rows_r4<4, kRCtasPerSM, false><<<g, kRT, 0, s>>>(a);  // no stage-dump bitmask
         return;
     }
     if (a.fix_mode) k_fix_rows<<<grid_rows(a.rows), kThreads, 0, s>>>(a);
