@@ -1987,6 +1987,7 @@ xg_status xg_shard_finish(xg_shard* h, xg_report* rep, xg_stream s) {
             rep->nnz_a = S.q.reduce ? (int64_t)d.nnzA : 0;
             rep->nnz_b = S.q.reduce ? (int64_t)d.nnzB : 0;
             rep->stats_fallbacks = d.nflag;
+            rep->comp_kernel = (d.csr && !d.csr_bad) ? 1 : 0;
         }
     });
 }

@@ -187,7 +187,7 @@ def run_protocol(shards: list, comm, nranks: int) -> None:
 
 def _report(rep: XgReport, result) -> GemmReport:
     return GemmReport(result, rep.density_a, rep.density_b, GemmPath(rep.path), {}, rep.nnz_a, rep.nnz_b,
-                      rep.stats_fallbacks)
+                      rep.stats_fallbacks, rep.comp_kernel)  # comp_kernel: this rank's compensation kernel
 
 
 def split_rows(m: int, nranks: int) -> list[int]:

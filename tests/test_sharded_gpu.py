@@ -143,3 +143,26 @@ def test_sharded_nccl_graph_replay():
                         os.path.join(root, "tools", "shard_graph_check.py")],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "equal single-GPU: True" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("g", [2, 3])
+def test_sharded_csr_compensation(g):
+    """The CUDA-core CSR compensation (forced) inside each shard: every rank's
+    rows equal the single-GPU result (itself equal to the masked-dense launch)."""
+    m, k, n = 700, 2052, 1028
+    a = torch.from_numpy(ol.random_dense(m, k, m + 3, -4, 4)).cuda()
+    b = torch.from_numpy(ol.random_dense(k, n, n + 5, -4, 4)).cuda()
+    c = torch.from_numpy(ol.random_dense(m, n, 9, -1, 1)).cuda()
+    cfg = _cfg(dict(bits=8, threshold=0.0202, density_limit=0.9, scheme=1, policy=0, rounding=1))
+    saved = xg.comp_model()["force"]
+    try:
+        xg.comp_model(force=1)
+        ref = xg.xigemm(a, b, c, 1.25, -0.5, cfg)
+        xg.comp_model(force=2)
+        got = sharded.xigemm_sharded_local(a, b, c, 1.25, -0.5, cfg, nranks=g)
+    finally:
+        xg.comp_model(force=saved)
+    assert int(ref.path) == 0 and ref.comp_kernel == 0 and got.comp_kernel == 1
+    assert beq(got.result, ref.result)
+    assert (got.density_a, got.density_b, got.nnz_a, got.nnz_b) == (ref.density_a, ref.density_b, ref.nnz_a,
+                                                                     ref.nnz_b)
