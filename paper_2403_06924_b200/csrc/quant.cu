@@ -706,6 +706,43 @@ __device__ __forceinline__ uint32_t qn(float x, float lam32, float& dmax) {
     return __float_as_uint(u);
 }
 __device__ __forceinline__ uint32_t ubits(int q) { return (uint32_t)(q + 0x4B400000); }
+
+// The same for 4 values with packed fp32x2 FMA/SUB (FFMA2 / FADD2: two IEEE
+// round-to-nearest operations per instruction, results identical to qn's):
+// u = RN(x*lam32 + magic), d = RN(x*lam32 + (magic - u)).
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ void qn4(const float (&x)[4], float lam32, uint32_t (&u)[4], float& dmax) {
+    const uint64_t L = pk2(lam32, lam32), MG = pk2(kMagic, kMagic);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const uint64_t X = pk2(x[2 * p], x[2 * p + 1]);
+        const uint64_t U = fma2(X, L, MG);
+        const uint64_t D = fma2(X, L, sub2(MG, U));
+        float u0, u1, d0, d1;
+        upk2(U, u0, u1);
+        upk2(D, d0, d1);
+        u[2 * p] = __float_as_uint(u0);
+        u[2 * p + 1] = __float_as_uint(u1);
+        dmax = fmax_nan(fmax_nan(dmax, fabsf(d0)), fabsf(d1));
+    }
+}
 __device__ __forceinline__ uint32_t pack4u(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
@@ -787,14 +824,14 @@ __device__ __forceinline__ void select_quad_n(const float (&x)[4], uint32_t lut_
                                               unsigned& cnt, float& lmax) {
     uint32_t u[4], ur[4];
     float dmax = 0.0f;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) u[e] = qn(x[e], lam32, dmax);
+    qn4(x, lam32, u, dmax);
     float res[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-        res[e] = __fsub_rn(x[e], lut_at<SHIFT>(u[e], lut_adj));
-        ur[e] = qn(res[e], lam_r32, dmax);
-    }
+    for (int p = 0; p < 2; ++p)  // residual x - deq(q), two per FADD2
+        upk2(sub2(pk2(x[2 * p], x[2 * p + 1]),
+                  pk2(lut_at<SHIFT>(u[2 * p], lut_adj), lut_at<SHIFT>(u[2 * p + 1], lut_adj))),
+             res[2 * p], res[2 * p + 1]);
+    qn4(res, lam_r32, ur, dmax);
     if (exact || !(dmax < 0.4999f)) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -1147,7 +1184,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_quant_rows_r4(const QuantRowsArgs
             uint32_t u[4];
             float dmax = 0.0f;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) u[e] = qn(x[e], lam32, dmax);
+            qn4(x, lam32, u, dmax);
             if (exact || !(dmax < 0.4999f)) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(x[e], lam, qmaxf, kNearest));
@@ -1296,8 +1333,7 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
                 } else {
                     uint32_t u[4];
                     float dmax = 0.0f;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) u[e] = qn(xq[e], lam32, dmax);
+                    qn4(xq, lam32, u, dmax);
                     if (exact || !(dmax < 0.4999f)) {
 #pragma unroll
                         for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(xq[e], lam, qmaxf, kNearest));
@@ -1508,8 +1544,7 @@ __global__ void __launch_bounds__(kWW * 32, 1)
                     const float xq[4] = {x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]};
                     uint32_t u[4];
                     float dmax = 0.0f;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) u[e] = qn(xq[e], lam32, dmax);
+                    qn4(xq, lam32, u, dmax);
                     if (exact || !(dmax < 0.4999f)) {
 #pragma unroll
                         for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(xq[e], lam, qmaxf, kNearest));
