@@ -678,6 +678,7 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * Cfg::ACC_COLS +
                                    half * (Cfg::BN / 2);
+            uint32_t acc2[2][CW];  // EPI_DF: the accumulator columns of a chunk pair
 #pragma unroll 1
             for (int i = 0; i < nchunk; ++i) {
                 const int c = rev ? nchunk - 1 - i : i;
@@ -701,6 +702,22 @@ __global__ void __launch_bounds__(384, 1)
                 if (NACC > 1) scw[32 + lane] = nrc1;
                 if (i + 1 < nchunk) col_rcp(rev ? c - 1 : c + 1, nrc0, nrc1);
                 uint32_t acc[NACC][CW];
+                if constexpr (EPI == EPI_DF && NACC == 1) {
+                    // two chunks per TMEM round trip (the D_F epilogue is latency-bound at K <= 4096):
+                    // the odd chunk's accumulator columns arrived with the even one's
+                    if ((i & 1) == 0) {
+                        tmem_ld_cols<CW>(tbase + c * CW, acc2[0]);
+                        if (i + 1 < nchunk) tmem_ld_cols<CW>(tbase + (c + 1) * CW, acc2[1]);
+                        tmem_ld_wait();
+                        if (i + 2 >= nchunk) {  // accumulator drained: hand TMEM back to the MMA early
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(tempty_leader0 + buf * 8);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < CW; ++j) acc[0][j] = (i & 1) ? acc2[1][j] : acc2[0][j];
+                } else {
 #pragma unroll
                 for (int a = 0; a < NACC; ++a) tmem_ld_cols<CW>(tbase + a * Cfg::BN + c * CW, acc[a]);
                 tmem_ld_wait();
@@ -708,6 +725,7 @@ __global__ void __launch_bounds__(384, 1)
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(tempty_leader0 + buf * 8);
+                }
                 }
                 if (args.debug & 4) continue;  // probe: TMEM drain only
                 if (resident) {  // term-0 result in place: its own store must have read it out
