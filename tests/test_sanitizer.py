@@ -68,7 +68,12 @@ def test_racecheck_only_tmem_alloc_slot(comp):
             block.append(ln)
     if block:
         bad.append(block)
+    # the allocator's write has no program counter (+0xffff...fe80 past the kernel or
+    # tmem_alloc2 symbol, depending on inlining); its readers are the tmem-slot loads
+    # of the GEMM kernels (tmem_alloc2 / common.cuh / k_gemm_i8_tc* frames)
     unexplained = [b for b in bad
-                   if not (b[0].find("+0xfffffffffffffe") >= 0 and all("tmem_alloc" in x for x in b[1:]))]
+                   if not (b[0].find("+0xfffffffffffffe") >= 0
+                           and ("tmem_alloc" in b[0] or "k_gemm_i8_tc" in b[0])
+                           and all(("tmem_alloc" in x or "common.cuh" in x or "k_gemm_i8_tc" in x) for x in b[1:]))]
     assert not unexplained, "\n".join("\n".join(b) for b in unexplained) + "\n" + out[-3000:]
     assert races is not None

@@ -19,12 +19,12 @@ if [[ $what == ncu || $what == all ]]; then
   T=$(python -c "import json;print(json.loads(open('$OUT/bench.json').read().strip().splitlines()[-1])['config']['threshold_M'])")
   echo "threshold $T"
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-      python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-accuracy --threshold $T > $OUT/ncu_launch_run.log 2>&1
+      python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-accuracy --no-configs --threshold $T > $OUT/ncu_launch_run.log 2>&1
   python tools/launches.py $OUT/launches.csv
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm_i8_tc2 -s 3 -c 3 \
-      -o $OUT/prof_gemm -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-accuracy --threshold $T > $OUT/ncu_gemm.log 2>&1
+      -o $OUT/prof_gemm -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-accuracy --no-configs --threshold $T > $OUT/ncu_gemm.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on \
       -k regex:"k_quant|k_select|k_stats|k_absmax|k_cols|k_fallback" -s 6 -c 6 \
-      -o $OUT/prof_mem -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-accuracy --threshold $T > $OUT/ncu_mem.log 2>&1
+      -o $OUT/prof_mem -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-accuracy --no-configs --threshold $T > $OUT/ncu_mem.log 2>&1
   ls -la $OUT
 fi
