@@ -174,3 +174,29 @@ def test_calibrate_eta_on_device():
     cal = xg.calibrate_eta(1024, xg.QuantBits.Int8, 3)
     assert 1.0 / 1024 <= cal.eta <= 1.0
     assert cal.gemm_ops_per_s > 1e14 and cal.spmm_macs_per_s > 1e11
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_csr_random_configs_vs_oracle(oracle, force, seed):
+    """Random small shapes and configurations (bits, rounding, scheme, policy, C,
+    alpha/beta) with the CSR compensation forced: equal to the oracle bit for bit
+    whenever the SparseResidual branch runs (the CSR build may fall back to the
+    masked-dense launch at high density; both are checked against the oracle)."""
+    rng = np.random.default_rng(500 + seed)
+    m, k, n = (int(v) for v in rng.integers(1, 400, size=3))
+    a = ol.random_dense(m, k, seed * 3 + 1, -4, 4)
+    b = ol.random_dense(k, n, seed * 3 + 2, -4, 4)
+    cm = ol.random_dense(m, n, seed + 9, -1, 1)
+    force(2)
+    for scheme in (0, 1):
+        for pol in (0, 1):
+            c = ol.cfg(bits=int(rng.choice([4, 8])), threshold=float(10 ** rng.uniform(-2.5, 0.3)),
+                       density_limit=float(rng.uniform(0.05, 1.0)), scheme=scheme, policy=pol,
+                       rounding=int(rng.integers(0, 2)))
+            rc, ref, orep = oracle.xigemm(a, b, c=cm, alpha=1.25, beta=-0.5, config=c)
+            assert rc == 0
+            rep = _run(a, b, cm, 1.25, -0.5, cfg_from(c))
+            assert beq(rep.result, ref), (m, k, n, scheme, pol)
+            assert (rep.density_a, rep.density_b, int(rep.path)) == (orep.density_a, orep.density_b, orep.path)
+            if int(rep.path) == 1:
+                assert rep.comp_kernel == 0
