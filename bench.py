@@ -717,8 +717,7 @@ def run_b200_sharded(args, world, rank, local):
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
-    L = xg.lib()
-    L.xg_launch_count(1)
+    sharded.launch_count(reset=True)
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -727,7 +726,7 @@ def run_b200_sharded(args, world, rank, local):
             rep = step()
         e1.record(stream)
         torch.cuda.synchronize()
-    launches = int(L.xg_launch_count(1))
+    launches = sharded.launch_count(reset=True)  # includes the kernels replayed in the shard's graph
     tt = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     ms = float(tt.item())
@@ -767,7 +766,7 @@ def run_b200_sharded(args, world, rank, local):
     # roofline of one rank's share: its M rows against the replicated B (the
     # B-side stages run on every rank: B_alg counts them once per rank)
     rf = roofline(m, n, k, rep.nnz_a // world, rep.nnz_b, ms * 1e-3)
-    peaks = measure_peaks(L)
+    peaks = measure_peaks(xg.lib())
     rm = roofline(m, n, k, rep.nnz_a // world, rep.nnz_b, ms * 1e-3, peaks["int8_ops"], peaks["hbm_Bps"],
                   peaks.get("idp4a_macs"))
     cpu = None

@@ -190,6 +190,19 @@ def _report(rep: XgReport, result) -> GemmReport:
                       rep.stats_fallbacks, rep.comp_kernel)  # comp_kernel: this rank's compensation kernel
 
 
+_replayed_launches = 0
+
+
+def launch_count(reset: bool = False) -> int:
+    """This library's kernel launches (xg_launch_count) plus those replayed inside
+    the shards' captured CUDA graphs (which the library does not see)."""
+    global _replayed_launches
+    n = int(lib().xg_launch_count(1 if reset else 0)) + _replayed_launches
+    if reset:
+        _replayed_launches = 0
+    return n
+
+
 def split_rows(m: int, nranks: int) -> list[int]:
     """Balanced contiguous row blocks (the first m % nranks ranks get one more)."""
     if m < nranks:
@@ -288,11 +301,15 @@ def xigemm_sharded(a_rows, b, c_rows=None, alpha: float = 1.0, beta: float = 0.0
         # second call of the same problem: capture the six stages and their NCCL
         # collectives once, replay from then on (one launch per call)
         g = torch.cuda.CUDAGraph()
+        n0 = lib().xg_launch_count(0)
         with torch.cuda.graph(g):
             run_protocol([sh], DistComm(group), world)
+        sh._graph_launches = int(lib().xg_launch_count(0) - n0)  # kernels inside the captured graph
         sh._graph = g
     if getattr(sh, "_graph", None) is not None:
         sh._graph.replay()
+        global _replayed_launches
+        _replayed_launches += sh._graph_launches
     else:
         run_protocol([sh], DistComm(group), world)
     sh._runs = runs + 1
