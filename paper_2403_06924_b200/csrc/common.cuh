@@ -260,6 +260,41 @@ __device__ __forceinline__ float dq_ff24c(int32_t p, float2 c, uint32_t& slowmas
     return f;
 }
 
+// Packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2 on sm_100a): two IEEE
+// round-to-nearest operations per instruction, each lane's result identical to
+// the scalar operation's (tools/microbench/f32x2_check.cu).  Caution: ptxas
+// contracts a packed mul feeding a packed add/sub into one FFMA2 even with .rn
+// (tools/microbench/dq2_check.cu), so a product must only ever reach an FMA as
+// its addend; the users here (quant.cu qn4) have no such pair.
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
 __device__ __forceinline__ float dq_ff24(int32_t p, float2 a, float2 b, uint32_t& slowmask,
                                          uint32_t bit) {
     return dq_ff24c(p, ff_mul(a, b), slowmask, bit);

@@ -710,24 +710,6 @@ __device__ __forceinline__ uint32_t ubits(int q) { return (uint32_t)(q + 0x4B400
 // The same for 4 values with packed fp32x2 FMA/SUB (FFMA2 / FADD2: two IEEE
 // round-to-nearest operations per instruction, results identical to qn's):
 // u = RN(x*lam32 + magic), d = RN(x*lam32 + (magic - u)).
-__device__ __forceinline__ uint64_t pk2(float a, float b) {
-    uint64_t r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void upk2(uint64_t r, float& a, float& b) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
-}
-__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
-    uint64_t r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
-    uint64_t r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
 __device__ __forceinline__ void qn4(const float (&x)[4], float lam32, uint32_t (&u)[4], float& dmax) {
     const uint64_t L = pk2(lam32, lam32), MG = pk2(kMagic, kMagic);
 #pragma unroll

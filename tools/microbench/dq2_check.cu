@@ -1,0 +1,90 @@
+// Probe: the exact epilogue dequantisation (common.cuh dq_ff24) written with
+// packed fp32x2 ops, two elements per instruction, against the scalar form on
+// random (p, la, lb).  variant 0 writes f = t1 + lo with t1 = pf*ch a packed
+// mul: ptxas contracts the pair into one FFMA2 even with .rn and the results
+// differ (~44% of elements); variant 1 keeps the product an FMA addend and is
+// exact.  Measured on B200: neither is faster than the scalar form in the GEMM
+// epilogues (profiles/README.md), so the library keeps the scalar one.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O2 -I ../../paper_2403_06924_b200/csrc dq2_check.cu -o dq2_check
+#include <cstdio>
+#include <cstdint>
+#include "common.cuh"
+using namespace xg;
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+template <int V>
+__device__ void dq_ff24x2(int32_t p0, int32_t p1, float2 a, float2 b0, float2 b1, float& f0, float& f1,
+                          uint32_t& slowmask, uint32_t bit0) {
+    const uint64_t Z = 0ull;
+    const uint64_t AX = pk2(a.x, a.x), AY = pk2(a.y, a.y), BX = pk2(b0.x, b1.x), BY = pk2(b0.y, b1.y);
+    const uint64_t CH = mul2(AX, BX);
+    const uint64_t CE = fma2(AX, BX, sub2(Z, CH));
+    const uint64_t CL = fma2(AX, BY, fma2(AY, BX, CE));
+    const float pf0 = __int2float_rn(p0), pf1 = __int2float_rn(p1);
+    const uint64_t PF = pk2(pf0, pf1);
+    const uint64_t T1 = mul2(PF, CH);
+    const uint64_t E1 = fma2(PF, CH, sub2(Z, T1));
+    const uint64_t LO = fma2(PF, CL, E1);
+    uint64_t F, R;
+    if (V == 0) {
+        F = add2(T1, LO);
+        R = add2(sub2(T1, F), LO);
+    } else {
+        F = fma2(LO, pk2(1.0f, 1.0f), T1);
+        R = add2(fma2(F, pk2(-1.0f, -1.0f), T1), LO);
+    }
+    float r0, r1;
+    upk2(F, f0, f1);
+    upk2(R, r0, r1);
+    const int e0 = (int)((__float_as_uint(f0) - 1u) & 0x7f800000u);
+    const int e1 = (int)((__float_as_uint(f1) - 1u) & 0x7f800000u);
+    const bool ok0 = fabsf(pf0) < 16777216.0f && fabsf(r0) <= __int_as_float(max(e0 - ((24 << 23) + 256), 0));
+    const bool ok1 = fabsf(pf1) < 16777216.0f && fabsf(r1) <= __int_as_float(max(e1 - ((24 << 23) + 256), 0));
+    slowmask |= (ok0 ? 0u : bit0) | (ok1 ? 0u : bit0 << 1);
+}
+template <int V>
+__global__ void k(int* bad, float* ex) {
+    uint32_t s = blockIdx.x * 977u + threadIdx.x * 131u + 7u;
+    for (int it = 0; it < 500; ++it) {
+        s = s * 1664525u + 1013904223u;
+        const int32_t p0 = (int32_t)(s % 200001) - 100000;
+        s = s * 1664525u + 1013904223u;
+        const int32_t p1 = (int32_t)(s % 200001) - 100000;
+        s = s * 1664525u + 1013904223u;
+        const double la = 127.0 / (0.5 + (s % 1000) * 0.01);
+        s = s * 1664525u + 1013904223u;
+        const double lb0 = 127.0 / (0.5 + (s % 1000) * 0.01);
+        s = s * 1664525u + 1013904223u;
+        const double lb1 = 127.0 / (0.5 + (s % 1000) * 0.01);
+        const float2 a = ff_recip(la), b0 = ff_recip(lb0), b1 = ff_recip(lb1);
+        uint32_t sm = 0, sm2 = 0;
+        const float f0 = dq_ff24(p0, a, b0, sm, 1u), f1 = dq_ff24(p1, a, b1, sm, 2u);
+        float g0, g1;
+        dq_ff24x2<V>(p0, p1, a, b0, b1, g0, g1, sm2, 1u);
+        if (__float_as_uint(f0) != __float_as_uint(g0) || __float_as_uint(f1) != __float_as_uint(g1) || sm != sm2) {
+            int i = atomicAdd(bad, 1);
+            if (i < 6) { float* x = ex + i * 10; x[0] = p0; x[1] = p1; x[2] = f0; x[3] = g0; x[4] = f1; x[5] = g1; x[6] = sm; x[7] = sm2; x[8] = (float)la; x[9] = (float)lb0; }
+        }
+    }
+}
+int main() {
+    int* bad; float* ex; cudaMalloc(&bad, 4); cudaMalloc(&ex, 60 * 4);
+    for (int v = 0; v < 2; ++v) {
+    cudaMemset(bad, 0, 4);
+    if (v == 0) k<0><<<148, 256>>>(bad, ex); else k<1><<<148, 256>>>(bad, ex);
+    cudaError_t e = cudaDeviceSynchronize();
+    printf("variant %d ", v);
+    int hb; float he[60]; cudaMemcpy(&hb, bad, 4, cudaMemcpyDeviceToHost); cudaMemcpy(he, ex, sizeof he, cudaMemcpyDeviceToHost);
+    printf("%s: %d mismatches of %d\n", cudaGetErrorString(e), hb, 148 * 256 * 500);
+    for (int i = 0; i < (hb < 6 ? hb : 6); ++i) { float* x = he + i * 10; printf("p=(%g,%g) f0 %.9g vs %.9g  f1 %.9g vs %.9g  sm %g vs %g  la %g lb0 %g\n", x[0],x[1],x[2],x[3],x[4],x[5],x[6],x[7],x[8],x[9]); }
+    }
+    return 0;
+}
