@@ -10,16 +10,6 @@
 #include <cstdint>
 #include "common.cuh"
 using namespace xg;
-__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
-    uint64_t r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
-    uint64_t r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
 template <int V>
 __device__ void dq_ff24x2(int32_t p0, int32_t p1, float2 a, float2 b0, float2 b1, float& f0, float& f1,
                           uint32_t& slowmask, uint32_t bit0) {
