@@ -1731,7 +1731,9 @@ void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
 struct ColW { int ww, slots, ctas; };
 ColW colw_shape() {
     static const ColW c = [] {
-        ColW d{16, 2, 1};
+        // 8 warps x 2 CTAs per SM since the strip-major item order (select-B at C3
+        // 111 -> 105 us, C4 -4 us, C2 +1 us against 16 x 1)
+        ColW d{8, 2, 2};
         if (const char* e = getenv("XG_COLW")) {
             ColW v{};
             if (sscanf(e, "%dx%dx%d", &v.ww, &v.slots, &v.ctas) == 3) d = v;
@@ -1761,7 +1763,7 @@ void launch_cols_any(const CUtensorMap& tm, const QuantColsArgs& qa, const Selec
     else if (c.ww == 24 && c.slots == 1 && c.ctas == 1) launch_cols_w<SELECT, 24, 1, 1>(tm, qa, sa, rows, cols, co_share, s);
     else if (c.ww == 16 && c.slots == 2 && c.ctas == 1) launch_cols_w<SELECT, 16, 2, 1>(tm, qa, sa, rows, cols, co_share, s);
     else if (c.ww == 4 && c.slots == 4 && c.ctas == 2) launch_cols_w<SELECT, 4, 4, 2>(tm, qa, sa, rows, cols, co_share, s);
-    else launch_cols_w<SELECT, 8, 2, 2>(tm, qa, sa, rows, cols, co_share, s);
+    else launch_cols_w<SELECT, 8, 2, 2>(tm, qa, sa, rows, cols, co_share, s);  // default
 }
 
 // Fused column maxima + quantisation (k_cols_maxq); false when the shape or
