@@ -1103,11 +1103,11 @@ __global__ void __launch_bounds__(kRT, MINB) k_select_rows_r4(const SelectArgs a
 
 // K1, A side: the row lives in registers (VPT float4 per thread), absmax ->
 // lambda -> table -> quantise -> residual max; two CTA barriers per row.
-template <int VPT, int MINB = 4>
-__global__ void __launch_bounds__(kRT, MINB) k_quant_rows_r4(const QuantRowsArgs a) {
+template <int VPT, int MINB = 4, int NT = kRT>
+__global__ void __launch_bounds__(NT, MINB) k_quant_rows_r4(const QuantRowsArgs a) {
     XG_PDL_WAIT();
     __shared__ float lut[2][256];
-    __shared__ float red[2][kRT / 32];
+    __shared__ float red[2][NT / 32];
     const int qmax = quant_max(a.bits);
     const float qmaxf = (float)qmax;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -1119,7 +1119,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_quant_rows_r4(const QuantRowsArgs
         float4 f[VPT];
 #pragma unroll
         for (int v = 0; v < VPT; ++v) {
-            const int c = (v * kRT + (int)threadIdx.x) * 4;
+            const int c = (v * NT + (int)threadIdx.x) * 4;
             f[v] = c < a.cols ? ld_stream(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         float m = 0.0f, sum = 0.0f;
@@ -1140,7 +1140,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_quant_rows_r4(const QuantRowsArgs
         if (l == 0) rb[w] = m;
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < kRT / 32; ++i) m = fmaxf(m, rb[i]);
+        for (int i = 0; i < NT / 32; ++i) m = fmaxf(m, rb[i]);
         bad |= m > FLT_MAX ? 1 : 0;
         gmax_acc = fmaxf(gmax_acc, m);
         double lam;
@@ -1161,7 +1161,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_quant_rows_r4(const QuantRowsArgs
         int8_t* qrow = a.q + (int64_t)r * a.ldq;
 #pragma unroll
         for (int v = 0; v < VPT; ++v) {
-            const int c = (v * kRT + (int)threadIdx.x) * 4;
+            const int c = (v * NT + (int)threadIdx.x) * 4;
             const float x[4] = {f[v].x, f[v].y, f[v].z, f[v].w};
             uint32_t u[4];
             float dmax = 0.0f;
@@ -1182,7 +1182,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_quant_rows_r4(const QuantRowsArgs
     if (l == 0) red[0][w] = rmax_acc;
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int i = 1; i < kRT / 32; ++i) rmax_acc = fmaxf(rmax_acc, red[0][i]);
+        for (int i = 1; i < NT / 32; ++i) rmax_acc = fmaxf(rmax_acc, red[0][i]);
         if (a.rmax) atomicMax(a.rmax, fbits(rmax_acc));
         if (a.gmax) atomicMax(a.gmax, fbits(gmax_acc));
     }
@@ -1702,6 +1702,17 @@ void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
         else if (vpt <= 4) k_quant_rows_r4<4><<<g, kRT, 0, s>>>(a);
         else if (vpt <= 8) k_quant_rows_r4<8><<<g, kRT, 0, s>>>(a);
         else k_quant_rows_r4<16><<<g, kRT, 0, s>>>(a);
+        return;
+    }
+    if (a.rounding == kNearest && aligned && a.cols > 8192 && a.cols <= 16384 && r4_enabled()) {
+        // K in (8192, 16384] (C5): the same register-resident row over 256 threads
+        static const int qctas = [] {
+            const char* e = getenv("XG_R4Q16");  // tuning aid: CTAs per SM
+            return e ? atoi(e) : 2;
+        }();
+        const int cap = kNumSMs * (a.co_share > 0 ? a.co_share : qctas);
+        const int g = a.rows < cap ? a.rows : cap;
+        k_quant_rows_r4<16, 2, 256><<<g, 256, 0, s>>>(a);
         return;
     }
     if (a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 16384 && async_enabled()) {
