@@ -220,19 +220,12 @@ Aux& aux_stream() {
 // A-side and B-side kernels of K1 and K3 on two streams (graph branches), each
 // with its full persistent grid, so the second side fills the SMs the first
 // one's tail frees: K1 203 -> 191 us at C3 (K3 unchanged).  XG_COSCHED=0
-// serialises them; XG_COSCHED=1 also splits the grids per SM (measured
-// slower: 220 -> 281 us for K1, 309 -> 454 us for K3).
+// serialises them (diagnostic).  Splitting the grids per SM between the two
+// sides measured slower (220 -> 281 us for K1, 309 -> 454 us for K3).
 bool coschedule_enabled() {
     static const bool on = [] {
         const char* e = getenv("XG_COSCHED");
         return !(e && *e == '0');
-    }();
-    return on;
-}
-bool coschedule_share() {
-    static const bool on = [] {
-        const char* e = getenv("XG_COSCHED");
-        return e && *e == '1';
     }();
     return on;
 }
@@ -275,7 +268,6 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
     qa.bits = bits; qa.rounding = rnd;
     qa.q = p.aq; qa.ldq = p.ldk;
     qa.rmax = &p.sc->maxRA; qa.nonfinite = &p.sc->nonfinite;
-    qa.co_share = co && coschedule_share() ? 2 : 0;
     if (p.vw) {
         qa.per_row = 1; qa.lam_out = p.la; qa.rcp_out = p.lar; qa.gmax = &p.sc->maxA;
     } else {
@@ -289,7 +281,6 @@ void quantize_operands(Pipe& p, const float* a, const float* b, int phases = 7) 
     qb.bits = bits; qb.rounding = rnd;
     qb.qT = p.bqT; qb.ldq = p.ldk; qb.rmax = &p.sc->maxRB;
     qb.nonfinite = &p.sc->nonfinite;
-    qb.co_share = co && coschedule_share() ? 1 : 0;
     if (p.vw) {
         qb.per_col = 1; qb.colmax = p.colmax; qb.lam_out = p.lb; qb.rcp_out = p.lbr;
         if (launch_quant_cols_fused(qb, &p.sc->maxB, &p.sc->nonfinite, sb)) {
@@ -389,10 +380,8 @@ void select_operands(Pipe& p, const float* a, const float* b, int reduce, const 
     {
     const bool co = coschedule_enabled();
     cudaStream_t s2 = co ? fork(p.s) : p.s;
-    sa.co_share = co && coschedule_share() ? 4 : 0;
     launch_select_rows(sa, p.s);
     check_launch("select A");
-    sb.co_share = co && coschedule_share() ? 1 : 0;
     launch_select_cols_T(sb, s2);
     check_launch("select B");
     if (co) join(p.s);
@@ -483,36 +472,20 @@ void gemm_comp(Pipe& p, float* out, const float* c, float alpha, float beta) {
         g.bmap[1][0] = 4; g.bmap[1][1] = 5;
         g.rs[1][0] = r2; g.rs[1][1] = r2;
         g.cs[1][0] = c2d; g.cs[1][1] = c2s;
-        static const bool split = [] {
-            const char* e = getenv("XG_COMP_SPLIT");
-            return e && *e == '1';
-        }();
-        if (!split) {  // one launch, both terms per tile (TMEM buffers alternate by term)
-            g.dual = 1;
-            g.stamp = p.stamp_comp;
-            if (p.report_dst) {
-                g.done = &p.sc->done;
-                g.rep_src = reinterpret_cast<const uint32_t*>(p.sc);
-                g.rep_dst = p.report_dst;
-                g.rep_words = (int)(sizeof(xg::DevScalars) / 4);
-            }
-            // two operand pairs live per tile: half the raster group of the single GEMM
-            // keeps more of them in L2 (measured at C3: 8 -> 0.712 ms, 16 -> 0.720, 4 -> 0.738)
-            g.group_m = 8;
-            gemm_i8(EPI_ACC, ops, isb, 6, g, p.s);
-            check_launch("gemm compensate");
-            return;
+        // one launch, both terms per tile (TMEM buffers alternate by term)
+        g.dual = 1;
+        g.stamp = p.stamp_comp;
+        if (p.report_dst) {
+            g.done = &p.sc->done;
+            g.rep_src = reinterpret_cast<const uint32_t*>(p.sc);
+            g.rep_dst = p.report_dst;
+            g.rep_words = (int)(sizeof(xg::DevScalars) / 4);
         }
-        g.finalize = 0;
+        // two operand pairs live per tile: half the raster group of the single GEMM
+        // keeps more of them in L2 (measured at C3: 8 -> 0.712 ms, 16 -> 0.720, 4 -> 0.738)
+        g.group_m = 8;
         gemm_i8(EPI_ACC, ops, isb, 6, g, p.s);
-        check_launch("gemm compensate dr1");
-        g.amap[0][0] = 3; g.amap[0][1] = 3;
-        g.bmap[0][0] = 4; g.bmap[0][1] = 5;
-        g.rs[0][0] = r2; g.rs[0][1] = r2;
-        g.cs[0][0] = c2d; g.cs[0][1] = c2s;
-        g.finalize = 1;
-        gemm_i8(EPI_ACC, ops, isb, 6, g, p.s);
-        check_launch("gemm compensate dr2");
+        check_launch("gemm compensate");
         return;
     }
     GemmArgs g{};
@@ -850,11 +823,7 @@ void capture_entry(GraphEntry& e) {
     // the report: written into the pinned buffer by the compensation GEMM when it
     // runs the pair kernel with its one-launch (dual) compensation, else copied
     uint32_t* rep_dev = nullptr;
-    static const bool split = [] {
-        const char* v = getenv("XG_COMP_SPLIT");
-        return v && *v == '1';
-    }();
-    if (xg::pair_gemm_used(e.key.M, e.key.N) && !split && !getenv("XG_GEMM_1CTA")) {
+    if (xg::pair_gemm_used(e.key.M, e.key.N) && !getenv("XG_GEMM_1CTA")) {
         void* dp = nullptr;
         if (cudaHostGetDevicePointer(&dp, e.host_sc, 0) == cudaSuccess) rep_dev = static_cast<uint32_t*>(dp);
         else cudaGetLastError();

@@ -67,7 +67,6 @@ struct QuantRowsArgs {
     uint32_t* gmax;         // atomicMax of max|x| (float bits), may be null
     uint32_t* rmax;         // atomicMax of max|x - deq| (float bits), may be null
     int* nonfinite;
-    int co_share;           // host-only: CTAs per SM when co-scheduled with the B side (0: all)
 };
 
 struct QuantColsArgs {
@@ -83,7 +82,6 @@ struct QuantColsArgs {
     int8_t* qT;              // [cols x ldq] transposed (K-major)
     int64_t ldq;
     uint32_t* rmax;
-    int co_share;            // host-only: CTAs per SM when co-scheduled with the A side (0: all)
     const int* nonfinite;    // see SelectArgs::nonfinite (set by the column absmax pass)
 };
 
@@ -109,7 +107,6 @@ struct SelectArgs {
     uint32_t* retmax;
     // fix-up mode: rewrite `red` with the retained-max scale when it differs
     int fix_mode;
-    int co_share;            // host-only: CTAs per SM when co-scheduled (0: all)
     // set by the K1 kernels when an input is not finite: the call will fail
     // (pipeline.cpp:50-52), so the table-driven kernels exit instead of
     // indexing their dequant tables with NaN bit patterns

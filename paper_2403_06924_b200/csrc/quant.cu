@@ -903,109 +903,9 @@ __global__ void __launch_bounds__(kThreads) k_quant_cols_T_fast(const QuantColsA
 }
 
 
-// ============================================================ async streaming
-// HBM-bound kernels fed by the copy engines: the next rows / tiles are already
-// in flight (cp.async.bulk / TMA into a shared-memory ring, completion on
-// mbarriers) while the CTA reduces and quantises the current one, so the load
-// latency overlaps the compute instead of alternating with it.
-constexpr int kRowSlots = 3;
-
-__device__ __forceinline__ void issue_row(float* slot, const float* src, uint32_t bytes, uint64_t* bar) {
-    mbar_expect_tx(bar, bytes);
-    bulk_load(slot, src, bytes, bar);
-}
-
-// K1, A side: per-row absmax -> lambda, quantise, residual max (Nearest).
-__global__ void __launch_bounds__(kThreads) k_quant_rows_async(const QuantRowsArgs a) {
-    XG_PDL_WAIT();
-    extern __shared__ float4 dyn_smem[];
-    float* ring = reinterpret_cast<float*>(dyn_smem);
-    __shared__ uint64_t full[kRowSlots];
-    __shared__ float lut[256];
-    __shared__ float red[kThreads / 32];
-    const int qmax = quant_max(a.bits);
-    const float qmaxf = (float)qmax;
-    const uint32_t adj = smem_u32(lut) + 4u * (uint32_t)qmax - 4u * 0x4B400000u;
-    const uint32_t bytes = (uint32_t)a.cols * 4u;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kRowSlots; ++i) mbar_init(&full[i], 1);
-        fence_mbar_init();
-        for (int i = 0; i < kRowSlots; ++i) {
-            const int r = blockIdx.x + i * gridDim.x;
-            if (r < a.rows) issue_row(ring + (size_t)i * a.cols, a.x + (int64_t)r * a.ld, bytes, &full[i]);
-        }
-    }
-    __syncthreads();
-    float rmax_acc = 0.0f, gmax_acc = 0.0f;
-    int bad = 0;
-    for (int it = 0;; ++it) {
-        const int r = blockIdx.x + it * gridDim.x;
-        if (r >= a.rows) break;
-        const int slot = it % kRowSlots;
-        const float* row = ring + (size_t)slot * a.cols;
-        mbar_wait(&full[slot], (it / kRowSlots) & 1);
-        float m = 0.0f, sum = 0.0f;
-        for (int c = threadIdx.x * 4; c < a.cols; c += kThreads * 4) {
-            const float4 f = *reinterpret_cast<const float4*>(row + c);
-            m = fmaxf(fmaxf(m, fabsf(f.x)), fmaxf(fmaxf(fabsf(f.y), fabsf(f.z)), fabsf(f.w)));
-            sum = __fadd_rn(sum, __fadd_rn(__fadd_rn(f.x, f.y), __fadd_rn(f.z, f.w)));
-        }
-        const bool odd = !(fabsf(sum) <= FLT_MAX);
-        if (odd)
-            for (int c = threadIdx.x; c < a.cols; c += kThreads) bad |= fabsf(row[c]) <= FLT_MAX ? 0 : 2;
-        m = block_max(m, red);
-        bad |= m > FLT_MAX ? 1 : 0;
-        gmax_acc = fmaxf(gmax_acc, m);
-        double lam;
-        if (a.per_row) {
-            lam = compute_scale((double)m, a.bits);
-            if (threadIdx.x == 0 && a.lam_out) a.lam_out[r] = lam;
-            if (threadIdx.x == 0 && a.rcp_out) a.rcp_out[r] = ff_recip(lam);
-        } else {
-            lam = compute_scale((double)__uint_as_float(*a.tensor_max), a.bits);
-        }
-        const float lam32 = __double2float_rn(lam);
-        const bool exact = odd || !(lam32 <= FLT_MAX);
-        if (threadIdx.x <= 2 * qmax) lut[threadIdx.x] = dequant_value((int)threadIdx.x - qmax, lam);
-        __syncthreads();
-        float rm = 0.0f;
-        int8_t* qrow = a.q + (int64_t)r * a.ldq;
-        for (int c = threadIdx.x * 4; c < a.cols; c += kThreads * 4) {
-            const float4 f = *reinterpret_cast<const float4*>(row + c);
-            const float x[4] = {f.x, f.y, f.z, f.w};
-            uint32_t u[4];
-            float dmax = 0.0f;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) u[e] = qn(x[e], lam32, dmax);
-            if (exact || !(dmax < 0.4999f)) {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(x[e], lam, qmaxf, kNearest));
-            }
-#pragma unroll
-            for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[e], lut_at<2>(u[e], adj))));
-            *reinterpret_cast<uint32_t*>(qrow + c) = pack4u(u[0], u[1], u[2], u[3]);
-        }
-        rmax_acc = fmaxf(rmax_acc, rm);
-        __syncthreads();  // slot and lut free
-        if (threadIdx.x == 0) {
-            const int rn = blockIdx.x + (it + kRowSlots) * gridDim.x;
-            if (rn < a.rows) {
-                fence_proxy_async();
-                issue_row(ring + (size_t)slot * a.cols, a.x + (int64_t)rn * a.ld, bytes, &full[slot]);
-            }
-        }
-    }
-    rmax_acc = block_max(rmax_acc, red);
-    if (threadIdx.x == 0) {
-        if (a.rmax) atomicMax(a.rmax, fbits(rmax_acc));
-        if (a.gmax) atomicMax(a.gmax, fbits(gmax_acc));
-    }
-    if (bad && a.nonfinite) atomicOr(a.nonfinite, bad);
-}
-
 // ============================================================ row kernels, r4
-// One 128-thread CTA (4 warps) per row, 8 CTAs per SM.  Compared with the
-// 256-thread ring kernels above: one CTA barrier per row instead of three (the
+// One 128-thread CTA (4 warps) per row, 8 CTAs per SM.  Compared with a
+// 256-thread kernel staging rows through a cp.async.bulk shared-memory ring: one CTA barrier per row instead of three (the
 // dequant table is double-buffered, so building row i+1's table never waits
 // for row i's readers), plain 16-byte streaming loads issued U at a time per
 // lane for memory-level parallelism, and 7 rows per CTA so the static
@@ -1638,29 +1538,6 @@ void set_dyn_smem(K kern, int bytes) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-bool async_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("XG_NO_ASYNC");
-        return !(e && *e == '1');
-    }();
-    return on;
-}
-
-bool r4_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("XG_NO_R4");
-        return !(e && *e == '1');
-    }();
-    return on;
-}
-
-// persistent grid: as many CTAs as fit (by shared memory) on every SM
-int async_grid(int rows, int smem_bytes) {
-    const int per_sm = smem_bytes <= 70 * 1024 ? 3 : smem_bytes <= 105 * 1024 ? 2 : 1;
-    const int g = kNumSMs * per_sm;
-    return rows < g ? rows : g;
-}
-
 // ----------------------------------------------------------------- launches --
 void launch_absmax_global(const float* x, int64_t n, uint32_t* gmax, int* nonfinite,
                           cudaStream_t s) {
@@ -1690,13 +1567,9 @@ void quant_rows_rnd(const QuantRowsArgs& a, cudaStream_t s) {
 void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
     const bool aligned = (a.ld % 4 == 0) && (a.ldq % 4 == 0) && (a.cols % 4 == 0) &&
                          ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
-    if (a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 8192 && r4_enabled()) {
+    if (a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 8192) {
         const int vpt = (a.cols + kRT * 4 - 1) / (kRT * 4);
-        static const int qctas = [] {
-            const char* e = getenv("XG_R4Q");  // tuning aid: CTAs per SM
-            return e ? atoi(e) : 4;
-        }();
-        const int cap = kNumSMs * (a.co_share > 0 ? a.co_share : qctas);
+        const int cap = kNumSMs * 4;
         const int g = a.rows < cap ? a.rows : cap;
         if (vpt <= 2) k_quant_rows_r4<2><<<g, kRT, 0, s>>>(a);
         else if (vpt <= 4) k_quant_rows_r4<4><<<g, kRT, 0, s>>>(a);
@@ -1704,21 +1577,11 @@ void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
         else k_quant_rows_r4<16><<<g, kRT, 0, s>>>(a);
         return;
     }
-    if (a.rounding == kNearest && aligned && a.cols > 8192 && a.cols <= 16384 && r4_enabled()) {
+    if (a.rounding == kNearest && aligned && a.cols > 8192 && a.cols <= 16384) {
         // K in (8192, 16384] (C5): the same register-resident row over 256 threads
-        static const int qctas = [] {
-            const char* e = getenv("XG_R4Q16");  // tuning aid: CTAs per SM
-            return e ? atoi(e) : 2;
-        }();
-        const int cap = kNumSMs * (a.co_share > 0 ? a.co_share : qctas);
+        const int cap = kNumSMs * 2;
         const int g = a.rows < cap ? a.rows : cap;
         k_quant_rows_r4<16, 2, 256><<<g, 256, 0, s>>>(a);
-        return;
-    }
-    if (a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 16384 && async_enabled()) {
-        const int bytes = kRowSlots * a.cols * 4;
-        set_dyn_smem(k_quant_rows_async, bytes);
-        k_quant_rows_async<<<async_grid(a.rows, bytes), kThreads, bytes, s>>>(a);
         return;
     }
     if (a.rounding == kNearest) {
@@ -1737,49 +1600,30 @@ void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
 
 
 
-// Column-kernel shape (warps per CTA, ring slots per warp, CTAs per SM);
-// XG_COLW=WWxSLOTSxCTAS picks a compiled variant (tuning aid).
-struct ColW { int ww, slots, ctas; };
-ColW colw_shape() {
-    static const ColW c = [] {
-        // 8 warps x 2 CTAs per SM since the strip-major item order (select-B at C3
-        // 111 -> 105 us, C4 -4 us, C2 +1 us against 16 x 1)
-        ColW d{8, 2, 2};
-        if (const char* e = getenv("XG_COLW")) {
-            ColW v{};
-            if (sscanf(e, "%dx%dx%d", &v.ww, &v.slots, &v.ctas) == 3) d = v;
-        }
-        return d;
-    }();
-    return c;
-}
-
 template <bool SELECT, int WW, int SLOTS, int CTAS>
 void launch_cols_w(const CUtensorMap& tm, const QuantColsArgs& qa, const SelectArgs& sa, int rows, int cols,
-                   int co_share, cudaStream_t s) {
+                   cudaStream_t s) {
     constexpr int smem = col_w_smem<WW, SLOTS>();
     // no stage-dump bitmask: the variant without the per-quad check
     auto kern = (SELECT && !sa.keep) ? k_cols_w4<SELECT, WW, SLOTS, CTAS, false> : k_cols_w4<SELECT, WW, SLOTS, CTAS>;
     set_dyn_smem(kern, smem);
     const int items = ((cols + kWC - 1) / kWC) * ((rows + WW * kWR * kWSub - 1) / (WW * kWR * kWSub));
-    const int cap = kNumSMs * (co_share > 0 ? co_share : CTAS);
+    const int cap = kNumSMs * CTAS;
     kern<<<items < cap ? items : cap, WW * 32, smem, s>>>(tm, qa, sa);
 }
 
+// Column-kernel shape: 8 warps x 2 ring slots per warp x 2 CTAs per SM since the
+// strip-major item order (select-B at C3 111 -> 105 us, C4 -4 us, C2 +1 us
+// against 16 x 2 x 1; 12x1x2, 24x1x1 and 4x4x2 measured slower, profiles/README.md)
 template <bool SELECT>
 void launch_cols_any(const CUtensorMap& tm, const QuantColsArgs& qa, const SelectArgs& sa, int rows, int cols,
-                     int co_share, cudaStream_t s) {
-    const ColW c = colw_shape();
-    if (c.ww == 12 && c.slots == 1 && c.ctas == 2) launch_cols_w<SELECT, 12, 1, 2>(tm, qa, sa, rows, cols, co_share, s);
-    else if (c.ww == 24 && c.slots == 1 && c.ctas == 1) launch_cols_w<SELECT, 24, 1, 1>(tm, qa, sa, rows, cols, co_share, s);
-    else if (c.ww == 16 && c.slots == 2 && c.ctas == 1) launch_cols_w<SELECT, 16, 2, 1>(tm, qa, sa, rows, cols, co_share, s);
-    else if (c.ww == 4 && c.slots == 4 && c.ctas == 2) launch_cols_w<SELECT, 4, 4, 2>(tm, qa, sa, rows, cols, co_share, s);
-    else launch_cols_w<SELECT, 8, 2, 2>(tm, qa, sa, rows, cols, co_share, s);  // default
+                     cudaStream_t s) {
+    launch_cols_w<SELECT, 8, 2, 2>(tm, qa, sa, rows, cols, s);
 }
 
 // Fused column maxima + quantisation (k_cols_maxq); false when the shape or
-// options need the two-kernel path.  XG_COLS_FUSED=0 disables it; =WWxSLOTSxSUB
-// picks a compiled shape (warps, ring slots per warp, sub-tiles per warp).
+// options need the two-kernel path.  Launched as 16 warps x 2 ring slots x 4
+// sub-tiles per warp (8x4x8, 12x3x4 and 8x6x8 measured slower).
 template <int WW, int SLOTS, int SUB>
 bool launch_cols_maxq(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cudaStream_t s) {
     constexpr int rows_cta = WW * kWR * SUB;
@@ -1787,11 +1631,7 @@ bool launch_cols_maxq(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cu
     // K <= 8192 (clusters of <= 4): measured 1-5% faster end to end than the two
     // kernels at C2-C4; 8-CTA clusters (K = 16384) co-schedule worse with the
     // A side and measured ~1% slower, so larger K keeps the two-kernel path
-    static const int maxc = [] {  // tuning aid: XG_COLS_FUSED_MAXC (largest cluster used)
-        const char* e = getenv("XG_COLS_FUSED_MAXC");
-        return e ? atoi(e) : 4;
-    }();
-    if (csize > maxc || csize > 8) return false;
+    if (csize > 4) return false;
     alignas(64) CUtensorMap tm;
     if (!make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) return false;
     constexpr int smem = col_w_smem<WW, SLOTS>();
@@ -1825,27 +1665,15 @@ bool launch_cols_maxq(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cu
 }
 
 bool launch_quant_cols_fused(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cudaStream_t s) {
-    static const int3 shape = [] {
-        int3 v = make_int3(16, 2, 4);
-        if (const char* e = getenv("XG_COLS_FUSED")) {
-            if (*e == '0') v = make_int3(0, 0, 0);
-            else sscanf(e, "%dx%dx%d", &v.x, &v.y, &v.z);
-        }
-        return v;
-    }();
-    if (!shape.x || !a.per_col || a.rounding != kNearest || !r4_enabled() || a.rows < 256 || (a.ldq % 16) != 0)
-        return false;
-    if (shape.x == 8 && shape.y == 4 && shape.z == 8) return launch_cols_maxq<8, 4, 8>(a, gmax, nonfinite, s);
-    if (shape.x == 12 && shape.y == 3 && shape.z == 4) return launch_cols_maxq<12, 3, 4>(a, gmax, nonfinite, s);
-    if (shape.x == 8 && shape.y == 6 && shape.z == 8) return launch_cols_maxq<8, 6, 8>(a, gmax, nonfinite, s);
+    if (!a.per_col || a.rounding != kNearest || a.rows < 256 || (a.ldq % 16) != 0) return false;
     return launch_cols_maxq<16, 2, 4>(a, gmax, nonfinite, s);
 }
 
 void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {
-    if (a.rounding == kNearest && r4_enabled() && a.rows >= 256 && (a.ldq % 16) == 0) {
+    if (a.rounding == kNearest && a.rows >= 256 && (a.ldq % 16) == 0) {
         alignas(64) CUtensorMap tm;
         if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) {
-            launch_cols_any<false>(tm, a, SelectArgs{}, a.rows, a.cols, a.co_share, s);
+            launch_cols_any<false>(tm, a, SelectArgs{}, a.rows, a.cols, s);
             return;
         }
     }
@@ -1862,19 +1690,11 @@ void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {
 void launch_select_rows(const SelectArgs& a, cudaStream_t s) {
     const bool aligned = (a.ld % 4 == 0) && (a.ldq % 4 == 0) && (a.cols % 4 == 0) &&
                          ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
-    if (!a.fix_mode && a.rounding == kNearest && aligned && a.cols >= 512 && r4_enabled()) {
-        // XG_R4SEL=UxCTAS tuning aid (U loads in flight per thread, CTAs per SM)
-        static const int2 cfg = [] {
-            int2 c = make_int2(4, kRCtasPerSM);
-            if (const char* e = getenv("XG_R4SEL")) sscanf(e, "%dx%d", &c.x, &c.y);
-            return c;
-        }();
-        const int cap = kNumSMs * (a.co_share > 0 ? a.co_share : cfg.y);
+    if (!a.fix_mode && a.rounding == kNearest && aligned && a.cols >= 512) {
+        // 4 loads in flight per thread, kRCtasPerSM CTAs per SM (2x8, 8x6 and 4x12 measured slower)
+        const int cap = kNumSMs * kRCtasPerSM;
         const int g = a.rows < cap ? a.rows : cap;
-        if (cfg.x == 2) k_select_rows_r4<2, 8><<<g, kRT, 0, s>>>(a);
-        else if (cfg.x == 8) k_select_rows_r4<8, 6><<<g, kRT, 0, s>>>(a);
-        else if (cfg.y >= 12) k_select_rows_r4<4, 12><<<g, kRT, 0, s>>>(a);
-        else if (a.keep) k_select_rows_r4<4><<<g, kRT, 0, s>>>(a);
+        if (a.keep) k_select_rows_r4<4><<<g, kRT, 0, s>>>(a);
         else k_select_rows_r4<4, kRCtasPerSM, false><<<g, kRT, 0, s>>>(a);  // no stage-dump bitmask
         return;
     }
@@ -1888,10 +1708,10 @@ void launch_select_cols_T(const SelectArgs& a, cudaStream_t s) {
         k_fix_cols_T<<<grid_rows(a.cols), kThreads, 0, s>>>(a);
         return;
     }
-    if (a.rounding == kNearest && r4_enabled() && a.rows >= 256 && (a.ldq % 16) == 0) {
+    if (a.rounding == kNearest && a.rows >= 256 && (a.ldq % 16) == 0) {
         alignas(64) CUtensorMap tm;
         if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) {
-            launch_cols_any<true>(tm, QuantColsArgs{}, a, a.rows, a.cols, a.co_share, s);
+            launch_cols_any<true>(tm, QuantColsArgs{}, a, a.rows, a.cols, s);
             return;
         }
     }
