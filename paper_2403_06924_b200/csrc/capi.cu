@@ -338,21 +338,7 @@ void quantize_b_vw(Pipe& p, const float* b) {
     check_launch("quantize B");
 }
 
-// Threshold statistics fused into the D_F GEMM's epilogue (EPI_DF_AVG/MIN)
-// where the pair kernel runs and K is long enough for the epilogue to hide
-// under the MMA (at K = 4096 it already bounds the tile).
-constexpr int kStatsFuseMinK = 8192;
-bool stats_fused(int M, int N, int K) { return K >= kStatsFuseMinK && xg::pair_gemm_used(M, N); }
-
-struct StatsOut {  // accumulators of the fused statistics (policy < 0: none)
-    int policy = -1;
-    double* row_sum = nullptr;
-    double* col_sum = nullptr;
-    float* row_stat = nullptr;
-    float* col_stat = nullptr;
-};
-
-void gemm_df(Pipe& p, float* out, const StatsOut& st = StatsOut{}) {
+void gemm_df(Pipe& p, float* out) {
     using namespace xg;
     KOperand ops[2] = {{p.aq, p.M, p.ldk}, {p.bqT, p.N, p.ldk}};
     int isb[2] = {0, 1};
@@ -364,17 +350,7 @@ void gemm_df(Pipe& p, float* out, const StatsOut& st = StatsOut{}) {
     g.stamp = p.stamp_df;
     g.rs[0][0] = g.rs[0][1] = p.vw ? sref(p.la, 1, p.lar) : sref(&p.sc->lamA, 0, &p.sc->rA);
     g.cs[0][0] = g.cs[0][1] = p.vw ? sref(p.lb, 1, p.lbr) : sref(&p.sc->lamB, 0, &p.sc->rB);
-    int epi = EPI_DF;
-    if (st.policy == XG_AVG_RULE) {
-        epi = EPI_DF_AVG;
-        g.row_sum = st.row_sum;
-        g.col_sum = st.col_sum;
-    } else if (st.policy >= 0) {  // MinRule: the float bit patterns order like uints (stats.cu)
-        epi = EPI_DF_MIN;
-        g.row_min = reinterpret_cast<uint32_t*>(st.row_stat);
-        g.col_min = reinterpret_cast<uint32_t*>(st.col_stat);
-    }
-    gemm_i8(epi, ops, isb, 2, g, p.s);
+    gemm_i8(EPI_DF, ops, isb, 2, g, p.s);
     check_launch("gemm D_F");
 }
 
@@ -681,13 +657,7 @@ int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* du
         }
         quantize_operands(p, q.a, q.b);
     } else if (stage == 1) {
-        StatsOut st;
-        if (q.reduce && stats_fused(M, N, K)) {  // accumulators initialised by stage 0
-            st.policy = q.cfg.policy;
-            st.row_sum = w.rsum; st.col_sum = w.csum;
-            st.row_stat = w.rstat; st.col_stat = w.cstat;
-        }
-        gemm_df(p, q.out, st);
+        gemm_df(p, q.out);
         if (dump && dump->d_f)
             ck(cudaMemcpyAsync(dump->d_f, q.out, sizeof(float) * (size_t)M * N, cudaMemcpyDeviceToDevice, s), "dump");
     } else if (stage == 2) {
@@ -699,13 +669,11 @@ int64_t enqueue_stage(int stage, const PipeCall& q, const PipeWs& w, xg_dump* du
                 return e ? atoi(e) : 0;
             }();
             const xg::StatsDefer def{q.a, K, q.b, N, K, q.cfg.threshold, widen};
-            // accumulators were initialised by stage 0 (launch_pipe_init); the
-            // partial pass ran in the D_F GEMM's epilogue when stats_fused()
-            if (!stats_fused(M, N, K))
-                xg::launch_stats_partial(q.out, M, N, q.cfg.policy, w.rstat, w.cstat, w.rsum, w.csum, &p.sc->nflag, s, 2);
+            // accumulators were initialised by stage 0 (launch_pipe_init)
+            xg::launch_stats_partial(q.out, M, N, q.cfg.policy, w.rstat, w.cstat, w.rsum, w.csum, &p.sc->nflag, s, 2);
             xg::launch_stats_final(q.out, M, N, M, q.cfg.policy, w.rstat, w.cstat, w.rsum, w.csum, w.flags,
                                    &p.sc->nflag, s, dump ? nullptr : &def);
-            check_launch("stats", (stats_fused(M, N, K) ? 0 : 1) + (q.cfg.policy == XG_AVG_RULE ? 2 : 0));
+            check_launch("stats", q.cfg.policy == XG_AVG_RULE ? 3 : 1);
         }
         if (dump && q.reduce) {  // kept-element bitmasks, OR-ed in by the selection kernels
             const size_t kw = (size_t)(K + 31) / 32;

@@ -178,12 +178,10 @@ bool make_tmap_f32(void* tmap, const float* p, int rows, int cols, int64_t ld, i
 void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const GemmArgs& args,
              cudaStream_t s) {
     // the pair kernel's TMA-store epilogue needs 16-byte row pitch for the fp32 maps
-    if (use_pair_kernel(args) && (epi_df(epi) || epi == EPI_COMP || epi == EPI_ACC) && (args.N % 4) == 0) {
+    if (use_pair_kernel(args) && (epi == EPI_DF || epi == EPI_COMP || epi == EPI_ACC) && (args.N % 4) == 0) {
         const bool mc = pair_count(args) == 2;
         switch (epi) {
             case EPI_DF: mc ? run2<1, EPI_DF, 2>(ops, is_b, nops, args, s) : run2<1, EPI_DF, 1>(ops, is_b, nops, args, s); return;
-            case EPI_DF_AVG: run2<1, EPI_DF_AVG, 1>(ops, is_b, nops, args, s); return;
-            case EPI_DF_MIN: run2<1, EPI_DF_MIN, 1>(ops, is_b, nops, args, s); return;
             case EPI_COMP: mc ? run2<2, EPI_COMP, 2>(ops, is_b, nops, args, s) : run2<2, EPI_COMP, 1>(ops, is_b, nops, args, s); return;
             case EPI_ACC:  // K <= 4096: the epilogue bounds the tile - deeper D_F prefetch, 5 stages
                 if (args.K <= 4096) run2<1, EPI_ACC, 1, 5>(ops, is_b, nops, args, s);
@@ -196,9 +194,7 @@ void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const Gemm
         case EPI_DF: run<256, 1, EPI_DF>(ops, is_b, nops, args, s); break;
         case EPI_COMP: run<128, 2, EPI_COMP>(ops, is_b, nops, args, s); break;
         case EPI_FULL3: run<128, 3, EPI_FULL3>(ops, is_b, nops, args, s); break;
-        case EPI_ACC:
-        case EPI_DF_AVG:
-        case EPI_DF_MIN: throw std::invalid_argument("gemm_i8: epilogue needs the pair kernel");
+        case EPI_ACC: throw std::invalid_argument("gemm_i8: EPI_ACC needs the pair kernel");
         default: throw std::invalid_argument("gemm_i8: bad epilogue");
     }
 }

@@ -17,8 +17,6 @@
 
 #include <cuda.h>
 
-#include <cfloat>
-
 #include "common.cuh"
 
 namespace xg {
@@ -28,13 +26,8 @@ enum EpiMode : int {
     EPI_DF = 1,    // store float(acc / (la_i * lb_j))
     EPI_COMP = 2,  // store ((D_F + float(acc0/(l1_i*l2_j))) + float(acc1/(l3_i*l4_j))), alpha/beta
     EPI_FULL3 = 3, // full residual: ((float(acc0/s0) + float(acc1/s1)) + float(acc2/s2))
-    EPI_ACC = 4,   // out = float(din + float(acc/(l_i*l_j))), then alpha/beta if `finalize`
-    // EPI_DF plus the threshold statistics of |D_F| (pipeline.cpp:215-247) from
-    // the values in registers, so no pass re-reads D_F (pair kernel only):
-    EPI_DF_AVG = 5,  // fp64 row / column sums of |D_F| (AvgRule) into row_sum / col_sum
-    EPI_DF_MIN = 6   // row / column minima of |D_F| (MinRule), float bits into row_min / col_min
+    EPI_ACC = 4    // out = float(din + float(acc/(l_i*l_j))), then alpha/beta if `finalize`
 };
-constexpr bool epi_df(int e) { return e == EPI_DF || e == EPI_DF_AVG || e == EPI_DF_MIN; }
 
 struct ScaleRef {  // per-row (stride 1) or per-tensor (stride 0) fp64 scales
     const double* p;
@@ -89,11 +82,6 @@ struct GemmArgs {
     const uint32_t* rep_src;
     uint32_t* rep_dst;
     int rep_words;
-    // EPI_DF_AVG / EPI_DF_MIN: statistics accumulators (initialised by the caller)
-    double* row_sum;
-    double* col_sum;
-    uint32_t* row_min;
-    uint32_t* col_min;
 };
 
 template <int BN, int NACC>
@@ -405,69 +393,6 @@ namespace xg {
 // (128+256) for the 1-CTA 128x256 tile: 64 B/clk/SM at full MMA rate.  The
 // accumulator rows 0-127 land in the leader's TMEM, 128-255 in the peer's.
 // 8 epilogue warps (two per TMEM lane quadrant, one per 128-column half).
-// Threshold statistics of one 32-row x 16-column chunk of D_F held one row per
-// lane (res[j] = column col0 + j): the row's partial (sum or min) accumulates in
-// the lane, the column partials over the warp's 32 rows are reduced by a
-// transposing butterfly (each exchange halves the columns a lane keeps) and
-// added to the global accumulators by the even lanes.  AvgRule sums |x| in fp64
-// in a tree order: the verified-mean bound of stats.cu covers any order.
-template <int EPI>
-__device__ __forceinline__ void tile_stats(const GemmArgs& args, const float (&res)[16], bool row_ok, int col0,
-                                           int lane, double& rs, float& rm) {
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-    const int cj = (b4 ? 8 : 0) + (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
-    const int nv = row_ok ? min(16, args.N - col0) : 0;  // valid columns of this row
-    if constexpr (EPI == EPI_DF_AVG) {
-        double v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = j < nv ? fabs((double)res[j]) : 0.0;
-        double e0 = 0.0, e1 = 0.0;
-#pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-            e0 = __dadd_rn(e0, v[j]);
-            e1 = __dadd_rn(e1, v[j + 1]);
-        }
-        rs = __dadd_rn(rs, __dadd_rn(e0, e1));
-        double w8[8], w4[4], w2[2];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            w8[k] = __dadd_rn(b4 ? v[k + 8] : v[k], __shfl_xor_sync(0xffffffffu, b4 ? v[k] : v[k + 8], 16));
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            w4[k] = __dadd_rn(b3 ? w8[k + 4] : w8[k], __shfl_xor_sync(0xffffffffu, b3 ? w8[k] : w8[k + 4], 8));
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-            w2[k] = __dadd_rn(b2 ? w4[k + 2] : w4[k], __shfl_xor_sync(0xffffffffu, b2 ? w4[k] : w4[k + 2], 4));
-        double w1 = __dadd_rn(b1 ? w2[1] : w2[0], __shfl_xor_sync(0xffffffffu, b1 ? w2[0] : w2[1], 2));
-        w1 = __dadd_rn(w1, __shfl_xor_sync(0xffffffffu, w1, 1));
-        if (!(lane & 1) && col0 + cj < args.N) atomicAdd(args.col_sum + col0 + cj, w1);
-    } else {
-        float v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = j < nv ? fabsf(res[j]) : FLT_MAX;
-        float m0 = v[0], m1 = v[1];
-#pragma unroll
-        for (int j = 2; j < 16; j += 2) {
-            m0 = fminf(m0, v[j]);
-            m1 = fminf(m1, v[j + 1]);
-        }
-        rm = fminf(rm, fminf(m0, m1));
-        float w8[8], w4[4], w2[2];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            w8[k] = fminf(b4 ? v[k + 8] : v[k], __shfl_xor_sync(0xffffffffu, b4 ? v[k] : v[k + 8], 16));
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            w4[k] = fminf(b3 ? w8[k + 4] : w8[k], __shfl_xor_sync(0xffffffffu, b3 ? w8[k] : w8[k + 4], 8));
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-            w2[k] = fminf(b2 ? w4[k + 2] : w4[k], __shfl_xor_sync(0xffffffffu, b2 ? w4[k] : w4[k + 2], 4));
-        float w1 = fminf(b1 ? w2[1] : w2[0], __shfl_xor_sync(0xffffffffu, b1 ? w2[0] : w2[1], 2));
-        w1 = fminf(w1, __shfl_xor_sync(0xffffffffu, w1, 1));
-        if (!(lane & 1) && col0 + cj < args.N && w1 != FLT_MAX) atomicMin(args.col_min + col0 + cj, __float_as_uint(w1));
-    }
-}
-
 template <int NACC, int EPI = EPI_DF, int ST = 0>
 struct Gemm2Cfg {
     static constexpr int BM = 128;   // rows per CTA (pair M = 256)
@@ -487,7 +412,7 @@ struct Gemm2Cfg {
     // 32x16 tiles) for the compensation GEMM, whose smaller staging tiles leave
     // room for the sixth stage, and for the D_F GEMM (two tiles in the space of
     // one 32x32: stores overlap the next chunk); 32 (128B swizzle) for EPI_COMP
-    static constexpr int CHW = ((EPI == EPI_ACC && STAGES >= 5) || epi_df(EPI)) ? 16 : 32;
+    static constexpr int CHW = ((EPI == EPI_ACC && STAGES >= 5) || EPI == EPI_DF) ? 16 : 32;
     static constexpr int ACC_COLS = NACC * BN;
     static constexpr int ACC_BUFS = (512 / ACC_COLS) >= 2 ? 2 : 1;
     static constexpr int TMEM_COLS = 512;
@@ -754,8 +679,6 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + buf * Cfg::ACC_COLS +
                                    half * (Cfg::BN / 2);
             uint32_t acc2[2][CW];  // EPI_DF: the accumulator columns of a chunk pair
-            double st_rs = 0.0;     // EPI_DF_AVG: this row's partial sum over the tile half
-            float st_rm = FLT_MAX;  // EPI_DF_MIN: its partial minimum
 #pragma unroll 1
             for (int i = 0; i < nchunk; ++i) {
                 const int c = rev ? nchunk - 1 - i : i;
@@ -779,7 +702,7 @@ __global__ void __launch_bounds__(384, 1)
                 if (NACC > 1) scw[32 + lane] = nrc1;
                 if (i + 1 < nchunk) col_rcp(rev ? c - 1 : c + 1, nrc0, nrc1);
                 uint32_t acc[NACC][CW];
-                if constexpr (epi_df(EPI) && NACC == 1) {
+                if constexpr (EPI == EPI_DF && NACC == 1) {
                     // two chunks per TMEM round trip (the D_F epilogue is latency-bound at K <= 4096):
                     // the odd chunk's accumulator columns arrived with the even one's
                     if ((i & 1) == 0) {
@@ -819,7 +742,7 @@ __global__ void __launch_bounds__(384, 1)
                 __syncwarp();
                 float4* rowp = reinterpret_cast<float4*>(tile + lane * CW);
                 float res[CW];
-                if constexpr (epi_df(EPI)) {
+                if constexpr (EPI == EPI_DF) {
                     bool slow = false;
                     if (args.debug & 64) {  // probe: no dequant math
 #pragma unroll
@@ -840,7 +763,6 @@ __global__ void __launch_bounds__(384, 1)
                         }
                     }
                     (void)slow;
-                    if constexpr (EPI != EPI_DF) tile_stats<EPI>(args, res, row_ok, col0, lane, st_rs, st_rm);
                 } else if constexpr (EPI == EPI_ACC) {
                     // pipeline.cpp:141-145 one term at a time: out = fl(din + deq(acc)).
                     // In place over res[] (register budget: 168/thread); the rare
@@ -921,11 +843,6 @@ __global__ void __launch_bounds__(384, 1)
                     bulk_commit();
                 }
                 __syncwarp();
-            }
-            if constexpr (EPI == EPI_DF_AVG) {
-                if (row_ok && nchunk > 0) atomicAdd(args.row_sum + row, st_rs);
-            } else if constexpr (EPI == EPI_DF_MIN) {
-                if (row_ok && nchunk > 0) atomicMin(args.row_min + row, __float_as_uint(st_rm));
             }
             if (nchunk <= 0) {  // nothing to store (N edge / probe): still release the accumulator
                 tc_fence_before();
