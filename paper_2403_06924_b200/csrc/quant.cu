@@ -951,9 +951,31 @@ __global__ void __launch_bounds__(kRT, MINB) k_select_rows_r4(const SelectArgs a
     unsigned cnt = 0;
     float ret = 0.0f;
     int it = 0;
-    for (int r = blockIdx.x; r < a.rows; r += gridDim.x, ++it) {
-        const double lam = a.vec ? a.lam[r] : lam_t;
-        const float tf = a.do_select ? float_above(threshold_of(a.policy, a.thr_m, a.stat[r], so, a.cols))
+    // the row's scale and statistic are fetched one row ahead, and the row's first
+    // U loads are issued before its table is built: the per-row latency chain
+    // (scalar loads -> fp64 threshold and table -> barrier -> row loads) overlaps
+    int r = blockIdx.x;
+    double lam_n = 0.0;
+    float stat_n = 0.0f;
+    if (r < a.rows) {
+        lam_n = a.vec ? a.lam[r] : lam_t;
+        if (a.do_select) stat_n = a.stat[r];
+    }
+    for (; r < a.rows; r += gridDim.x, ++it) {
+        const float* row = a.x + (int64_t)r * a.ld;
+        float4 f[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c = threadIdx.x * 4 + u * kRT * 4;
+            f[u] = c < a.cols ? ld_stream(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        const double lam = lam_n;
+        const float stat = stat_n;
+        if (r + (int)gridDim.x < a.rows) {
+            lam_n = a.vec ? a.lam[r + gridDim.x] : lam_t;
+            if (a.do_select) stat_n = a.stat[r + gridDim.x];
+        }
+        const float tf = a.do_select ? float_above(threshold_of(a.policy, a.thr_m, stat, so, a.cols))
                                      : __int_as_float(0x7f800000);
         float* tb = lut[it & 1];
         build_row_lut(tb, lam, qmax);
@@ -961,16 +983,16 @@ __global__ void __launch_bounds__(kRT, MINB) k_select_rows_r4(const SelectArgs a
         const float lam32 = __double2float_rn(lam);
         const bool exact = !(lam32 <= FLT_MAX) || !(lam_r32 <= FLT_MAX);
         const uint32_t adj = smem_u32(tb) + 4u * (uint32_t)qmax - 4u * 0x4B400000u;
-        const float* row = a.x + (int64_t)r * a.ld;
         int8_t* rq_row = a.rq + (int64_t)r * a.ldq;
         int8_t* rd_row = a.red + (int64_t)r * a.ldq;
         float lmax = 0.0f;
         for (int c0 = threadIdx.x * 4; c0 < a.cols; c0 += kRT * 4 * U) {
-            float4 f[U];
+            if (c0 != (int)threadIdx.x * 4) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int c = c0 + u * kRT * 4;
-                f[u] = c < a.cols ? ld_stream(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int u = 0; u < U; ++u) {
+                    const int c = c0 + u * kRT * 4;
+                    f[u] = c < a.cols ? ld_stream(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -1109,7 +1131,10 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
     constexpr int kWItemRows = kWW * kWR * kWSub;
     XG_EXIT_IF_NONFINITE(SELECT ? sa.nonfinite : qa.nonfinite);
     extern __shared__ float4 dyn_smem[];
-    float* ring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(dyn_smem) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment by arithmetic on the shared array itself (a uintptr_t
+    // round trip makes the compiler emit generic LD for the tile reads, not LDS)
+    const uint32_t pad = (1024u - (smem_u32(dyn_smem) & 1023u)) & 1023u;
+    float* ring = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(dyn_smem) + pad);
     float(*lut)[kWC] = reinterpret_cast<float(*)[kWC]>(ring + kWW * kWSlots * kWC * kWR);
     __shared__ uint64_t full[kWW][kWSlots];
     __shared__ float redf[kWW];
