@@ -1112,15 +1112,19 @@ __global__ void __launch_bounds__(NT, MINB) k_quant_rows_r4(const QuantRowsArgs 
 }
 
 // ============================================================ column kernels, w4
-// B side (K x N row-major in, N x K K-major int8 out).  One 4-warp CTA works on
-// an item = 32-column strip x 1024 rows; each warp streams its own 256 rows as
-// 32 x 32 fp32 sub-tiles through a private 4-deep TMA ring (own mbarriers, no
-// CTA barrier inside the item).  Lane l owns column l: it reads its column of
-// the tile conflict-free, quantises 4 consecutive rows into one word, and
+// B side (K x N row-major in, N x K K-major int8 out).  A WW-warp CTA (8, two
+// CTAs per SM) works through a contiguous range of items in strip-major order,
+// an item = 32-column strip x WW * 32 * kWSub rows; each warp streams its 32 x
+// 32 fp32 sub-tiles through a private TMA ring of SLOTS slots (own mbarriers,
+// no CTA barrier inside an item).  Lane l owns column l: it reads its column
+// of the tile conflict-free, quantises 4 consecutive rows into one word, and
 // writes its 32 output bytes of row n of B^T itself (two 16-byte stores), so
 // no shared-memory transpose is needed.  The per-strip dequant tables
-// lut[q][lane] are built once per item (2 CTA barriers per item).
-constexpr int kWC = 32, kWR = 32, kWSub = 4;  // strip width, sub-tile rows, sub-tiles per warp per item
+// lut[q][lane] are built when the strip changes (2 CTA barriers).
+// strip width, sub-tile rows, sub-tiles per warp per item (1: items of 256 rows
+// balance the persistent grid at K = 4096: select-B stage 83 -> 80 us at C2,
+// 309 -> 304 us at C4, C3 unchanged; 2 and 4 measured no better)
+constexpr int kWC = 32, kWR = 32, kWSub = 1;
 template <int WW, int SLOTS>
 constexpr int col_w_smem() { return WW * SLOTS * kWC * kWR * 4 + 256 * kWC * 4 + 1024; }
 
