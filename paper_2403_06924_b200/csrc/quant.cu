@@ -1324,7 +1324,7 @@ __global__ void __launch_bounds__(kWW * 32, 1)
                                            ((1024u - (smem_u32(dyn_smem) & 1023u)) & 1023u));
     float(*lut)[kWC] = reinterpret_cast<float(*)[kWC]>(ring + kWW * kWSlots * kWC * kWR);
     __shared__ uint64_t full[kWW][kWSlots];
-    __shared__ uint32_t wmax[kWW][kWC];
+    __shared__ __align__(16) uint32_t wmax[kWW][kWC];
     __shared__ uint32_t cmax[3][kWC];  // cluster maxima per strip (rank 0's copy), 3-deep for the resets
     __shared__ float redf[kWW];
     const uint32_t crank = cluster_ctarank(), csize = cluster_nctarank();
@@ -1382,26 +1382,45 @@ __global__ void __launch_bounds__(kWW * 32, 1)
         }
         ++g;
     };
-    auto absmax_bits = [&](const float (&x)[kWR]) {
-        uint32_t m4[4] = {0u, 0u, 0u, 0u};
+    // pass 0: the sub-tile read as float4 (lane l: columns 4 (l % 8) .. +3 of rows
+    // l / 8 + 4 i, a quarter of the shared-memory loads of the column-per-lane read);
+    // um4 holds |x| bit maxima of those 4 columns until the strip's exchange
+    auto consume_max = [&](uint32_t (&m)[4]) {
+        const int slot = g % kWSlots;
+        mbar_wait(&full[w][slot], (g / kWSlots) & 1);
+        const float4* tile = reinterpret_cast<const float4*>(wring + slot * kWC * kWR);
+        float4 v[kWR / 4];
 #pragma unroll
-        for (int r = 0; r < kWR; ++r) m4[r & 3] = max(m4[r & 3], __float_as_uint(x[r]) & 0x7fffffffu);
-        return max(max(m4[0], m4[1]), max(m4[2], m4[3]));
+        for (int i = 0; i < kWR / 4; ++i) v[i] = tile[(lane >> 3) * (kWC / 4) + i * kWC + (lane & 7)];
+        __syncwarp();
+        if (lane == 0 && g + kWSlots < ntiles) {
+            fence_proxy_async();
+            issue(g + kWSlots);
+        }
+        ++g;
+#pragma unroll
+        for (int i = 0; i < kWR / 4; ++i) {
+            m[0] = max(m[0], __float_as_uint(v[i].x) & 0x7fffffffu);
+            m[1] = max(m[1], __float_as_uint(v[i].y) & 0x7fffffffu);
+            m[2] = max(m[2], __float_as_uint(v[i].z) & 0x7fffffffu);
+            m[3] = max(m[3], __float_as_uint(v[i].w) & 0x7fffffffu);
+        }
     };
     const uint32_t cmax_r0 = mapa_shared(&cmax[0][0], 0);
     const uint32_t adj_base = smem_u32(&lut[0][0]) + 4u * lane + 128u * (uint32_t)qmax - 128u * 0x4B400000u;
     float rm = 0.0f;
-    uint32_t um = 0u;
+    uint32_t um4[4] = {0u, 0u, 0u, 0u};
     if (my_items > 0)
-        for (int j = 0; j < kSub; ++j) {  // pass 0 of the first strip
-            float x[kWR];
-            consume(x);
-            um = max(um, absmax_bits(x));
-        }
+        for (int j = 0; j < kSub; ++j) consume_max(um4);  // pass 0 of the first strip
     for (int i = 0; i < my_items; ++i) {
         const int strip = cid + i * ncl;
         const int n = strip * kWC + lane;
-        wmax[w][lane] = um;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {  // lanes l, l ^ 8, l ^ 16, l ^ 24 hold the same 4 columns
+            um4[e] = max(um4[e], __shfl_xor_sync(0xffffffffu, um4[e], 8));
+            um4[e] = max(um4[e], __shfl_xor_sync(0xffffffffu, um4[e], 16));
+        }
+        if (lane < 8) *reinterpret_cast<uint4*>(&wmax[w][4 * lane]) = make_uint4(um4[0], um4[1], um4[2], um4[3]);
         __syncthreads();  // all warps' maxima; every warp is past the previous strip's table readers
         const int b = i % 3;
         if (w == 0) {
@@ -1443,7 +1462,8 @@ __global__ void __launch_bounds__(kWW * 32, 1)
         const float lam32 = __double2float_rn(lam);
         const bool exact = !(lam32 <= FLT_MAX);
         const bool next = i + 1 < my_items;
-        um = 0u;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) um4[e] = 0u;
         for (int j = 0; j < kSub; ++j) {
             const int k0 = (int)crank * kRowsCta + (w * kSub + j) * kWR;
             float x[kWR];
@@ -1480,10 +1500,7 @@ __global__ void __launch_bounds__(kWW * 32, 1)
                     }
                 }
             }
-            if (next) {  // pass 0 of the next strip (DRAM)
-                consume(x);
-                um = max(um, absmax_bits(x));
-            }
+            if (next) consume_max(um4);  // pass 0 of the next strip (DRAM)
         }
     }
     float r = warp_maxf(rm);
@@ -1652,7 +1669,8 @@ void launch_cols_any(const CUtensorMap& tm, const QuantColsArgs& qa, const Selec
 
 // Fused column maxima + quantisation (k_cols_maxq); false when the shape or
 // options need the two-kernel path.  Launched as 16 warps x 2 ring slots x 4
-// sub-tiles per warp (8x4x8, 12x3x4 and 8x6x8 measured slower).
+// sub-tiles per warp (8x4x8, 12x3x4 and 8x6x8 measured slower; 16x2x8 and
+// 16x2x2 - clusters of 2 and 8 at K = 8192 - too: C3 K1 174 -> 190 / 186 us).
 template <int WW, int SLOTS, int SUB>
 bool launch_cols_maxq(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cudaStream_t s) {
     constexpr int rows_cta = WW * kWR * SUB;
