@@ -82,6 +82,7 @@ struct GemmArgs {
     const uint32_t* rep_src;
     uint32_t* rep_dst;
     int rep_words;
+    int rep_flag;  // word of rep_dst written last (after a system fence); 0: none
 };
 
 template <int BN, int NACC>
@@ -874,8 +875,14 @@ __global__ void __launch_bounds__(384, 1)
         if (*last) {
             __threadfence();
             for (int i = threadIdx.x; i < args.rep_words; i += blockDim.x)
-                args.rep_dst[i] = *reinterpret_cast<const volatile uint32_t*>(args.rep_src + i);
+                if (i != args.rep_flag || args.rep_flag == 0)
+                    args.rep_dst[i] = *reinterpret_cast<const volatile uint32_t*>(args.rep_src + i);
             __threadfence_system();
+            __syncthreads();
+            if (args.rep_dst && args.rep_flag > 0 && threadIdx.x == 0) {  // published last: the host polls it
+                *reinterpret_cast<volatile uint32_t*>(args.rep_dst + args.rep_flag) = gridDim.x;
+                __threadfence_system();
+            }
         }
     }
 }
