@@ -1,0 +1,21 @@
+"""C3 with the reference's default configuration (PerTensor, MinRule): stage
+timings per call (profiling driver).  THR overrides the threshold M."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2403_06924_b200 as xg  # noqa: E402
+
+n = int(os.environ.get("N", "8192"))
+a = xg.generate("student_t3", n, n, 1)
+b = xg.generate("student_t3", n, n, 2)
+out = torch.empty((n, n), dtype=torch.float32, device="cuda")
+cfg = xg.XigemmConfig(threshold=float(os.environ.get("THR", "0.01414")), scheme=xg.QuantScheme.PerTensor,
+                      policy=xg.ReductionPolicy.MinRule)
+for _ in range(int(os.environ.get("CALLS", "5"))):
+    rep = xg.xigemm(a, b, cfg=cfg, out=out)
+torch.cuda.synchronize()
+print("density", rep.density_a, rep.density_b, int(rep.path), rep.timings)
