@@ -364,10 +364,13 @@ def test_deferred_mean_fallback_widened():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("shape", [(129, 2052, 300), (64, 8192, 96), (300, 1024, 1028), (40, 4096, 2048)])
+@pytest.mark.parametrize("shape", [(129, 2052, 300), (64, 8192, 96), (300, 1024, 1028), (40, 4096, 2048),
+                                   (257, 2048, 1000), (300, 1500, 516), (260, 700, 260)])
 def test_pipeline_vs_oracle_wide(oracle, shape):
     """Shapes with K >= 1024 (multiple of 4) and N >= 1024 that take the
-    streaming row kernels (4 warps per row) and the column-tile kernels."""
+    streaming row kernels (4 warps per row) and the column-tile kernels; K of
+    700, 1500 and 2048 take K1-B's short-K cluster shapes (256- and 1024-row
+    CTAs, clusters of 3 and 2)."""
     m, k, n = shape
     rng = np.random.default_rng(sum(shape))
     a = ol.random_dense(m, k, m + 1, -4, 4)
