@@ -1507,7 +1507,7 @@ xg_status xg_spmm_i8(int rows, int cols, const int32_t* row_ptr, const int32_t* 
                      xg_stream s) {
     return guarded([&] {
         req(cols <= xg::gemm_max_inner(d_bits), "spmm_int: inner dimension permits 32-bit overflow");
-        if (rows > 0 && d_cols > 0 && cols < 65536 && xg::spmm_strip_width(cols) > 0 && !getenv("XG_SPMM_NAIVE")) {
+        if (rows > 0 && d_cols > 0 && cols < 65536 && xg::spmm_strip_width(cols) > 0) {
             // quad-packed rows + the strip SpMM (spmm.cu); the nnz sizes the buffer
             int32_t nnz = 0;
             ck(cudaMemcpyAsync(&nnz, row_ptr + rows, sizeof nnz, cudaMemcpyDeviceToHost, st(s)), "nnz");

@@ -145,14 +145,6 @@ bool use_pair_kernel(const GemmArgs& args) {
     return !env && args.M >= 256;
 }
 
-int pair_count(const GemmArgs& args) {
-    static const int env = [] {
-        const char* e = getenv("XG_GEMM_PAIRS");
-        return e ? atoi(e) : 0;
-    }();
-    if (env == 1 || env == 2) return env;
-    return 1;  // 4-CTA multicast measured slower on B200 (fewer co-resident clusters); opt-in only
-}
 
 }  // namespace
 
@@ -182,10 +174,12 @@ void gemm_i8(int epi, const KOperand* ops, const int* is_b, int nops, const Gemm
              cudaStream_t s) {
     // the pair kernel's TMA-store epilogue needs 16-byte row pitch for the fp32 maps
     if (use_pair_kernel(args) && (epi == EPI_DF || epi == EPI_COMP || epi == EPI_ACC) && (args.N % 4) == 0) {
-        const bool mc = pair_count(args) == 2;
+        // one pair per cluster: the 4-CTA variant (PAIRS = 2, B^T multicast to two
+        // pairs) measured slower on B200 - 33 co-resident clusters, 132 SMs: D_F
+        // 306 -> 365 us at C3 (profiles/README.md) - and is not instantiated
         switch (epi) {
-            case EPI_DF: mc ? run2<1, EPI_DF, 2>(ops, is_b, nops, args, s) : run2<1, EPI_DF, 1>(ops, is_b, nops, args, s); return;
-            case EPI_COMP: mc ? run2<2, EPI_COMP, 2>(ops, is_b, nops, args, s) : run2<2, EPI_COMP, 1>(ops, is_b, nops, args, s); return;
+            case EPI_DF: run2<1, EPI_DF, 1>(ops, is_b, nops, args, s); return;
+            case EPI_COMP: run2<2, EPI_COMP, 1>(ops, is_b, nops, args, s); return;
             case EPI_ACC:  // K <= 4096: the epilogue bounds the tile - deeper D_F prefetch, 5 stages
                 if (args.K <= 4096) run2<1, EPI_ACC, 1, 5>(ops, is_b, nops, args, s);
                 else run2<1, EPI_ACC, 1>(ops, is_b, nops, args, s);

@@ -441,7 +441,7 @@ struct Gemm2Cfg {
 };
 
 // PAIRS = 2: a 4-CTA cluster of two pairs stacked along M sharing B^T tiles
-// through TMA multicast (opt-in: measured slower on B200, fewer co-resident
+// through TMA multicast (not instantiated: measured slower on B200, fewer co-resident
 // clusters).  Stages may only be overwritten once BOTH pairs' MMAs are done, so
 // the MMA commits that free stages are multicast to all four CTAs.
 //
