@@ -681,7 +681,13 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
     return v;
 }
-// table entry at adj + (u << SHIFT): one IMAD (adj already holds the -(magic << SHIFT) bias)
+// table entry at adj + (u << SHIFT): one IMAD (adj already holds the -(magic << SHIFT) bias;
+// opaque_u32 keeps the compiler from splitting the bias back out into a second add per lookup)
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+    uint32_t o;  // a shuffle with the own lane: opaque to ptxas's reassociation
+    asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(o) : "r"(v), "r"((int)(threadIdx.x & 31)));
+    return o;
+}
 template <int SHIFT>
 __device__ __forceinline__ float lut_at(uint32_t u, uint32_t adj) {
     uint32_t a;
@@ -982,7 +988,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_select_rows_r4(const SelectArgs a
         __syncthreads();  // table of this row complete (and the previous row's readers are past it)
         const float lam32 = __double2float_rn(lam);
         const bool exact = !(lam32 <= FLT_MAX) || !(lam_r32 <= FLT_MAX);
-        const uint32_t adj = smem_u32(tb) + 4u * (uint32_t)qmax - 4u * 0x4B400000u;
+        const uint32_t adj = opaque_u32(smem_u32(tb) + 4u * (uint32_t)qmax - 4u * 0x4B400000u);
         int8_t* rq_row = a.rq + (int64_t)r * a.ldq;
         int8_t* rd_row = a.red + (int64_t)r * a.ldq;
         float lmax = 0.0f;
@@ -1078,7 +1084,7 @@ __global__ void __launch_bounds__(NT, MINB) k_quant_rows_r4(const QuantRowsArgs 
         __syncthreads();
         const float lam32 = __double2float_rn(lam);
         const bool exact = odd || !(lam32 <= FLT_MAX);
-        const uint32_t adj = smem_u32(tb) + 4u * (uint32_t)qmax - 4u * 0x4B400000u;
+        const uint32_t adj = opaque_u32(smem_u32(tb) + 4u * (uint32_t)qmax - 4u * 0x4B400000u);
         float rm = 0.0f;
         int8_t* qrow = a.q + (int64_t)r * a.ldq;
 #pragma unroll
@@ -1183,7 +1189,7 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
     __syncthreads();
     if (lane == 0)
         for (int g = 0; g < kWSlots && g < nsub; ++g) issue(g);
-    const uint32_t adj_base = smem_u32(&lut[0][0]) + 4u * lane + 128u * (uint32_t)qmax - 128u * 0x4B400000u;
+    const uint32_t adj_base = opaque_u32(smem_u32(&lut[0][0]) + 4u * lane + 128u * (uint32_t)qmax - 128u * 0x4B400000u);
     float rm = 0.0f, ret = 0.0f;
     unsigned cnt = 0;
     int g = 0;
@@ -1407,7 +1413,7 @@ __global__ void __launch_bounds__(kWW * 32, 1)
         }
     };
     const uint32_t cmax_r0 = mapa_shared(&cmax[0][0], 0);
-    const uint32_t adj_base = smem_u32(&lut[0][0]) + 4u * lane + 128u * (uint32_t)qmax - 128u * 0x4B400000u;
+    const uint32_t adj_base = opaque_u32(smem_u32(&lut[0][0]) + 4u * lane + 128u * (uint32_t)qmax - 128u * 0x4B400000u);
     float rm = 0.0f;
     uint32_t um4[4] = {0u, 0u, 0u, 0u};
     if (my_items > 0)
