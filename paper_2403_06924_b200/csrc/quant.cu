@@ -1664,13 +1664,14 @@ void launch_cols_w(const CUtensorMap& tm, const QuantColsArgs& qa, const SelectA
     kern<<<items < cap ? items : cap, WW * 32, smem, s>>>(tm, qa, sa);
 }
 
-// Column-kernel shape: 8 warps x 2 ring slots per warp x 2 CTAs per SM since the
-// strip-major item order (select-B at C3 111 -> 105 us, C4 -4 us, C2 +1 us
-// against 16 x 2 x 1; 12x1x2, 24x1x1 and 4x4x2 measured slower, profiles/README.md)
+// Column-kernel shape: 8 warps x 1 ring slot per warp x 3 CTAs per SM (80
+// registers; 24 warps per SM hide more latency than a deeper ring: select-B
+// 102.4 -> 97.7 us at C3, reduce stage -5 / -8 us at C3 / C4, against 8x2x2;
+// 16x2x1, 12x1x2, 24x1x1 and 4x4x2 measured slower, profiles/README.md)
 template <bool SELECT>
 void launch_cols_any(const CUtensorMap& tm, const QuantColsArgs& qa, const SelectArgs& sa, int rows, int cols,
                      cudaStream_t s) {
-    launch_cols_w<SELECT, 8, 2, 2>(tm, qa, sa, rows, cols, s);
+    launch_cols_w<SELECT, 8, 1, 3>(tm, qa, sa, rows, cols, s);
 }
 
 // Fused column maxima + quantisation (k_cols_maxq); false when the shape or
