@@ -1621,12 +1621,15 @@ void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
                          ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
     if (a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 8192) {
         const int vpt = (a.cols + kRT * 4 - 1) / (kRT * 4);
-        const int cap = kNumSMs * (vpt > 8 ? 5 : 4);
+        // CTAs per SM by row length (registers hold the row): 5 at VPT 16 (96
+        // registers; C3 67.0 -> 64.0 us), 6 at VPT 8 (75; C2 24.4 -> 21.2 us),
+        // 8 below; one more CTA spills in each case
+        const int cap = kNumSMs * (vpt > 8 ? 5 : vpt > 4 ? 6 : 8);
         const int g = a.rows < cap ? a.rows : cap;
-        if (vpt <= 2) k_quant_rows_r4<2><<<g, kRT, 0, s>>>(a);
-        else if (vpt <= 4) k_quant_rows_r4<4><<<g, kRT, 0, s>>>(a);
-        else if (vpt <= 8) k_quant_rows_r4<8><<<g, kRT, 0, s>>>(a);
-        else k_quant_rows_r4<16, 5><<<g, kRT, 0, s>>>(a);  // 5 CTAs per SM (96 registers): 67.0 -> 64.0 us at C3; 6 spills (69.7)
+        if (vpt <= 2) k_quant_rows_r4<2, 8><<<g, kRT, 0, s>>>(a);
+        else if (vpt <= 4) k_quant_rows_r4<4, 8><<<g, kRT, 0, s>>>(a);
+        else if (vpt <= 8) k_quant_rows_r4<8, 6><<<g, kRT, 0, s>>>(a);
+        else k_quant_rows_r4<16, 5><<<g, kRT, 0, s>>>(a);
         return;
     }
     if (a.rounding == kNearest && aligned && a.cols > 8192 && a.cols <= 16384) {
