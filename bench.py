@@ -698,7 +698,9 @@ def run_b200_sharded(args, world, rank, local):
     import paper_2403_06924_b200 as xg
     from paper_2403_06924_b200 import sharded
 
-    torch.cuda.set_device(local)
+    # local % device count: the one-box check of this path runs both ranks on one
+    # GPU over gloo (XG_BENCH_BACKEND=gloo); one process per GPU otherwise
+    torch.cuda.set_device(local % torch.cuda.device_count())
     m, n, k = args.m, args.n, args.k
     a = xg.generate("student_t3", m, k, 1 + 7919 * rank, 0.0, 1.0)
     b = xg.generate("student_t3", k, n, 2, 0.0, 1.0) if rank == 0 else \
@@ -715,7 +717,9 @@ def run_b200_sharded(args, world, rank, local):
 
     def step():
         sharded.broadcast_b(b)
-        return sharded.xigemm_sharded(a, b, cfg=cfg, out=out, rank_rows=[m] * world)
+        # graph capture needs NCCL collectives (the gloo check runs eagerly)
+        return sharded.xigemm_sharded(a, b, cfg=cfg, out=out, rank_rows=[m] * world,
+                                      graph=dist.get_backend() == "nccl")
 
     rep = step()
     for _ in range(args.warmup):
@@ -754,7 +758,7 @@ def run_b200_sharded(args, world, rank, local):
         if rank == 0:
             bd.copy_(bh, non_blocking=True)
         sharded.broadcast_b(bd)
-        sharded.xigemm_sharded(ad, bd, cfg=cfg, out=out, rank_rows=[m] * world)
+        sharded.xigemm_sharded(ad, bd, cfg=cfg, out=out, rank_rows=[m] * world, graph=dist.get_backend() == "nccl")
         oh.copy_(out, non_blocking=True)
         torch.cuda.synchronize()
 
