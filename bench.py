@@ -57,7 +57,7 @@ def _dist_init():
         import torch.distributed as dist
         backend = "nccl" if os.environ.get("XG_BENCH_BACKEND", "nccl") == "nccl" else "gloo"
         if backend == "nccl":
-            torch.cuda.set_device(local)
+            torch.cuda.set_device(local % torch.cuda.device_count())
         dist.init_process_group(backend)
     return world, rank, local
 
@@ -836,10 +836,11 @@ def main():
                     help="use the row-sharded pipeline even at N=1 (needs torchrun / a process group)")
     args = ap.parse_args()
     args.ref_rows_set = args.ref_rows is not None
+    if args.impl == "reference":  # CPU only: rank 0 runs it, the other ranks exit 0; no process group
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
+        return
     world, rank, local = _dist_init()
-    if args.impl == "reference":
-        run_reference(args, world, rank)
-    elif (world > 1 and not args.replicas) or args.sharded:
+    if (world > 1 and not args.replicas) or args.sharded:
         run_b200_sharded(args, world, rank, local)
     else:
         run_b200(args, world, rank, local)
