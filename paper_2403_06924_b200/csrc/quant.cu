@@ -731,6 +731,33 @@ __device__ __forceinline__ void qn4(const float (&x)[4], float lam32, uint32_t (
         dmax = fmax_nan(fmax_nan(dmax, fabsf(d0)), fabsf(d1));
     }
 }
+// Floor (quantize.cpp:16-20: 4-eps nudge away from zero, then truncation): u =
+// the bits of magic + trunc(t), from floor(|t|) by a round-toward-zero add, and
+// the distance of frac(|t|) from 0.5 in dmax - the fast result stands when
+// frac lies in (2e-4, 1 - 2e-4), so neither the fp32 product's error (<= 1.5e-5
+// at |t| <= 128) nor the nudge can move the truncation (the margin q32<kFloor> uses)
+__device__ __forceinline__ uint32_t qf(float x, float lam32, float& dmax) {
+    const float t = __fmul_rn(x, lam32);
+    const float at = fabsf(t);
+    const float f = __fadd_rz(at, kMagic);         // magic + floor(|t|)
+    const float frac = __fsub_rn(at, __fsub_rn(f, kMagic));
+    dmax = fmax_nan(dmax, fabsf(__fsub_rn(frac, 0.5f)));
+    const uint32_t fb = __float_as_uint(f);
+    return t < 0.0f ? 2u * 0x4B400000u - fb : fb;  // ubits(-floor(|t|)) for t < 0
+}
+// the quad quantiser of rounding mode RND and its acceptance bound on dmax
+template <int RND>
+__device__ __forceinline__ void qr4(const float (&x)[4], float lam32, uint32_t (&u)[4], float& dmax) {
+    if constexpr (RND == kNearest) {
+        qn4(x, lam32, u, dmax);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) u[e] = qf(x[e], lam32, dmax);
+    }
+}
+template <int RND>
+constexpr float qok() { return RND == kNearest ? 0.4999f : 0.4998f; }
+
 __device__ __forceinline__ uint32_t pack4u(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
@@ -805,27 +832,27 @@ __global__ void __launch_bounds__(NT) k_quant_rows_fast(const QuantRowsArgs a) {
 }
 
 // Selection quad, Nearest.  lut_adj: smem address of lut entry q = adj + (u << shift).
-template <int SHIFT>
+template <int SHIFT, int RND = kNearest>
 __device__ __forceinline__ void select_quad_n(const float (&x)[4], uint32_t lut_adj, double lam,
                                               float lam32, double lam_r, float lam_r32, float tf,
                                               float qmaxf, bool exact, uint32_t& pq, uint32_t& pr,
                                               unsigned& cnt, float& lmax) {
     uint32_t u[4], ur[4];
     float dmax = 0.0f;
-    qn4(x, lam32, u, dmax);
+    qr4<RND>(x, lam32, u, dmax);
     float res[4];
 #pragma unroll
     for (int p = 0; p < 2; ++p)  // residual x - deq(q), two per FADD2
         upk2(sub2(pk2(x[2 * p], x[2 * p + 1]),
                   pk2(lut_at<SHIFT>(u[2 * p], lut_adj), lut_at<SHIFT>(u[2 * p + 1], lut_adj))),
              res[2 * p], res[2 * p + 1]);
-    qn4(res, lam_r32, ur, dmax);
-    if (exact || !(dmax < 0.4999f)) {
+    qr4<RND>(res, lam_r32, ur, dmax);
+    if (exact || !(dmax < qok<RND>())) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            u[e] = ubits(qexact(x[e], lam, qmaxf, kNearest));
+            u[e] = ubits(qexact(x[e], lam, qmaxf, RND));
             res[e] = __fsub_rn(x[e], lut_at<SHIFT>(u[e], lut_adj));
-            ur[e] = ubits(qexact(res[e], lam_r, qmaxf, kNearest));
+            ur[e] = ubits(qexact(res[e], lam_r, qmaxf, RND));
         }
     }
     uint32_t d[4];
@@ -940,7 +967,7 @@ __device__ __forceinline__ void build_row_lut(float* lut, double lam, int qmax) 
     }
 }
 
-template <int U, int MINB = kRCtasPerSM, bool KEEP = true>
+template <int U, int MINB = kRCtasPerSM, bool KEEP = true, int RND = kNearest>
 __global__ void __launch_bounds__(kRT, MINB) k_select_rows_r4(const SelectArgs a) {
     XG_PDL_WAIT();
     XG_EXIT_IF_NONFINITE(a.nonfinite);
@@ -1006,7 +1033,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_select_rows_r4(const SelectArgs a
                 if (c < a.cols) {
                     const float x[4] = {f[u].x, f[u].y, f[u].z, f[u].w};
                     uint32_t pq, pr;
-                    select_quad_n<2>(x, adj, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, pq, pr, cnt, lmax);
+                    select_quad_n<2, RND>(x, adj, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, pq, pr, cnt, lmax);
                     *reinterpret_cast<uint32_t*>(rq_row + c) = pq;
                     if (a.do_select) *reinterpret_cast<uint32_t*>(rd_row + c) = pr;
                     if (KEEP && a.keep) dump_keep4(a, r, c, x, tf);
@@ -1031,7 +1058,7 @@ __global__ void __launch_bounds__(kRT, MINB) k_select_rows_r4(const SelectArgs a
 
 // K1, A side: the row lives in registers (VPT float4 per thread), absmax ->
 // lambda -> table -> quantise -> residual max; two CTA barriers per row.
-template <int VPT, int MINB = 4, int NT = kRT>
+template <int VPT, int MINB = 4, int NT = kRT, int RND = kNearest>
 __global__ void __launch_bounds__(NT, MINB) k_quant_rows_r4(const QuantRowsArgs a) {
     XG_PDL_WAIT();
     __shared__ float lut[2][256];
@@ -1094,10 +1121,10 @@ __global__ void __launch_bounds__(NT, MINB) k_quant_rows_r4(const QuantRowsArgs 
             uint32_t u[4];
             float dmax = 0.0f;
 #pragma unroll
-            qn4(x, lam32, u, dmax);
-            if (exact || !(dmax < 0.4999f)) {
+            qr4<RND>(x, lam32, u, dmax);
+            if (exact || !(dmax < qok<RND>())) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(x[e], lam, qmaxf, kNearest));
+                for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(x[e], lam, qmaxf, RND));
             }
 #pragma unroll
             for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(x[e], lut_at<2>(u[e], adj))));
@@ -1134,7 +1161,7 @@ constexpr int kWC = 32, kWR = 32, kWSub = 1;
 template <int WW, int SLOTS>
 constexpr int col_w_smem() { return WW * SLOTS * kWC * kWR * 4 + 256 * kWC * 4 + 1024; }
 
-template <bool SELECT, int kWW, int kWSlots, int kWCtas, bool KEEP = true>
+template <bool SELECT, int kWW, int kWSlots, int kWCtas, bool KEEP = true, int RND = kNearest>
 __global__ void __launch_bounds__(kWW * 32, kWCtas)
     k_cols_w4(const __grid_constant__ CUtensorMap tmap, const QuantColsArgs qa, const SelectArgs sa) {
     XG_PDL_WAIT();
@@ -1244,16 +1271,16 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
             for (int q = 0; q < kWR / 4; ++q) {
                 const float xq[4] = {x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]};
                 if (SELECT) {
-                    select_quad_n<7>(xq, adj_base, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, w0[q], w1[q],
+                    select_quad_n<7, RND>(xq, adj_base, lam, lam32, lam_r, lam_r32, tf, qmaxf, exact, w0[q], w1[q],
                                      cnt, lmax);
                     if (KEEP && sa.keep && n < cols && k0 + 4 * q < rows) dump_keep4(sa, n, k0 + 4 * q, xq, tf);
                 } else {
                     uint32_t u[4];
                     float dmax = 0.0f;
-                    qn4(xq, lam32, u, dmax);
-                    if (exact || !(dmax < 0.4999f)) {
+                    qr4<RND>(xq, lam32, u, dmax);
+                    if (exact || !(dmax < qok<RND>())) {
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(xq[e], lam, qmaxf, kNearest));
+                        for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(xq[e], lam, qmaxf, RND));
                     }
 #pragma unroll
                     for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(xq[e], lut_at<7>(u[e], adj_base))));
@@ -1616,29 +1643,37 @@ void quant_rows_rnd(const QuantRowsArgs& a, cudaStream_t s) {
     else k_quant_rows_generic<<<g, kThreads, 0, s>>>(a);
 }
 
-void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
-    const bool aligned = (a.ld % 4 == 0) && (a.ldq % 4 == 0) && (a.cols % 4 == 0) &&
-                         ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
-    if (a.rounding == kNearest && aligned && a.cols >= 1024 && a.cols <= 8192) {
+// the register-resident row kernels for K in [1024, 16384]; false otherwise
+template <int RND>
+bool launch_quant_rows_r4(const QuantRowsArgs& a, cudaStream_t s) {
+    if (a.cols >= 1024 && a.cols <= 8192) {
         const int vpt = (a.cols + kRT * 4 - 1) / (kRT * 4);
         // CTAs per SM by row length (registers hold the row): 5 at VPT 16 (96
         // registers; C3 67.0 -> 64.0 us), 6 at VPT 8 (75; C2 24.4 -> 21.2 us),
         // 8 below; one more CTA spills in each case
         const int cap = kNumSMs * (vpt > 8 ? 5 : vpt > 4 ? 6 : 8);
         const int g = a.rows < cap ? a.rows : cap;
-        if (vpt <= 2) k_quant_rows_r4<2, 8><<<g, kRT, 0, s>>>(a);
-        else if (vpt <= 4) k_quant_rows_r4<4, 8><<<g, kRT, 0, s>>>(a);
-        else if (vpt <= 8) k_quant_rows_r4<8, 6><<<g, kRT, 0, s>>>(a);
-        else k_quant_rows_r4<16, 5><<<g, kRT, 0, s>>>(a);
-        return;
+        if (vpt <= 2) k_quant_rows_r4<2, 8, kRT, RND><<<g, kRT, 0, s>>>(a);
+        else if (vpt <= 4) k_quant_rows_r4<4, 8, kRT, RND><<<g, kRT, 0, s>>>(a);
+        else if (vpt <= 8) k_quant_rows_r4<8, 6, kRT, RND><<<g, kRT, 0, s>>>(a);
+        else k_quant_rows_r4<16, 5, kRT, RND><<<g, kRT, 0, s>>>(a);
+        return true;
     }
-    if (a.rounding == kNearest && aligned && a.cols > 8192 && a.cols <= 16384) {
+    if (a.cols > 8192 && a.cols <= 16384) {
         // K in (8192, 16384] (C5): the same register-resident row over 256 threads
         const int cap = kNumSMs * 2;
         const int g = a.rows < cap ? a.rows : cap;
-        k_quant_rows_r4<16, 2, 256><<<g, 256, 0, s>>>(a);
-        return;
+        k_quant_rows_r4<16, 2, 256, RND><<<g, 256, 0, s>>>(a);
+        return true;
     }
+    return false;
+}
+
+void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
+    const bool aligned = (a.ld % 4 == 0) && (a.ldq % 4 == 0) && (a.cols % 4 == 0) &&
+                         ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+    if (aligned && (a.rounding == kNearest ? launch_quant_rows_r4<kNearest>(a, s) : launch_quant_rows_r4<kFloor>(a, s)))
+        return;
     if (a.rounding == kNearest) {
         const int g = grid_rows(a.rows);
         const int vpt = (a.cols + kThreads * 4 - 1) / (kThreads * 4);
@@ -1655,12 +1690,13 @@ void launch_quant_rows(const QuantRowsArgs& a, cudaStream_t s) {
 
 
 
-template <bool SELECT, int WW, int SLOTS, int CTAS>
+template <bool SELECT, int WW, int SLOTS, int CTAS, int RND>
 void launch_cols_w(const CUtensorMap& tm, const QuantColsArgs& qa, const SelectArgs& sa, int rows, int cols,
                    cudaStream_t s) {
     constexpr int smem = col_w_smem<WW, SLOTS>();
     // no stage-dump bitmask: the variant without the per-quad check
-    auto kern = (SELECT && !sa.keep) ? k_cols_w4<SELECT, WW, SLOTS, CTAS, false> : k_cols_w4<SELECT, WW, SLOTS, CTAS>;
+    auto kern = (SELECT && !sa.keep) ? k_cols_w4<SELECT, WW, SLOTS, CTAS, false, RND>
+                                     : k_cols_w4<SELECT, WW, SLOTS, CTAS, true, RND>;
     set_dyn_smem(kern, smem);
     const int items = ((cols + kWC - 1) / kWC) * ((rows + WW * kWR * kWSub - 1) / (WW * kWR * kWSub));
     const int cap = kNumSMs * CTAS;
@@ -1673,8 +1709,9 @@ void launch_cols_w(const CUtensorMap& tm, const QuantColsArgs& qa, const SelectA
 // 16x2x1, 12x1x2, 24x1x1 and 4x4x2 measured slower, profiles/README.md)
 template <bool SELECT>
 void launch_cols_any(const CUtensorMap& tm, const QuantColsArgs& qa, const SelectArgs& sa, int rows, int cols,
-                     cudaStream_t s) {
-    launch_cols_w<SELECT, 8, 1, 3>(tm, qa, sa, rows, cols, s);
+                     int rounding, cudaStream_t s) {
+    if (rounding == kNearest) launch_cols_w<SELECT, 8, 1, 3, kNearest>(tm, qa, sa, rows, cols, s);
+    else launch_cols_w<SELECT, 8, 1, 3, kFloor>(tm, qa, sa, rows, cols, s);
 }
 
 // Fused column maxima + quantisation (k_cols_maxq); false when the shape or
@@ -1731,10 +1768,10 @@ bool launch_quant_cols_fused(const QuantColsArgs& a, uint32_t* gmax, int* nonfin
 }
 
 void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {
-    if (a.rounding == kNearest && a.rows >= 256 && (a.ldq % 16) == 0) {
+    if (a.rows >= 256 && (a.ldq % 16) == 0) {
         alignas(64) CUtensorMap tm;
         if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) {
-            launch_cols_any<false>(tm, a, SelectArgs{}, a.rows, a.cols, s);
+            launch_cols_any<false>(tm, a, SelectArgs{}, a.rows, a.cols, a.rounding, s);
             return;
         }
     }
@@ -1751,12 +1788,17 @@ void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {
 void launch_select_rows(const SelectArgs& a, cudaStream_t s) {
     const bool aligned = (a.ld % 4 == 0) && (a.ldq % 4 == 0) && (a.cols % 4 == 0) &&
                          ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
-    if (!a.fix_mode && a.rounding == kNearest && aligned && a.cols >= 512) {
+    if (!a.fix_mode && aligned && a.cols >= 512) {
         // 4 loads in flight per thread, kRCtasPerSM CTAs per SM (2x8, 8x6 and 4x12 measured slower)
         const int cap = kNumSMs * kRCtasPerSM;
         const int g = a.rows < cap ? a.rows : cap;
-        if (a.keep) k_select_rows_r4<4><<<g, kRT, 0, s>>>(a);
-        else k_select_rows_r4<4, kRCtasPerSM, false><<<g, kRT, 0, s>>>(a);  // no stage-dump bitmask
+        if (a.rounding == kNearest) {
+            if (a.keep) k_select_rows_r4<4><<<g, kRT, 0, s>>>(a);
+            else k_select_rows_r4<4, kRCtasPerSM, false><<<g, kRT, 0, s>>>(a);  // no stage-dump bitmask
+        } else {
+            if (a.keep) k_select_rows_r4<4, kRCtasPerSM, true, kFloor><<<g, kRT, 0, s>>>(a);
+            else k_select_rows_r4<4, kRCtasPerSM, false, kFloor><<<g, kRT, 0, s>>>(a);
+        }
         return;
     }
     if (a.fix_mode) k_fix_rows<<<grid_rows(a.rows), kThreads, 0, s>>>(a);
@@ -1769,10 +1811,10 @@ void launch_select_cols_T(const SelectArgs& a, cudaStream_t s) {
         k_fix_cols_T<<<grid_rows(a.cols), kThreads, 0, s>>>(a);
         return;
     }
-    if (a.rounding == kNearest && a.rows >= 256 && (a.ldq % 16) == 0) {
+    if (a.rows >= 256 && (a.ldq % 16) == 0) {
         alignas(64) CUtensorMap tm;
         if (make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) {
-            launch_cols_any<true>(tm, QuantColsArgs{}, a, a.rows, a.cols, s);
+            launch_cols_any<true>(tm, QuantColsArgs{}, a, a.rows, a.cols, a.rounding, s);
             return;
         }
     }

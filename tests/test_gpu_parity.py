@@ -370,18 +370,20 @@ def test_pipeline_vs_oracle_wide(oracle, shape):
     """Shapes with K >= 1024 (multiple of 4) and N >= 1024 that take the
     streaming row kernels (4 warps per row) and the column-tile kernels; K of
     700, 1500 and 2048 take K1-B's short-K cluster shapes (256- and 1024-row
-    CTAs, clusters of 3 and 2)."""
+    CTAs, clusters of 3 and 2).  Nearest and Floor rounding (Floor runs the same
+    register-row and column-tile kernels with the truncating quantiser)."""
     m, k, n = shape
     rng = np.random.default_rng(sum(shape))
     a = ol.random_dense(m, k, m + 1, -4, 4)
     b = ol.random_dense(k, n, n + 2, -4, 4)
     a[3 % m, 5] = 37.0  # an outlier row / column
-    for scheme, pol, bits, thr in ((1, 0, 8, 0.05), (0, 1, 8, 0.3), (1, 1, 4, 0.1), (0, 0, 8, 0.02)):
-        c = ol.cfg(bits=bits, threshold=thr, density_limit=0.5, scheme=scheme, policy=pol, rounding=1)
+    for scheme, pol, bits, thr, rnd in ((1, 0, 8, 0.05, 1), (0, 1, 8, 0.3, 1), (1, 1, 4, 0.1, 1), (0, 0, 8, 0.02, 1),
+                                        (1, 0, 8, 0.05, 0), (0, 1, 8, 0.3, 0), (1, 1, 4, 0.1, 0)):
+        c = ol.cfg(bits=bits, threshold=thr, density_limit=0.5, scheme=scheme, policy=pol, rounding=rnd)
         rc, ref, orep = oracle.xigemm(a, b, config=c)
         assert rc == 0
         rep = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), cfg=cfg_from(c))
-        assert beq(rep.result, ref), (shape, scheme, pol, bits)
+        assert beq(rep.result, ref), (shape, scheme, pol, bits, rnd)
         assert (rep.density_a, rep.density_b, int(rep.path)) == (orep.density_a, orep.density_b, orep.path)
 
 

@@ -40,9 +40,9 @@ def beq(x, y):
     return np.array_equal(x, y)
 
 
-def vw_cfg(thr, s=0.3):
+def vw_cfg(thr, s=0.3, rnd=1):
     return xg.XigemmConfig(threshold=thr, density_limit=s, scheme=xg.QuantScheme.VectorWise,
-                           policy=xg.ReductionPolicy.AvgRule)
+                           policy=xg.ReductionPolicy.AvgRule, rounding=xg.RoundingMode(rnd))
 
 
 def bisect_threshold(a, b, target, s=0.3):
@@ -57,12 +57,12 @@ def bisect_threshold(a, b, target, s=0.3):
     return mid
 
 
-def stagewise(a, b, thr, s=0.3, nrows=48, seed=0, graph_check=False):
+def stagewise(a, b, thr, s=0.3, nrows=48, seed=0, graph_check=False, rnd=1):
     """Stage-wise parity of one full-size problem; nrows=None checks D_F and the
     final C on every row.  graph_check: the production path (CUDA-graph replay,
     no dump) must give the dump run's C bit for bit on every row."""
     o = ol.oracle()
-    cfg = vw_cfg(thr, s)
+    cfg = vw_cfg(thr, s, rnd)
     rep, d = xg.xigemm_dump(a, b, cfg)
     if graph_check:
         out = torch.empty_like(rep.result)
@@ -76,15 +76,15 @@ def stagewise(a, b, thr, s=0.3, nrows=48, seed=0, graph_check=False):
     m, k = an.shape
     n = bn.shape[1]
     # K1
-    rc, aq, la = o.quantize(an, 8, 1, 1)
+    rc, aq, la = o.quantize(an, 8, 1, rnd)
     assert rc == 0 and beq(d["aq"], aq) and beq(d["aq_scales"], la)
-    rc, bq, lb = o.quantize(bn, 8, 2, 1)
+    rc, bq, lb = o.quantize(bn, 8, 2, rnd)
     assert rc == 0 and beq(d["bq"], bq) and beq(d["bq_scales"], lb)
     rc, ra = o.residual(an, aq, la, 1)
-    rc, raq, lra = o.quantize(ra, 8, 0, 1)  # pipeline.cpp:86-93: always per tensor
+    rc, raq, lra = o.quantize(ra, 8, 0, rnd)  # pipeline.cpp:86-93: always per tensor
     assert beq(d["raq"], raq) and beq(d["raq_scale"], lra)
     rc, rb = o.residual(bn, bq, lb, 2)
-    rc, rbq, lrb = o.quantize(rb, 8, 0, 1)
+    rc, rbq, lrb = o.quantize(rb, 8, 0, rnd)
     assert beq(d["rbq"], rbq) and beq(d["rbq_scale"], lrb)
     del ra, rb
     # K2 on sampled rows (int8 products summed exactly in fp64: |sum| < 2^31)
@@ -135,6 +135,15 @@ def test_c2_4096_normal_density_sweep():
         thr = bisect_threshold(a, b, target)
         rep = stagewise(a, b, thr, nrows=None if target == 0.05 else 256, seed=int(target * 100))
         assert abs(max(rep.density_a, rep.density_b) - target) <= 0.1 * target
+
+
+def test_c3_floor_rounding_stagewise():
+    """C3 data with Floor rounding (quantize.cpp:16-20): the register-row and
+    column-tile kernels with the truncating quantiser (K1-B takes the two-kernel
+    path), stage-wise against the oracle at full size, and the graph path."""
+    a = xg.generate("student_t3", 8192, 8192, 1, 0.0, 1.0)
+    b = xg.generate("student_t3", 8192, 8192, 2, 0.0, 1.0)
+    stagewise(a, b, 0.0154, nrows=32, seed=3, graph_check=True, rnd=0)
 
 
 def test_c3_8192_student_t_5pct():

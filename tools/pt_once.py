@@ -19,3 +19,14 @@ for _ in range(int(os.environ.get("CALLS", "5"))):
     rep = xg.xigemm(a, b, cfg=cfg, out=out)
 torch.cuda.synchronize()
 print("density", rep.density_a, rep.density_b, int(rep.path), rep.timings)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+steps = int(os.environ.get("STEPS", "20"))
+e0.record()
+for _ in range(steps):
+    rep = xg.xigemm(a, b, cfg=cfg, out=out)
+e1.record()
+torch.cuda.synchronize()
+st = rep.timings
+print("per call %.1f us (events); stages quant %d df %d reduce %d comp %d us" % (
+    e0.elapsed_time(e1) / steps * 1e3, st["quant"] // 1000, st["gemm_df"] // 1000, st["reduce"] // 1000,
+    st["gemm_comp"] // 1000))
