@@ -1347,7 +1347,7 @@ __global__ void __launch_bounds__(kWW * 32, kWCtas)
 // cluster exchange sits between strips.  B leaves DRAM once instead of twice
 // (k_absmax_cols + k_cols_w4<0>).  A strip with a non-finite value raises
 // `nonfinite` and is not quantised (the call fails, pipeline.cpp:50-52).
-template <int kWW, int kWSlots, int kSub>
+template <int kWW, int kWSlots, int kSub, int RND = kNearest>
 __global__ void __launch_bounds__(kWW * 32, 1)
     k_cols_maxq(const __grid_constant__ CUtensorMap tmap, const QuantColsArgs qa, uint32_t* gmax, int* nonfinite) {
     XG_PDL_WAIT();
@@ -1508,10 +1508,10 @@ __global__ void __launch_bounds__(kWW * 32, 1)
                     const float xq[4] = {x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]};
                     uint32_t u[4];
                     float dmax = 0.0f;
-                    qn4(xq, lam32, u, dmax);
-                    if (exact || !(dmax < 0.4999f)) {
+                    qr4<RND>(xq, lam32, u, dmax);
+                    if (exact || !(dmax < qok<RND>())) {
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(xq[e], lam, qmaxf, kNearest));
+                        for (int e = 0; e < 4; ++e) u[e] = ubits(qexact(xq[e], lam, qmaxf, RND));
                     }
 #pragma unroll
                     for (int e = 0; e < 4; ++e) rm = fmaxf(rm, fabsf(__fsub_rn(xq[e], lut_at<7>(u[e], adj_base))));
@@ -1718,7 +1718,7 @@ void launch_cols_any(const CUtensorMap& tm, const QuantColsArgs& qa, const Selec
 // options need the two-kernel path.  Launched as 16 warps x 2 ring slots x 4
 // sub-tiles per warp (8x4x8, 12x3x4 and 8x6x8 measured slower; 16x2x8 and
 // 16x2x2 - clusters of 2 and 8 at K = 8192 - too: C3 K1 174 -> 190 / 186 us).
-template <int WW, int SLOTS, int SUB>
+template <int WW, int SLOTS, int SUB, int RND>
 bool launch_cols_maxq(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cudaStream_t s) {
     constexpr int rows_cta = WW * kWR * SUB;
     const int csize = (a.rows + rows_cta - 1) / rows_cta;
@@ -1729,7 +1729,7 @@ bool launch_cols_maxq(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cu
     alignas(64) CUtensorMap tm;
     if (!make_tmap_f32(&tm, a.x, a.rows, a.cols, a.ld, kWC, kWR)) return false;
     constexpr int smem = col_w_smem<WW, SLOTS>();
-    auto kern = k_cols_maxq<WW, SLOTS, SUB>;
+    auto kern = k_cols_maxq<WW, SLOTS, SUB, RND>;
     set_dyn_smem(kern, smem);
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
@@ -1758,13 +1758,19 @@ bool launch_cols_maxq(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cu
     return cudaLaunchKernelEx(&cfg, kern, tm, a, gmax, nonfinite) == cudaSuccess;
 }
 
-bool launch_quant_cols_fused(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cudaStream_t s) {
-    if (!a.per_col || a.rounding != kNearest || a.rows < 256 || (a.ldq % 16) != 0) return false;
+template <int RND>
+bool launch_quant_cols_fused_rnd(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cudaStream_t s) {
     // short K: CTAs of fewer rows, so the cluster grid (strips x cluster size)
     // still spreads over the SMs (C1 1024^3: K1 19 -> 13 us; 2048^3: 25 -> 21 us)
-    if (a.rows <= 1024) return launch_cols_maxq<8, 2, 1>(a, gmax, nonfinite, s);
-    if (a.rows <= 2048) return launch_cols_maxq<16, 2, 2>(a, gmax, nonfinite, s);
-    return launch_cols_maxq<16, 2, 4>(a, gmax, nonfinite, s);
+    if (a.rows <= 1024) return launch_cols_maxq<8, 2, 1, RND>(a, gmax, nonfinite, s);
+    if (a.rows <= 2048) return launch_cols_maxq<16, 2, 2, RND>(a, gmax, nonfinite, s);
+    return launch_cols_maxq<16, 2, 4, RND>(a, gmax, nonfinite, s);
+}
+
+bool launch_quant_cols_fused(const QuantColsArgs& a, uint32_t* gmax, int* nonfinite, cudaStream_t s) {
+    if (!a.per_col || a.rows < 256 || (a.ldq % 16) != 0) return false;
+    return a.rounding == kNearest ? launch_quant_cols_fused_rnd<kNearest>(a, gmax, nonfinite, s)
+                                  : launch_quant_cols_fused_rnd<kFloor>(a, gmax, nonfinite, s);
 }
 
 void launch_quant_cols_T(const QuantColsArgs& a, cudaStream_t s) {

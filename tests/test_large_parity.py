@@ -138,9 +138,9 @@ def test_c2_4096_normal_density_sweep():
 
 
 def test_c3_floor_rounding_stagewise():
-    """C3 data with Floor rounding (quantize.cpp:16-20): the register-row and
-    column-tile kernels with the truncating quantiser (K1-B takes the two-kernel
-    path), stage-wise against the oracle at full size, and the graph path."""
+    """C3 data with Floor rounding (quantize.cpp:16-20): the register-row,
+    column-tile and K1-B cluster kernels with the truncating quantiser,
+    stage-wise against the oracle at full size, and the graph path."""
     a = xg.generate("student_t3", 8192, 8192, 1, 0.0, 1.0)
     b = xg.generate("student_t3", 8192, 8192, 2, 0.0, 1.0)
     stagewise(a, b, 0.0154, nrows=32, seed=3, graph_check=True, rnd=0)
