@@ -742,6 +742,19 @@ def run_b200_sharded(args, world, rank, local):
     ms = float(tt.item())
     ops = 2.0 * m * world * n * k
     value = ops / (ms * 1e-3) / 1e12
+    # SURVEY 8(e)'s resident-B design beside it: B already on every rank (weights
+    # style), the same step without the broadcast
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        sharded.xigemm_sharded(a, b, cfg=cfg, out=out, rank_rows=[m] * world, graph=dist.get_backend() == "nccl")
+    e1.record(stream)
+    torch.cuda.synchronize()
+    tr = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(tr, op=dist.ReduceOp.MAX)
+    ms_res = float(tr.item())
+    sharded.launch_count(reset=True)
 
     # e2e: host A rows on every rank, host B on rank 0, C rows back to the host
     ah = torch.empty((m, k), dtype=torch.float32, pin_memory=True)
@@ -797,6 +810,12 @@ def run_b200_sharded(args, world, rank, local):
                        workload=f"row-sharded xigemm: A {m * world}x{k} ({m} rows per GPU), B {k}x{n} "
                                 f"broadcast from rank 0 every step, Student-t(3), INT8 vector-wise AvgRule",
                        parallelism=f"rows{world} (B replicated by NCCL broadcast; exact all-reduce couplings)"),
+        "variants": {
+            "resident_b": {"value": ops / (ms_res * 1e-3) / 1e12, "ms_per_step": ms_res,
+                           "note": "B resident on every rank (SURVEY 8(e) resident-B design): the step without "
+                                   "the broadcast"},
+            "column_sliced_b": "not built: SURVEY 8(e)'s scalable design (1/g column slice of the B side per "
+                               "rank, all-gather of Bq / RBq / B'q) - the broadcast design is the north star's"},
         "e2e": {"value": e2e_val, "unit": "TFLOP/s", "h2d_bytes_per_step": 4 * (m * k * world + k * n),
                 "d2h_bytes_per_step": 4 * m * n * world},
         "roofline": {"bound": "tensor+hbm", "model": "per rank: T_roof = 2MNK/P_i8 + B_alg/BW of its rows "
