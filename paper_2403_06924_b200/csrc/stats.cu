@@ -27,7 +27,9 @@ __global__ void __launch_bounds__(kThreads)
                  double* col_sum, uint32_t* row_min, uint32_t* col_min) {
     XG_PDL_WAIT();
     const int c = (blockIdx.x * kThreads + threadIdx.x) * 4;
-    const int r0 = blockIdx.y * kSlab;
+    // slabs bottom-up: the D_F GEMM wrote the bottom row panels last, so the
+    // first slabs read are still in L2
+    const int r0 = (gridDim.y - 1 - blockIdx.y) * kSlab;
     const int lane = threadIdx.x & 31;
     const bool vec = (cols % 4 == 0) && c + 3 < cols;
     double cs0 = 0, cs1 = 0, cs2 = 0, cs3 = 0;
