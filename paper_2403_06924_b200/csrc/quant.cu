@@ -1807,14 +1807,16 @@ void launch_select_rows(const SelectArgs& a, cudaStream_t s) {
         }
         return;
     }
-    if (a.fix_mode) k_fix_rows<<<grid_rows(a.rows), kThreads, 0, s>>>(a);
+    // the fix-up grid: two CTAs per SM; it exits at once in the common case (the
+    // retained maximum is the tensor maximum), a full-size grid only paid its launch
+    if (a.fix_mode) k_fix_rows<<<a.rows < 2 * kNumSMs ? a.rows : 2 * kNumSMs, kThreads, 0, s>>>(a);
     else if (a.rounding == kNearest) k_select_rows<kNearest><<<grid_rows(a.rows), kThreads, 0, s>>>(a);
     else k_select_rows<kFloor><<<grid_rows(a.rows), kThreads, 0, s>>>(a);
 }
 
 void launch_select_cols_T(const SelectArgs& a, cudaStream_t s) {
     if (a.fix_mode) {
-        k_fix_cols_T<<<grid_rows(a.cols), kThreads, 0, s>>>(a);
+        k_fix_cols_T<<<a.cols < 2 * kNumSMs ? a.cols : 2 * kNumSMs, kThreads, 0, s>>>(a);
         return;
     }
     if (a.rows >= 256 && (a.ldq % 16) == 0) {
