@@ -1,4 +1,5 @@
-# Same-box A/B of two library builds: the in-tree one and paper_2403_06924_b200/lib/ab/ (XG_LIB_PATH):
+# Same-box A/B of two library builds: the in-tree one and a copy of the baseline build placed in
+# paper_2403_06924_b200/lib/ab/ beforehand (loaded through XG_LIB_PATH; delete it afterwards):
 # kernel durations from an ncu launch list of tools/c3_once.py, then the bench at SHAPES.
 B=paper_2403_06924_b200/lib/ab/libxigemm_b200.so
 for rep in 1 2; do
