@@ -364,6 +364,33 @@ def test_deferred_mean_fallback_widened():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("seed", range(32))
+def test_pipeline_vs_oracle_random_midsize(oracle, seed):
+    """Random mid-size shapes (rows >= 256, K in [512, 2200], ragged N - some not
+    a multiple of 4, which sends the GEMMs to the 1-CTA kernels) and random
+    configurations (bits, rounding, scheme, policy, threshold, C / alpha / beta):
+    the register-row, column-tile and K1-B cluster kernels with both rounding
+    modes on shapes the fixed cases do not hit, bit for bit against the oracle."""
+    rng = np.random.default_rng(4000 + seed)
+    m = int(rng.integers(256, 700))
+    k = int(rng.integers(128, 550)) * 4
+    n = int(rng.integers(256, 1100))
+    a = ol.random_dense(m, k, seed * 2 + 31, -4, 4)
+    b = ol.random_dense(k, n, seed * 2 + 32, -4, 4)
+    a[int(rng.integers(0, m)), int(rng.integers(0, k))] = 30.0
+    cm = ol.random_dense(m, n, seed + 97, -1, 1)
+    scheme, pol = int(rng.integers(0, 2)), int(rng.integers(0, 2))
+    c = ol.cfg(bits=int(rng.choice([4, 8])), threshold=float(10 ** rng.uniform(-2.3, -0.5)) if pol == 0 else
+               float(10 ** rng.uniform(2.0, 4.5)), density_limit=float(rng.uniform(0.05, 1.0)), scheme=scheme,
+               policy=pol, rounding=int(rng.integers(0, 2)))
+    rc, ref, orep = oracle.xigemm(a, b, c=cm, alpha=1.25, beta=-0.5, config=c)
+    assert rc == 0
+    rep = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                    torch.from_numpy(cm).cuda(), 1.25, -0.5, cfg_from(c))
+    assert beq(rep.result, ref), (m, k, n, c.scheme, c.policy, c.bits, c.rounding)
+    assert (rep.density_a, rep.density_b, int(rep.path)) == (orep.density_a, orep.density_b, orep.path)
+
+
 @pytest.mark.parametrize("shape", [(129, 2052, 300), (64, 8192, 96), (300, 1024, 1028), (40, 4096, 2048),
                                    (257, 2048, 1000), (300, 1500, 516), (260, 700, 260)])
 def test_pipeline_vs_oracle_wide(oracle, shape):
