@@ -391,6 +391,28 @@ def test_pipeline_vs_oracle_random_midsize(oracle, seed):
     assert (rep.density_a, rep.density_b, int(rep.path)) == (orep.density_a, orep.density_b, orep.path)
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_pipeline_vs_oracle_random_longk(oracle, seed):
+    """Random long-K shapes (K in [4100, 16384]): the 5-CTA and 256-thread
+    register-row kernels, K1-B in clusters of up to 4 or the two-kernel path
+    past K = 8192, the 8-line CSR strips' neighbourhood - bit for bit."""
+    rng = np.random.default_rng(5000 + seed)
+    m = int(rng.integers(256, 420))
+    k = int(rng.integers(1025, 4097)) * 4
+    n = int(rng.integers(256, 520))
+    a = ol.random_dense(m, k, seed * 2 + 51, -4, 4)
+    b = ol.random_dense(k, n, seed * 2 + 52, -4, 4)
+    scheme, pol = int(rng.integers(0, 2)), int(rng.integers(0, 2))
+    c = ol.cfg(bits=8, threshold=float(10 ** rng.uniform(-2.3, -0.7)) if pol == 0 else
+               float(10 ** rng.uniform(2.5, 5.0)), density_limit=float(rng.uniform(0.05, 1.0)), scheme=scheme,
+               policy=pol, rounding=int(rng.integers(0, 2)))
+    rc, ref, orep = oracle.xigemm(a, b, config=c)
+    assert rc == 0
+    rep = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), cfg=cfg_from(c))
+    assert beq(rep.result, ref), (m, k, n, c.scheme, c.policy, c.rounding)
+    assert (rep.density_a, rep.density_b, int(rep.path)) == (orep.density_a, orep.density_b, orep.path)
+
+
 @pytest.mark.parametrize("shape", [(129, 2052, 300), (64, 8192, 96), (300, 1024, 1028), (40, 4096, 2048),
                                    (257, 2048, 1000), (300, 1500, 516), (260, 700, 260)])
 def test_pipeline_vs_oracle_wide(oracle, shape):
