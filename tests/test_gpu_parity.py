@@ -395,7 +395,7 @@ def test_pipeline_vs_oracle_random_midsize(oracle, seed):
 def test_pipeline_vs_oracle_random_longk(oracle, seed):
     """Random long-K shapes (K in [4100, 16384]): the 5-CTA and 256-thread
     register-row kernels, K1-B in clusters of up to 4 or the two-kernel path
-    past K = 8192, the 8-line CSR strips' neighbourhood - bit for bit."""
+    past K = 8192 - bit for bit against the oracle."""
     rng = np.random.default_rng(5000 + seed)
     m = int(rng.integers(256, 420))
     k = int(rng.integers(1025, 4097)) * 4
