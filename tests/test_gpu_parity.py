@@ -653,3 +653,44 @@ def test_out_argument_contract(oracle):
     cn = c.cpu().numpy()
     out, _ = xg.xigemm_host(an, bn, cn, 1.5, -0.75, cfg=cfg, out=cn)  # in place on the host too
     assert beq(out, want)
+
+
+def _boundary_matrix(rows, cols, seed, axis):
+    """Uniform values in (-126, 126) with the slice maximum 127 (scale exactly 1.0
+    along `axis`) and, in every slice, values on and next to the rounding
+    boundaries of both modes: integers, halves and their float neighbours."""
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(-126, 126, (rows, cols)).astype(np.float32)
+    sp = [0.0, 1.0, -1.0, 2.5, -2.5, 3.0, -3.0, 0.5, -0.5, 126.5, -126.5, 64.0, -64.0]
+    sp += [float(np.nextafter(np.float32(v), np.float32(t))) for v in (3.0, 2.5, -2.5, 0.5, 126.0)
+           for t in (-1000.0, 1000.0)]
+    sp = np.array(sp, np.float32)
+    if axis == 1:  # per-row slices: columns 0..len(sp) of every row
+        a[:, 0] = 127.0
+        a[:, 1:1 + sp.size] = sp
+    else:          # per-column slices
+        a[0, :] = 127.0
+        a[1:1 + sp.size, :] = sp[:, None]
+    return a
+
+
+@pytest.mark.parametrize("shape", [(300, 2048, 300), (260, 8192, 256), (256, 1024, 260)])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_pipeline_quantisers_at_rounding_boundaries(oracle, shape, rnd):
+    """Aq and Bq of the pipeline (register-row kernel, K1-B cluster kernel) on
+    values exactly on and one ulp beside the Nearest ties and the Floor integer
+    boundaries, with scales of exactly 1.0: every fast-path rejection must reach
+    the reference's llround / nudged-truncation result (quantize.cpp:13-24)."""
+    m, k, n = shape
+    a = _boundary_matrix(m, k, m + k, axis=1)
+    b = _boundary_matrix(k, n, k + n, axis=0)
+    c = ol.cfg(bits=8, threshold=0.03, density_limit=0.9, scheme=1, policy=0, rounding=rnd)
+    rep, d = xg.xigemm_dump(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), cfg_from(c))
+    rc, aq, la = oracle.quantize(a, 8, 1, rnd)
+    assert rc == 0 and beq(d["aq"], aq) and beq(d["aq_scales"], la)
+    rc, bq, lb = oracle.quantize(b, 8, 2, rnd)
+    assert rc == 0 and beq(d["bq"], bq) and beq(d["bq_scales"], lb)
+    rc, dd = oracle.dump(a, b, c)
+    assert rc == 0 and beq(d["raq"], dd["raq"]) and beq(d["rbq"], dd["rbq"])
+    assert beq(d["a_red"], dd["a_red"]) and beq(d["b_red"], dd["b_red"])
+    assert beq(rep.result, dd["result"])
