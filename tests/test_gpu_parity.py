@@ -694,3 +694,26 @@ def test_pipeline_quantisers_at_rounding_boundaries(oracle, shape, rnd):
     assert rc == 0 and beq(d["raq"], dd["raq"]) and beq(d["rbq"], dd["rbq"])
     assert beq(d["a_red"], dd["a_red"]) and beq(d["b_red"], dd["b_red"])
     assert beq(rep.result, dd["result"])
+
+
+@pytest.mark.parametrize("k", [700, 1024, 2048, 8192, 12000])
+@pytest.mark.parametrize("rnd", [0, 1])
+def test_vectorwise_nonfinite_rejected_every_quantiser(k, rnd):
+    """A NaN or inf in A or B under VectorWise (register-row kernels, K1-B
+    cluster kernels of every short-K shape, the two-kernel path past K = 8192),
+    both rounding modes: the call is rejected (pipeline.cpp:50-52) and the next
+    finite call on the same buffers is still exact."""
+    m, n = 300, 264
+    cfg = xg.XigemmConfig(threshold=0.03, scheme=xg.QuantScheme.VectorWise, policy=xg.ReductionPolicy.AvgRule,
+                          rounding=xg.RoundingMode(rnd))
+    a = torch.from_numpy(ol.random_dense(m, k, k + 1, -2, 2)).cuda()
+    b = torch.from_numpy(ol.random_dense(k, n, k + 2, -2, 2)).cuda()
+    good = xg.xigemm(a, b, cfg=cfg).result.clone()
+    for t, (i, j), v in ((a, (m // 2, k - 1), float("nan")), (b, (k // 3, n // 2), float("inf")),
+                         (b, (k - 1, 0), float("-inf")), (a, (0, 0), float("inf"))):
+        old = float(t[i, j])
+        t[i, j] = v
+        with pytest.raises(xg.InvalidArgument):
+            xg.xigemm(a, b, cfg=cfg)
+        t[i, j] = old
+    assert beq(xg.xigemm(a, b, cfg=cfg).result, good)
