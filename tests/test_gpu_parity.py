@@ -717,3 +717,24 @@ def test_vectorwise_nonfinite_rejected_every_quantiser(k, rnd):
             xg.xigemm(a, b, cfg=cfg)
         t[i, j] = old
     assert beq(xg.xigemm(a, b, cfg=cfg).result, good)
+
+
+@pytest.mark.parametrize("shape", [(1024, 1536, 516), (300, 1024, 260)])
+def test_host_entry_all_configurations(shape):
+    """xg_xigemm_host - the overlapped row-chunk schedule (VectorWise, M >= 1024)
+    or upload-then-pipeline otherwise - against the device-pointer call for
+    every scheme x policy x rounding, with C / alpha / beta."""
+    m, k, n = shape
+    a = ol.random_dense(m, k, m + 3, -3, 3)
+    b = ol.random_dense(k, n, n + 4, -3, 3)
+    c = ol.random_dense(m, n, 11, -1, 1)
+    for scheme in (xg.QuantScheme.VectorWise, xg.QuantScheme.PerTensor):
+        for pol in (xg.ReductionPolicy.AvgRule, xg.ReductionPolicy.MinRule):
+            for rnd in (xg.RoundingMode.Nearest, xg.RoundingMode.Floor):
+                cfg = xg.XigemmConfig(threshold=0.05 if pol == xg.ReductionPolicy.AvgRule else 3000.0,
+                                      density_limit=0.5, scheme=scheme, policy=pol, rounding=rnd)
+                res, rep = xg.xigemm_host(a, b, c, 1.5, -0.25, cfg=cfg)
+                ref = xg.xigemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), torch.from_numpy(c).cuda(),
+                                1.5, -0.25, cfg)
+                assert beq(res, ref.result), (shape, scheme, pol, rnd)
+                assert (rep.density_a, rep.density_b, rep.path) == (ref.density_a, ref.density_b, int(ref.path))
